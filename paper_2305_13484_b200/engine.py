@@ -1,0 +1,265 @@
+"""The temporally fused decode loop -- drop-in for reference engine.py:24-207.
+
+Same public surface (``preprocess``, ``FusionStream`` with ``now``,
+``iteration_index``, ``layout``, ``active``, ``eos_at``, ``phase``,
+``events``, ``pending``, ``next_ready_time``, ``try_fuse_pending``,
+``step_iteration``, ``finished_all``; ``run_fusion``) and the same schedule:
+admission only at iteration boundaries (inclusive tie, FIFO by (ready, id)),
+an atomic iteration gives every fused request one token, then evict -> trim
+-> optional Alg.1 shuffle; idle gaps are skipped.
+
+What is new underneath:
+
+* an ``executor`` hook.  ``None`` is the pure schedule (bit-exact with the
+  reference; pinned by tests/test_engine_golden.py).  ``CudaExecutor``
+  (executor.py) runs every iteration as a real decode step on the B200
+  through the C-ABI and every shuffle plan as the K10 compaction kernel.
+* two clocks.  ``clock="cost"`` advances ``now`` with the reference cost
+  model (parity mode: identical schedule whatever the device does).
+  ``clock="device"`` advances it with the CUDA-event duration of the real
+  step/shuffle (performance mode: Poisson arrivals against measured time).
+* O(1) host bookkeeping per row.  The reference pays a
+  ``dataclasses.replace`` per row per iteration (core.py:122, ~5.6 us).
+  Stop lengths are known at admission, so here ``current_iteration`` is
+  derived as ``iteration_index - base`` and finishing requests are found in
+  a per-iteration bucket; token events are recorded as one snapshot per
+  iteration and expanded only when ``events`` is read.
+"""
+
+from __future__ import annotations
+
+from collections.abc import MutableMapping
+
+from .buffer import BufferLayout, apply_shuffle, plan_shuffle
+from .core import Context, Phase, Request, RuntimeInfo, advance_phase, stop_iteration
+from .cost import CostParams, TPConfig, iteration_time, shuffle_time
+from .errors import EmptyStream, InvalidParam
+from .trace import EventKind, Trace, TraceEvent
+
+_TOKEN = EventKind.TOKEN_GENERATED
+
+
+def preprocess(request: Request, params: CostParams, now: float) -> Context:
+    """A received request becomes a fusion-ready context ``preprocess_ms``
+    later; no slot, no tokens yet."""
+    info = RuntimeInfo(request.request_id, None, request.batch_size * params.request_bytes,
+                       "gpu", request.max_output_length, 0)
+    return Context(request.request_id, now + params.preprocess_ms, info)
+
+
+class _ActiveTable(MutableMapping):
+    """``rid -> RuntimeInfo`` in fusion order, materialised on access.
+
+    Internally a row is [memory_offset, tensor_size, device_type,
+    max_output_length, base] with current_iteration = iteration_index - base.
+    """
+
+    __slots__ = ("_s", "_rows")
+
+    def __init__(self, stream: "FusionStream"):
+        self._s = stream
+        self._rows: dict = {}
+
+    def __getitem__(self, rid):
+        r = self._rows[rid]
+        return RuntimeInfo(rid, r[0], r[1], r[2], r[3], self._s.iteration_index - r[4])
+
+    def __setitem__(self, rid, info: RuntimeInfo):
+        base = self._s.iteration_index - info.current_iteration
+        self._rows[rid] = [info.memory_offset, info.tensor_size, info.device_type,
+                           info.max_output_length, base]
+        self._s._schedule_finish(rid, base, info.max_output_length)
+
+    def __delitem__(self, rid):
+        del self._rows[rid]
+
+    def __iter__(self):
+        return iter(self._rows)
+
+    def __len__(self):
+        return len(self._rows)
+
+    def __contains__(self, rid):
+        return rid in self._rows
+
+    def __repr__(self):
+        return f"_ActiveTable({dict(self.items())!r})"
+
+
+class FusionStream:
+    """Mutable state of one fused serving stream."""
+
+    def __init__(self, requests, params: CostParams, tp: TPConfig,
+                 shuffle_enabled: bool = True, record_tokens: bool = True,
+                 slot_capacity: int | None = None, *, executor=None, clock: str = "cost"):
+        if clock not in ("cost", "device"):
+            raise InvalidParam(f"clock must be 'cost' or 'device', got {clock!r}")
+        if clock == "device" and executor is None:
+            raise InvalidParam("clock='device' needs an executor")
+        self.params = params
+        self.tp = tp
+        self.shuffle_enabled = shuffle_enabled
+        self.record_tokens = record_tokens
+        self.executor = executor
+        self.clock = clock
+        self.now = 0.0
+        self.iteration_index = 0
+        self.layout = BufferLayout(capacity=slot_capacity)
+        self.active = _ActiveTable(self)
+        self.eos_at: dict = {}
+        self.phase: dict = {}
+        self.requests: dict = {}
+        self._ev: list = []
+        self._tok: list = []          # (position in _ev, time, rid snapshot, k)
+        self._base: dict = {}         # rid -> base, kept after eviction
+        self._finish_at: dict = {}    # iteration index -> [rid] in fusion order
+        self._finish_of: dict = {}    # rid -> iteration index
+        self.device_ms: list = []     # per-iteration device time (executor runs)
+
+        pending = []
+        for req in sorted(requests, key=lambda r: (r.arrival_time, r.request_id)):
+            rid = req.request_id
+            self.requests[rid] = req
+            self.phase[rid] = Phase.RECEIVED
+            self._emit(req.arrival_time, EventKind.ARRIVED, rid)
+            self.phase[rid] = advance_phase(Phase.RECEIVED, Phase.PREPROCESSING)
+            self._emit(req.arrival_time, EventKind.PREPROCESS_START, rid)
+            ctx = preprocess(req, params, req.arrival_time)
+            self._emit(ctx.ready_time, EventKind.PREPROCESS_DONE, rid)
+            self.eos_at[rid] = req.actual_output_length
+            pending.append(ctx)
+        pending.sort(key=lambda c: (c.ready_time, c.request_id))
+        self.pending: list = pending
+        self._next_pending = 0
+
+    # -- events ------------------------------------------------------------
+    def _emit(self, time, kind, rid=None, value=None):
+        self._ev.append(TraceEvent(time, kind, rid, value))
+
+    @property
+    def events(self) -> list:
+        """Flat event list; per-iteration token snapshots expanded in place."""
+        if self._tok:
+            out = []
+            prev = 0
+            base = self._base
+            for pos, t, rids, k in self._tok:
+                out.extend(self._ev[prev:pos])
+                out.extend([TraceEvent(t, _TOKEN, rid, k - base[rid]) for rid in rids])
+                prev = pos
+            out.extend(self._ev[prev:])
+            self._ev = out
+            self._tok = []
+        return self._ev
+
+    # -- queue ---------------------------------------------------------------
+    def next_ready_time(self):
+        if self._next_pending >= len(self.pending):
+            return None
+        return self.pending[self._next_pending].ready_time
+
+    def _schedule_finish(self, rid, base, max_out):
+        old = self._finish_of.pop(rid, None)
+        if old is not None:
+            self._finish_at[old].remove(rid)
+        at = base + stop_iteration(self.eos_at[rid], max_out) - 1
+        self._finish_of[rid] = at
+        self._finish_at.setdefault(at, []).append(rid)
+        self._base[rid] = base
+
+    def try_fuse_pending(self) -> int:
+        """Admit, in FIFO order, every context ready at or before ``now``."""
+        n = 0
+        pend = self.pending
+        while self._next_pending < len(pend) and pend[self._next_pending].ready_time <= self.now:
+            ctx = pend[self._next_pending]
+            self._next_pending += 1
+            rid = ctx.request_id
+            slot = self.layout.fuse_request(rid, ctx.runtime.tensor_size)
+            rt = ctx.runtime
+            self.active[rid] = RuntimeInfo(rid, slot, rt.tensor_size, rt.device_type,
+                                           rt.max_output_length, rt.current_iteration)
+            ph = advance_phase(self.phase[rid], Phase.READY_FOR_FUSION)
+            self.phase[rid] = advance_phase(ph, Phase.RUNNING)
+            self._emit(self.now, EventKind.FUSED, rid)
+            if self.executor is not None:
+                self.executor.on_fuse(rid, slot, self.requests.get(rid))
+            n += 1
+        return n
+
+    # -- the atomic iteration --------------------------------------------------
+    def step_iteration(self) -> None:
+        if not self.active:
+            raise EmptyStream("no fused requests to iterate")
+        lay = self.layout
+        dev = None
+        if self.executor is not None:
+            dev = self.executor.run_iteration(self)
+            if dev is not None:
+                self.device_ms.append(dev)
+        if self.clock == "device":
+            duration = dev
+        else:
+            duration = iteration_time(len(self.active), lay.live_bytes(), self.params, self.tp)
+        self.now += duration
+        now = self.now
+        if self.record_tokens:
+            self._tok.append((len(self._ev), now, tuple(self.active._rows), self.iteration_index + 1))
+
+        done = self._finish_at.pop(self.iteration_index, ())
+        rows = self.active._rows
+        for rid in done:
+            slot = lay.per_request_offset[rid]
+            lay.evict_request(rid)
+            del rows[rid]
+            del self._finish_of[rid]
+            self.phase[rid] = advance_phase(self.phase[rid], Phase.FINISHED)
+            self._emit(now, EventKind.EVICTED, rid)
+            if self.executor is not None:
+                self.executor.on_evict(rid, slot)
+        self._emit(now, EventKind.ITERATION_COMPLETED, None, duration)
+        self.iteration_index += 1
+
+        if self.shuffle_enabled:
+            lay.trim_boundaries()
+            if done and lay.has_interior_holes():
+                plan = plan_shuffle(lay)
+                if plan.moves:
+                    apply_shuffle(lay, plan)
+                    dev_sh = None
+                    if self.executor is not None:
+                        dev_sh = self.executor.on_shuffle(plan)
+                    if self.clock == "device":
+                        self.now += dev_sh
+                    else:
+                        self.now += shuffle_time(plan.total_bytes_moved, self.params)
+                    self._emit(self.now, EventKind.SHUFFLE_EXECUTED, None, plan.total_bytes_moved)
+        else:
+            lay.trim_leading()
+
+    def finished_all(self) -> bool:
+        return not self.active and self._next_pending >= len(self.pending)
+
+
+def run_fusion(requests, params: CostParams, tp: TPConfig | None = None,
+               shuffle_enabled: bool = True, record_tokens: bool = True, *,
+               executor=None, clock: str = "cost") -> Trace:
+    """Serve every request to completion on one fused stream."""
+    stream = FusionStream(requests, params, tp or TPConfig(), shuffle_enabled=shuffle_enabled,
+                          record_tokens=record_tokens, executor=executor, clock=clock)
+    drive(stream)
+    trace = Trace("fusion" if shuffle_enabled else "fusion_noshuffle", stream.events)
+    trace.sort()
+    return trace
+
+
+def drive(stream: FusionStream) -> FusionStream:
+    """The loop of engine.py:199-203, idle jump included."""
+    while not stream.finished_all():
+        if not stream.active:
+            stream.now = max(stream.now, stream.next_ready_time())
+        stream.try_fuse_pending()
+        stream.step_iteration()
+    if stream.executor is not None:
+        stream.executor.on_drain(stream)
+    return stream
