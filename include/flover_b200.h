@@ -1,0 +1,167 @@
+/*
+ * flover_b200.h -- C-ABI of the B200 fused decode loop (Flover, arXiv 2305.13484).
+ *
+ * The reference (fusionsim, /root/reference/pkg/src/fusionsim) is a pure-Python
+ * simulator with no FFI; its fused loop *models* each device action.  Each entry
+ * point below is the device realisation of one modelled action and sits directly
+ * under the Python call that used to model it (see INTEGRATION.md for the
+ * ctypes binding the drop-in engine uses):
+ *
+ *   fl_create / fl_destroy    -- FusionStream construction / teardown
+ *                                (engine.py:48-85); device state is caller-owned.
+ *   fl_step                   -- one atomic iteration FusionStream.step_iteration
+ *                                (engine.py:128-160): every fused request gains one
+ *                                token; the reference only charges
+ *                                cost.iteration_time (cost.py:89-109) for it.
+ *                                Newly fused requests (try_fuse_pending,
+ *                                engine.py:97-124; preprocess engine.py:24-42) enter
+ *                                as PREFILL rows of the same launch sequence.
+ *   fl_shuffle                -- apply_shuffle (buffer.py:261-278) on the KV pool:
+ *                                the move list of plan_shuffle (buffer.py:226-258);
+ *                                the reference only charges shuffle_time
+ *                                (cost.py:119-123).
+ *   fl_comm_*                 -- the tensor-parallel communicator the reference
+ *                                models as TPConfig + comm_time (cost.py:26-33,73-86).
+ *
+ * Conventions: every pointer to device memory is owned by the caller (PyTorch);
+ * the library never allocates or frees caller memory.  All calls are stream-
+ * ordered and non-blocking unless stated.  Return 0 on success, a negative
+ * FL_E* code on failure (fl_last_error() has the message); no C++ exception
+ * crosses the ABI.  One host thread per handle.
+ */
+#ifndef FLOVER_B200_H
+#define FLOVER_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FL_ABI_VERSION 1
+
+enum fl_status {
+  FL_OK = 0,
+  FL_EINVAL = -1,     /* -> errors.InvalidParam      */
+  FL_ECAPACITY = -2,  /* -> errors.CapacityExceeded  */
+  FL_ESTALE = -3,     /* -> errors.StalePlan         */
+  FL_ECUDA = -4,      /* -> errors.DeviceError       */
+  FL_ENCCL = -5       /* -> errors.DeviceError       */
+};
+
+enum fl_family {
+  FL_FAMILY_GPT2 = 0, /* sequential pre-LN blocks, learned positions, GELU MLP   */
+  FL_FAMILY_GPTJ = 1, /* parallel residual, 1 LN, interleaved rotary (rotary_dim) */
+  FL_FAMILY_NEOX = 2  /* parallel residual, 2 LNs, rotate-half rotary             */
+};
+
+enum fl_dtype { FL_DTYPE_F32 = 0, FL_DTYPE_BF16 = 1 };
+
+enum fl_row_kind {
+  FL_ROW_DECODE = 0,  /* fused request: input token/pos from per-request state (or explicit) */
+  FL_ROW_PREFILL = 1, /* prompt token of a request fused at this boundary (no LM head)       */
+  FL_ROW_ORPHAN = 2   /* evicted slot still inside the live window (fusion_noshuffle):       */
+                      /* computed over stale KV, output discarded             */
+};
+
+/* Per-layer weight slots of fl_model_desc.layers (row-major [out, in] matrices). */
+enum fl_layer_tensor {
+  FL_W_LN1_G = 0, FL_W_LN1_B, FL_W_LN2_G, FL_W_LN2_B,
+  FL_W_QKV,    /* [3 * Hl * hd, d]  rows: q heads, k heads, v heads (this rank) */
+  FL_W_QKV_B,  /* [3 * Hl * hd] or NULL                                         */
+  FL_W_O,      /* [d, Hl * hd]  row-parallel slice                              */
+  FL_W_O_B,    /* [d] or NULL (added once, after the all-reduce)                */
+  FL_W_FC,     /* [Fl, d]                                                       */
+  FL_W_FC_B,   /* [Fl]                                                          */
+  FL_W_PROJ,   /* [d, Fl]                                                       */
+  FL_W_PROJ_B, /* [d]                                                           */
+  FL_W_LAYER_COUNT
+};
+
+typedef struct fl_model_desc {
+  int32_t family, dtype;
+  int32_t n_layer, d_model, n_head, head_dim, d_ff, vocab, max_pos, rotary_dim;
+  float ln_eps;
+  int32_t tp_rank, tp_size;    /* heads, FFN columns and vocab are split tp_size ways */
+  const void* wte;             /* [vocab, d] token embedding (replicated)             */
+  const void* wpe;             /* [max_pos, d] learned positions or NULL              */
+  const void* lnf_g;
+  const void* lnf_b;
+  const void* w_lm;            /* [ceil(vocab/tp), d] this rank's vocab slice          */
+  const void* b_lm;            /* [ceil(vocab/tp)] or NULL                             */
+  const void* const* layers;   /* host array [n_layer * FL_W_LAYER_COUNT]              */
+} fl_model_desc;
+
+typedef struct fl_pool_desc {
+  int32_t pool_slots;       /* C: physical KV slots; logical slot s lives at s % C       */
+  int32_t max_seq;          /* S: positions per slot (input_len + max_output - 1)        */
+  int32_t max_rows;         /* rows per fused iteration (decode + orphan + prefill)      */
+  int32_t state_slots;      /* R: per-request state ring, indexed rid % R                */
+  int32_t max_new_tokens;   /* token history length per request                         */
+  int32_t use_tensor_cores; /* 1: tcgen05 GEMMs (bf16 only); 0: SIMT FFMA GEMMs          */
+  void* kv;                 /* [L][C][2][Hl][S][hd] in the model dtype                   */
+  int32_t* req_tok;         /* [R] next input token of a running request                 */
+  int32_t* req_pos;         /* [R] position of that token                                */
+  int32_t* req_ngen;        /* [R] tokens generated so far                               */
+  int32_t* tok_hist;        /* [R][max_new_tokens] generated token ids                   */
+  void* workspace;          /* fl_workspace_bytes() bytes, 256-B aligned                 */
+  size_t workspace_bytes;
+} fl_pool_desc;
+
+/* One row of a fused iteration.  pos/tok < 0 on a DECODE row mean "read the
+ * request's state" (the steady-state case: the host uploads nothing). */
+typedef struct fl_row {
+  int32_t slot;   /* physical KV slot                               */
+  int32_t rid;    /* request id (state ring index = rid % R), -1 orphan */
+  int32_t pos;    /* position of the input token, or -1              */
+  int32_t tok;    /* input token id, or -1                            */
+  int32_t kind;   /* fl_row_kind                                     */
+  int32_t ctx;    /* ORPHAN only: stale context length to attend over */
+} fl_row;
+
+typedef struct fl_handle fl_handle;
+
+int fl_abi_version(void);
+const char* fl_last_error(void);
+
+/* Bytes of scratch the caller must provide in fl_pool_desc.workspace. */
+size_t fl_workspace_bytes(const fl_model_desc* model, const fl_pool_desc* pool);
+
+int fl_create(const fl_model_desc* model, const fl_pool_desc* pool, fl_handle** out);
+int fl_destroy(fl_handle* h);
+
+/* Tensor parallelism: rank 0 calls fl_comm_unique_id, the id travels to every
+ * rank (torch.distributed broadcast), then all ranks call fl_comm_init. */
+int fl_comm_unique_id(void* out_128_bytes);
+int fl_comm_init(fl_handle* h, const void* id_128_bytes, int rank, int world);
+
+/* One fused iteration over rows[0..n_rows): rows [0, n_dec) are the live window
+ * (DECODE / ORPHAN, window order), rows [n_dec, n_rows) are PREFILL rows.
+ * rows is a HOST array, uploaded only when rows_changed != 0.  Greedy tokens of
+ * DECODE rows update the per-request state and tok_hist on the device (no D2H).
+ * logits_out (device fp32 [n_dec, vocab_local], may be NULL) receives the LM-head
+ * output for parity checks. */
+int fl_step(fl_handle* h, const fl_row* rows, int n_rows, int n_dec, int rows_changed,
+            float* logits_out, void* cuda_stream);
+
+/* K10: moves is a HOST array of n triples (src_slot, dst_slot, ctx_len) of
+ * physical slots; copies the live KV prefix [0, ctx_len) of every
+ * (layer, K/V, head) from src to dst in one launch.  Slots are disjoint. */
+int fl_shuffle(fl_handle* h, const int32_t* moves, int n, void* cuda_stream);
+
+/* Number of kernels fl_step / fl_shuffle launched since fl_create. */
+int64_t fl_kernel_launches(const fl_handle* h);
+
+/* Diagnostic entry for kernel-level parity tests: one projection GEMM
+ * out[M,N] (=|+=) X[M,K] . W[N,K]^T + bias through the same kernels fl_step
+ * uses (use_tc: 1 tcgen05, 0 SIMT).  epi: 0 store(dtype) 1 gelu(dtype)
+ * 2 accumulate(f32) 3 store(f32).  workspace: >= fl_gemm_workspace_bytes(). */
+size_t fl_gemm_workspace_bytes(void);
+int fl_gemm(const void* x, int ldx, const void* w, const void* bias, void* out, int ldo, int M,
+            int N, int K, int epi, int dtype, int use_tc, void* workspace, void* cuda_stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLOVER_B200_H */

@@ -1,0 +1,428 @@
+// C-ABI of the fused decode loop (include/flover_b200.h).
+//
+// fl_step executes one atomic Flover iteration (reference engine.py:128-160)
+// over the rows of the live window plus the prompt rows of requests fused at
+// this boundary:
+//
+//   K1 embed -> per layer { K2 LN -> K3 QKV GEMM -> rotary + KV append ->
+//   K4 attention -> K5 attn-out GEMM [-> NCCL all-reduce] -> K2 LN ->
+//   K6 FFN-up GEMM + GELU -> K7 FFN-down GEMM [-> NCCL all-reduce] }
+//   -> K2 final LN -> K8 LM head GEMM -> greedy argmax [-> NCCL max] -> K9 state.
+//
+// Everything is stream-ordered on the caller's stream; nothing blocks the
+// host.  Tensor parallelism follows Megatron: heads and FFN columns are
+// column-parallel, attn-out and FFN-down row-parallel (one all-reduce after
+// each, as the north star prescribes), vocab-parallel LM head with a packed
+// (logit, index) max-reduce for the greedy token.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "gemm_tc.cuh"
+#include "kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define FL_CUDA(call)                                                                    \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess) return fail(FL_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+// ---- NCCL resolved at run time from the copy PyTorch already loaded -------
+struct Nccl {
+  void* lib = nullptr;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*getErrorString)(ncclResult_t) = nullptr;
+  bool load() {
+    if (lib) return true;
+    lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) return false;
+    getUniqueId = (decltype(getUniqueId))dlsym(lib, "ncclGetUniqueId");
+    commInitRank = (decltype(commInitRank))dlsym(lib, "ncclCommInitRank");
+    allReduce = (decltype(allReduce))dlsym(lib, "ncclAllReduce");
+    commDestroy = (decltype(commDestroy))dlsym(lib, "ncclCommDestroy");
+    getErrorString = (decltype(getErrorString))dlsym(lib, "ncclGetErrorString");
+    return getUniqueId && commInitRank && allReduce && commDestroy;
+  }
+} g_nccl;
+
+size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+
+}  // namespace
+
+namespace fl {
+std::atomic<int64_t> g_launches{0};
+}
+
+struct fl_handle {
+  fl_model_desc m;
+  fl_pool_desc p;
+  std::vector<const void*> layers;
+  int Hl, Dl, Fl, Vl, Vloc, es, ms;
+  // workspace carve
+  fl_row* rows;
+  int32_t *row_tok, *row_pos, *row_ctx, *moves;
+  float *x, *y, *logits, *att_o, *att_ml;
+  void *h, *h2, *qkv, *q, *a, *f;
+  unsigned long long* keys;
+  fl::TcWorkspace tcws;
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+};
+
+namespace {
+
+struct Carve {
+  size_t off = 0;
+  size_t take(size_t bytes) {
+    size_t o = off;
+    off = align256(off + bytes);
+    return o;
+  }
+};
+
+struct Layout {
+  size_t rows, row_tok, row_pos, row_ctx, moves, x, y, logits, att_o, att_ml, h, h2, qkv, q, a, f, keys,
+      tc, total;
+};
+
+int check_desc(const fl_model_desc* m, const fl_pool_desc* p) {
+  if (!m || !p) return fail(FL_EINVAL, "null descriptor");
+  if (m->family < 0 || m->family > 2) return fail(FL_EINVAL, "bad family %d", m->family);
+  if (m->dtype != FL_DTYPE_F32 && m->dtype != FL_DTYPE_BF16) return fail(FL_EINVAL, "bad dtype");
+  if (m->tp_size < 1 || m->tp_rank < 0 || m->tp_rank >= m->tp_size)
+    return fail(FL_EINVAL, "bad tp rank/size");
+  if (m->n_head % m->tp_size || m->d_ff % m->tp_size)
+    return fail(FL_EINVAL, "heads (%d) and d_ff (%d) must divide by tp (%d)", m->n_head, m->d_ff,
+                m->tp_size);
+  if (m->head_dim != 64 && m->head_dim != 96 && m->head_dim != 128 && m->head_dim != 256)
+    return fail(FL_EINVAL, "head_dim %d unsupported", m->head_dim);
+  if (m->d_model % 64 || m->d_model > 8192) return fail(FL_EINVAL, "d_model %d", m->d_model);
+  if (p->pool_slots < 1 || p->max_seq < 1 || p->max_rows < 1 || p->state_slots < 1)
+    return fail(FL_EINVAL, "bad pool sizes");
+  if (p->use_tensor_cores && m->dtype != FL_DTYPE_BF16)
+    return fail(FL_EINVAL, "tensor-core GEMMs need the bf16 path");
+  return FL_OK;
+}
+
+Layout plan(const fl_model_desc* m, const fl_pool_desc* p) {
+  const int es = m->dtype == FL_DTYPE_BF16 ? 2 : 4;
+  const int Hl = m->n_head / m->tp_size, Dl = Hl * m->head_dim, Fl = m->d_ff / m->tp_size;
+  const int Vl = (m->vocab + m->tp_size - 1) / m->tp_size;
+  const size_t Mr = p->max_rows, Md = p->pool_slots < p->max_rows ? p->pool_slots : p->max_rows;
+  const int ms = fl::attn_max_splits(p->max_seq);
+  const size_t d = m->d_model;
+  Carve c;
+  Layout L;
+  L.rows = c.take(Mr * sizeof(fl_row));
+  L.row_tok = c.take(Mr * 4);
+  L.row_pos = c.take(Mr * 4);
+  L.row_ctx = c.take(Mr * 4);
+  L.moves = c.take(size_t(p->pool_slots) * 3 * 4 + 16);
+  L.x = c.take(Mr * d * 4);
+  L.y = c.take(Mr * d * 4);
+  L.logits = c.take(Md * Vl * 4);
+  L.att_o = c.take(Mr * Hl * ms * m->head_dim * 4);
+  L.att_ml = c.take(Mr * Hl * ms * 2 * 4);
+  L.h = c.take(Mr * d * es);
+  L.h2 = c.take(m->family == FL_FAMILY_NEOX ? Mr * d * es : 0);
+  L.qkv = c.take(Mr * 3 * Dl * es);
+  L.q = c.take(Mr * Dl * es);
+  L.a = c.take(Mr * Dl * es);
+  L.f = c.take(Mr * Fl * es);
+  L.keys = c.take(Md * 8);
+  const int nmax = (3 * Dl > Fl ? 3 * Dl : Fl) > Vl ? (3 * Dl > Fl ? 3 * Dl : Fl) : Vl;
+  const int nmax2 = nmax > (int)d ? nmax : (int)d;
+  L.tc = c.take(p->use_tensor_cores ? fl::tc_workspace_bytes((int)Mr, nmax2) : 0);
+  L.total = c.off;
+  return L;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fl_abi_version(void) { return FL_ABI_VERSION; }
+const char* fl_last_error(void) { return g_err.c_str(); }
+
+size_t fl_workspace_bytes(const fl_model_desc* m, const fl_pool_desc* p) {
+  if (check_desc(m, p)) return 0;
+  return plan(m, p).total;
+}
+
+int fl_create(const fl_model_desc* m, const fl_pool_desc* p, fl_handle** out) {
+  if (!out) return fail(FL_EINVAL, "null out");
+  *out = nullptr;
+  if (int e = check_desc(m, p)) return e;
+  Layout L = plan(m, p);
+  if (!p->workspace || p->workspace_bytes < L.total)
+    return fail(FL_EINVAL, "workspace %zu bytes < required %zu", p->workspace_bytes, L.total);
+  if (!p->kv || !p->req_tok || !p->req_pos || !p->req_ngen || !p->tok_hist)
+    return fail(FL_EINVAL, "null pool pointer");
+  if (!m->layers || !m->wte || !m->lnf_g || !m->lnf_b || !m->w_lm)
+    return fail(FL_EINVAL, "null weight pointer");
+  fl_handle* h = new fl_handle();
+  h->m = *m;
+  h->p = *p;
+  h->layers.assign(m->layers, m->layers + (size_t)m->n_layer * FL_W_LAYER_COUNT);
+  h->m.layers = h->layers.data();
+  h->es = m->dtype == FL_DTYPE_BF16 ? 2 : 4;
+  h->Hl = m->n_head / m->tp_size;
+  h->Dl = h->Hl * m->head_dim;
+  h->Fl = m->d_ff / m->tp_size;
+  h->Vl = (m->vocab + m->tp_size - 1) / m->tp_size;
+  h->Vloc = m->vocab - m->tp_rank * h->Vl < h->Vl ? m->vocab - m->tp_rank * h->Vl : h->Vl;
+  h->ms = fl::attn_max_splits(p->max_seq);
+  char* w = static_cast<char*>(p->workspace);
+  h->rows = (fl_row*)(w + L.rows);
+  h->row_tok = (int32_t*)(w + L.row_tok);
+  h->row_pos = (int32_t*)(w + L.row_pos);
+  h->row_ctx = (int32_t*)(w + L.row_ctx);
+  h->moves = (int32_t*)(w + L.moves);
+  h->x = (float*)(w + L.x);
+  h->y = (float*)(w + L.y);
+  h->logits = (float*)(w + L.logits);
+  h->att_o = (float*)(w + L.att_o);
+  h->att_ml = (float*)(w + L.att_ml);
+  h->h = w + L.h;
+  h->h2 = w + L.h2;
+  h->qkv = w + L.qkv;
+  h->q = w + L.q;
+  h->a = w + L.a;
+  h->f = w + L.f;
+  h->keys = (unsigned long long*)(w + L.keys);
+  if (p->use_tensor_cores) {
+    int e = fl::tc_init(&h->tcws, w + L.tc, fl::tc_workspace_bytes(p->max_rows, 0));
+    (void)L;
+    if (e) {
+      delete h;
+      return fail(FL_ECUDA, "tensor-core GEMM init failed: %s", fl::tc_last_error());
+    }
+  }
+  *out = h;
+  return FL_OK;
+}
+
+int fl_destroy(fl_handle* h) {
+  if (!h) return FL_OK;
+  if (h->comm && g_nccl.commDestroy) g_nccl.commDestroy(h->comm);
+  fl::tc_destroy(&h->tcws);
+  delete h;
+  return FL_OK;
+}
+
+int fl_comm_unique_id(void* out) {
+  if (!g_nccl.load()) return fail(FL_ENCCL, "libnccl.so.2 not loadable: %s", dlerror());
+  ncclUniqueId id;
+  ncclResult_t r = g_nccl.getUniqueId(&id);
+  if (r != ncclSuccess) return fail(FL_ENCCL, "ncclGetUniqueId failed (%d)", (int)r);
+  std::memcpy(out, &id, sizeof id);
+  return FL_OK;
+}
+
+int fl_comm_init(fl_handle* h, const void* idp, int rank, int world) {
+  if (!h || !idp) return fail(FL_EINVAL, "null argument");
+  if (world != h->m.tp_size || rank != h->m.tp_rank)
+    return fail(FL_EINVAL, "comm rank/world %d/%d != model tp %d/%d", rank, world, h->m.tp_rank,
+                h->m.tp_size);
+  if (!g_nccl.load()) return fail(FL_ENCCL, "libnccl.so.2 not loadable");
+  ncclUniqueId id;
+  std::memcpy(&id, idp, sizeof id);
+  ncclResult_t r = g_nccl.commInitRank(&h->comm, world, id, rank);
+  if (r != ncclSuccess) return fail(FL_ENCCL, "ncclCommInitRank failed (%d)", (int)r);
+  h->rank = rank;
+  h->world = world;
+  return FL_OK;
+}
+
+int64_t fl_kernel_launches(const fl_handle*) { return fl::g_launches.load(); }
+
+}  // extern "C"
+
+namespace {
+
+using fl::GemmArgs;
+
+int gemm(fl_handle* h, const void* x, int ldx, const void* w, const void* bias, void* out,
+          int ldo, int M, int N, int K, int epi, cudaStream_t s) {
+  GemmArgs a{x, w, bias, out, M, N, K, ldx, ldo, epi, h->m.dtype, h->p.max_rows};
+  fl::g_launches += 1;
+  if (h->p.use_tensor_cores) return fl::gemm_tc(&h->tcws, a, s) ? FL_ECUDA : FL_OK;
+  fl::gemm_simt(a, s);
+  return FL_OK;
+}
+
+int allreduce_f32(fl_handle* h, float* buf, size_t n, cudaStream_t s) {
+  ncclResult_t r = g_nccl.allReduce(buf, buf, n, ncclFloat32, ncclSum, h->comm, s);
+  if (r != ncclSuccess) return fail(FL_ENCCL, "ncclAllReduce failed (%d)", (int)r);
+  return FL_OK;
+}
+
+}  // namespace
+
+extern "C" int fl_step(fl_handle* h, const fl_row* rows, int n_rows, int n_dec, int rows_changed,
+                       float* logits_out, void* stream) {
+  if (!h) return fail(FL_EINVAL, "null handle");
+  if (n_rows < 1 || n_dec < 0 || n_dec > n_rows) return fail(FL_EINVAL, "bad row counts");
+  if (n_rows > h->p.max_rows) return fail(FL_ECAPACITY, "%d rows > max_rows %d", n_rows, h->p.max_rows);
+  if (n_dec > h->p.pool_slots) return fail(FL_ECAPACITY, "window %d > pool %d", n_dec, h->p.pool_slots);
+  if (h->m.tp_size > 1 && !h->comm) return fail(FL_EINVAL, "tp_size > 1 needs fl_comm_init");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const fl_model_desc& m = h->m;
+  const fl_pool_desc& p = h->p;
+  const int d = m.d_model, hd = m.head_dim, L = m.n_layer, dt = m.dtype, es = h->es;
+  const int Hl = h->Hl, Dl = h->Dl, Fl = h->Fl;
+  const bool tp = m.tp_size > 1;
+  if (rows_changed) {
+    if (!rows) return fail(FL_EINVAL, "rows_changed with null rows");
+    for (int i = 0; i < n_rows; ++i) {
+      const fl_row& r = rows[i];
+      if (r.slot < 0 || r.slot >= p.pool_slots) return fail(FL_EINVAL, "row %d slot %d", i, r.slot);
+      if (r.kind != FL_ROW_ORPHAN && r.pos >= p.max_seq)
+        return fail(FL_ECAPACITY, "row %d position %d >= max_seq %d", i, r.pos, p.max_seq);
+      if ((r.kind == FL_ROW_PREFILL) != (i >= n_dec)) return fail(FL_EINVAL, "row %d kind order", i);
+    }
+    FL_CUDA(cudaMemcpyAsync(h->rows, rows, sizeof(fl_row) * n_rows, cudaMemcpyHostToDevice, s));
+  }
+  const size_t kv_layer_elems = (size_t)p.pool_slots * 2 * Hl * p.max_seq * hd;
+  char* kv = static_cast<char*>(p.kv);
+
+  fl::launch_embed(h->rows, n_rows, p.req_tok, p.req_pos, p.req_ngen, p.state_slots, m.wte, m.wpe,
+                   d, dt, h->x, h->row_tok, h->row_pos, h->row_ctx, s);
+  fl::g_launches += 1;
+  for (int l = 0; l < L; ++l) {
+    const void* const* W = m.layers + (size_t)l * FL_W_LAYER_COUNT;
+    void* kvl = kv + kv_layer_elems * es * l;
+    // K2 + K3
+    fl::launch_layernorm(h->x, W[FL_W_LN1_G], W[FL_W_LN1_B], h->h, n_rows, d, m.ln_eps, dt, s);
+    if (gemm(h, h->h, d, W[FL_W_QKV], W[FL_W_QKV_B], h->qkv, 3 * Dl, n_rows, 3 * Dl, d, fl::EPI_STORE, s)) return fail(FL_ECUDA, "tensor-core GEMM: %s", fl::tc_last_error());
+    fl::launch_rope_append(h->qkv, h->rows, h->row_pos, n_rows, Hl, hd, m.rotary_dim, m.family, kvl,
+                           p.pool_slots, p.max_seq, h->q, dt, s);
+    // K4
+    fl::launch_attention(h->q, h->rows, h->row_ctx, n_rows, Hl, hd, kvl, p.pool_slots, p.max_seq,
+                         h->a, h->att_o, h->att_ml, dt, s);
+    fl::g_launches += 3 + (h->ms > 1 ? 1 : 0);
+    // MLP input: GPT-2 = LN2 of the updated residual; GPT-J = LN1 output;
+    // NeoX = LN2 of the residual *before* the attention update.
+    if (m.family == FL_FAMILY_NEOX) {
+      fl::launch_layernorm(h->x, W[FL_W_LN2_G], W[FL_W_LN2_B], h->h2, n_rows, d, m.ln_eps, dt, s);
+      fl::g_launches += 1;
+    }
+    // K5 attn-out (+ all-reduce)
+    if (tp) {
+      if (gemm(h, h->a, Dl, W[FL_W_O], nullptr, h->y, d, n_rows, d, Dl, fl::EPI_STORE_F32, s)) return fail(FL_ECUDA, "tensor-core GEMM: %s", fl::tc_last_error());
+      if (int e = allreduce_f32(h, h->y, (size_t)n_rows * d, s)) return e;
+      fl::launch_add_partial(h->x, h->y, W[FL_W_O_B], nullptr, n_rows, d, dt, s);
+      fl::g_launches += 1;
+    } else {
+      if (gemm(h, h->a, Dl, W[FL_W_O], W[FL_W_O_B], h->x, d, n_rows, d, Dl, fl::EPI_ACC_F32, s)) return fail(FL_ECUDA, "tensor-core GEMM: %s", fl::tc_last_error());
+    }
+    const void* mlp_in = h->h;  // GPT-J: LN1 output
+    if (m.family == FL_FAMILY_GPT2) {
+      fl::launch_layernorm(h->x, W[FL_W_LN2_G], W[FL_W_LN2_B], h->h, n_rows, d, m.ln_eps, dt, s);
+      fl::g_launches += 1;
+    } else if (m.family == FL_FAMILY_NEOX) {
+      mlp_in = h->h2;   // LN2 of the residual before the attention update
+    }
+    // K6 + K7 (+ all-reduce)
+    if (gemm(h, mlp_in, d, W[FL_W_FC], W[FL_W_FC_B], h->f, Fl, n_rows, Fl, d, fl::EPI_GELU, s)) return fail(FL_ECUDA, "tensor-core GEMM: %s", fl::tc_last_error());
+    if (tp) {
+      if (gemm(h, h->f, Fl, W[FL_W_PROJ], nullptr, h->y, d, n_rows, d, Fl, fl::EPI_STORE_F32, s)) return fail(FL_ECUDA, "tensor-core GEMM: %s", fl::tc_last_error());
+      if (int e = allreduce_f32(h, h->y, (size_t)n_rows * d, s)) return e;
+      fl::launch_add_partial(h->x, h->y, W[FL_W_PROJ_B], nullptr, n_rows, d, dt, s);
+      fl::g_launches += 1;
+    } else {
+      if (gemm(h, h->f, Fl, W[FL_W_PROJ], W[FL_W_PROJ_B], h->x, d, n_rows, d, Fl, fl::EPI_ACC_F32, s)) return fail(FL_ECUDA, "tensor-core GEMM: %s", fl::tc_last_error());
+    }
+  }
+  if (n_dec > 0) {
+    fl::launch_layernorm(h->x, m.lnf_g, m.lnf_b, h->h, n_dec, d, m.ln_eps, dt, s);
+    if (gemm(h, h->h, d, m.w_lm, m.b_lm, h->logits, h->Vl, n_dec, h->Vloc, d, fl::EPI_STORE_F32, s)) return fail(FL_ECUDA, "tensor-core GEMM: %s", fl::tc_last_error());
+    fl::launch_argmax(h->logits, n_dec, h->Vloc, h->Vl, m.tp_rank * h->Vl, h->keys, s);
+    fl::g_launches += 2;
+    if (tp) {
+      ncclResult_t r = g_nccl.allReduce(h->keys, h->keys, n_dec, ncclUint64, ncclMax, h->comm, s);
+      if (r != ncclSuccess) return fail(FL_ENCCL, "argmax all-reduce failed (%d)", (int)r);
+    }
+    fl::launch_apply_tokens(h->keys, h->rows, h->row_pos, n_dec, p.req_tok, p.req_pos, p.req_ngen,
+                            p.tok_hist, p.state_slots, p.max_new_tokens, s);
+    fl::g_launches += 1;
+    if (logits_out)
+      FL_CUDA(cudaMemcpyAsync(logits_out, h->logits, sizeof(float) * n_dec * h->Vl,
+                              cudaMemcpyDeviceToDevice, s));
+  }
+  FL_CUDA(cudaGetLastError());
+  return FL_OK;
+}
+
+extern "C" int fl_shuffle(fl_handle* h, const int32_t* moves, int n, void* stream) {
+  if (!h) return fail(FL_EINVAL, "null handle");
+  if (n <= 0) return FL_OK;
+  if (n > h->p.pool_slots) return fail(FL_EINVAL, "%d moves > pool %d", n, h->p.pool_slots);
+  for (int i = 0; i < n; ++i) {
+    const int s0 = moves[3 * i], d0 = moves[3 * i + 1], c = moves[3 * i + 2];
+    if (s0 < 0 || s0 >= h->p.pool_slots || d0 < 0 || d0 >= h->p.pool_slots || s0 == d0 || c < 0 ||
+        c > h->p.max_seq)
+      return fail(FL_EINVAL, "bad move %d: %d -> %d (%d)", i, s0, d0, c);
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  FL_CUDA(cudaMemcpyAsync(h->moves, moves, sizeof(int32_t) * 3 * n, cudaMemcpyHostToDevice, s));
+  fl::launch_shuffle(h->moves, n, h->p.kv, h->m.n_layer, h->p.pool_slots, h->Hl, h->p.max_seq,
+                     h->m.head_dim, h->m.dtype, s);
+  fl::g_launches += 1;
+  FL_CUDA(cudaGetLastError());
+  return FL_OK;
+}
+
+namespace {
+fl::TcWorkspace g_dbg_ws;
+void* g_dbg_base = nullptr;
+}
+
+extern "C" size_t fl_gemm_workspace_bytes(void) { return fl::tc_workspace_bytes(0, 0); }
+
+extern "C" int fl_gemm(const void* x, int ldx, const void* w, const void* bias, void* out, int ldo,
+                       int M, int N, int K, int epi, int dtype, int use_tc, void* workspace,
+                       void* stream) {
+  if (!x || !w || !out || M < 1 || N < 1 || K < 1) return fail(FL_EINVAL, "bad gemm arguments");
+  fl::GemmArgs a{x, w, bias, out, M, N, K, ldx, ldo, epi, dtype, M};
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (use_tc) {
+    if (g_dbg_base != workspace) {
+      if (g_dbg_base) fl::tc_destroy(&g_dbg_ws);
+      if (fl::tc_init(&g_dbg_ws, workspace, fl::tc_workspace_bytes(0, 0)))
+        return fail(FL_ECUDA, "%s", fl::tc_last_error());
+      g_dbg_base = workspace;
+    }
+    if (fl::gemm_tc(&g_dbg_ws, a, s)) return fail(FL_EINVAL, "%s", fl::tc_last_error());
+  } else {
+    fl::gemm_simt(a, s);
+  }
+  FL_CUDA(cudaGetLastError());
+  return FL_OK;
+}

@@ -1,0 +1,33 @@
+// tcgen05 / TMEM / TMA GEMM for the projections of the fused decode step.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "kernels.cuh"
+
+namespace fl {
+
+struct TcWorkspace {
+  void* base = nullptr;        // caller-owned device scratch
+  size_t bytes = 0;
+  int* counters = nullptr;     // split-K arrival counters (self-resetting)
+  float* partials = nullptr;   // split-K fp32 partial tiles
+  size_t partial_floats = 0;
+  int num_sms = 148;
+  void* maps = nullptr;        // host-side tensor-map cache (opaque)
+};
+
+size_t tc_workspace_bytes(int max_rows, int max_n);
+int tc_init(TcWorkspace* ws, void* base, size_t bytes);
+void tc_destroy(TcWorkspace* ws);
+const char* tc_last_error();
+
+// out[M,N] = X[M,K] . W[N,K]^T (+bias, epilogue), bf16 operands, fp32 accumulate in TMEM.
+// Returns 0, or -1 with tc_last_error() set (shape the kernel does not cover).
+int gemm_tc(TcWorkspace* ws, const GemmArgs& a, cudaStream_t s);
+
+}  // namespace fl

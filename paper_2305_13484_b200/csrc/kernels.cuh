@@ -1,0 +1,69 @@
+// Launchers for the fused decode step kernels (host side, internal).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/flover_b200.h"
+
+namespace fl {
+
+enum Epilogue {
+  EPI_STORE = 0,      // out(T)   = acc + bias
+  EPI_GELU = 1,       // out(T)   = gelu(acc + bias)
+  EPI_ACC_F32 = 2,    // out(f32) += acc + bias      (residual update)
+  EPI_STORE_F32 = 3   // out(f32) = acc + bias       (partial sums, logits)
+};
+
+struct GemmArgs {
+  const void* x;      // [M, K] activations, row stride ldx (elements)
+  const void* w;      // [N, K] weights, row stride K
+  const void* bias;   // [N] or null (same dtype as w)
+  void* out;          // [M, N] row stride ldo
+  int M, N, K, ldx, ldo;
+  int epi;
+  int dtype;          // FL_DTYPE_*
+  int mcap;           // rows allocated behind x (>= M); fixes the TMA map per buffer
+};
+
+// SIMT FFMA GEMM (fp32 path and the reference path for the tensor-core GEMM).
+void gemm_simt(const GemmArgs& a, cudaStream_t s);
+
+// Resolve rows (token / position / context per row) and gather embeddings.
+void launch_embed(const fl_row* rows, int n_rows, const int32_t* req_tok, const int32_t* req_pos,
+                  int32_t* req_ngen, int R, const void* wte, const void* wpe, int d, int dtype,
+                  float* x, int32_t* row_tok, int32_t* row_pos, int32_t* row_ctx, cudaStream_t s);
+
+// out(T)[M, d] = LN(x[M, d]) * g + b
+void launch_layernorm(const float* x, const void* g, const void* b, void* out, int M, int d,
+                      float eps, int dtype, cudaStream_t s);
+
+// x += y + b1 (+ b2)   (after a tensor-parallel all-reduce of y)
+void launch_add_partial(float* x, const float* y, const void* b1, const void* b2, int M, int d,
+                        int dtype, cudaStream_t s);
+
+// rotary on q/k, q -> qout [M, Hl*hd]; k/v -> KV pool of this layer at (slot, pos).
+void launch_rope_append(const void* qkv, const fl_row* rows, const int32_t* row_pos, int M,
+                        int Hl, int hd, int rot, int family, void* kv_layer, int C, int S,
+                        void* qout, int dtype, cudaStream_t s);
+
+// split-K masked decode attention over each row's own context.
+int attn_max_splits(int S);
+void launch_attention(const void* q, const fl_row* rows, const int32_t* row_ctx, int M, int Hl,
+                      int hd, const void* kv_layer, int C, int S, void* out, float* ws_o,
+                      float* ws_ml, int dtype, cudaStream_t s);
+
+// per-row (max logit, lowest index) as a packed 64-bit key
+void launch_argmax(const float* logits, int M, int V, int ldl, int index_base,
+                   unsigned long long* keys, cudaStream_t s);
+
+// greedy token -> per-request state and token history
+void launch_apply_tokens(const unsigned long long* keys, const fl_row* rows,
+                         const int32_t* row_pos, int n_dec, int32_t* req_tok, int32_t* req_pos,
+                         int32_t* req_ngen, int32_t* tok_hist, int R, int max_new, cudaStream_t s);
+
+// K10: move live KV prefixes between physical slots
+void launch_shuffle(const int32_t* moves, int n_moves, void* kv, int L, int C, int Hl, int S,
+                    int hd, int dtype, cudaStream_t s);
+
+}  // namespace fl

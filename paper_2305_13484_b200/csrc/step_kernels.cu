@@ -1,0 +1,286 @@
+// Row-local kernels of the fused decode step: embedding gather (K1),
+// LayerNorm (K2), rotary + KV append (K3 epilogue), greedy argmax and the
+// per-request state step (K8/K9 -- the device image of core.record_token,
+// reference core.py:108-123).
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace fl {
+
+// ---------------------------------------------------------------- K1 embed
+template <typename T>
+__global__ void k_embed(const fl_row* __restrict__ rows, const int32_t* __restrict__ req_tok,
+                        const int32_t* __restrict__ req_pos, int32_t* __restrict__ req_ngen, int R,
+                        const T* __restrict__ wte, const T* __restrict__ wpe, int d,
+                        float* __restrict__ x, int32_t* __restrict__ row_tok,
+                        int32_t* __restrict__ row_pos, int32_t* __restrict__ row_ctx) {
+  const int r = blockIdx.x;
+  const fl_row row = rows[r];
+  int tok, pos, ctx;
+  if (row.kind == FL_ROW_ORPHAN) {
+    ctx = row.ctx > 0 ? row.ctx : 1;
+    pos = ctx - 1;
+    tok = 0;
+  } else {
+    const int q = row.rid % R;
+    pos = row.pos >= 0 ? row.pos : req_pos[q];
+    tok = row.tok >= 0 ? row.tok : req_tok[q];
+    ctx = pos + 1;
+    // first decode row of a freshly fused request: its generation count starts here
+    if (row.kind == FL_ROW_DECODE && row.tok >= 0 && threadIdx.x == 0) req_ngen[q] = 0;
+  }
+  if (threadIdx.x == 0) {
+    row_tok[r] = tok;
+    row_pos[r] = pos;
+    row_ctx[r] = ctx;
+  }
+  constexpr int V = Vec16<T>::N;
+  const T* e = wte + static_cast<size_t>(tok) * d;
+  const T* p = wpe ? wpe + static_cast<size_t>(pos) * d : nullptr;
+  float* xo = x + static_cast<size_t>(r) * d;
+  for (int i = threadIdx.x * V; i < d; i += blockDim.x * V) {
+    float a[V], b[V];
+    load16(e + i, a);
+    if (p) {
+      load16(p + i, b);
+#pragma unroll
+      for (int j = 0; j < V; ++j) a[j] += b[j];
+    }
+#pragma unroll
+    for (int j = 0; j < V; j += 4)
+      *reinterpret_cast<float4*>(xo + i + j) = make_float4(a[j], a[j + 1], a[j + 2], a[j + 3]);
+  }
+}
+
+void launch_embed(const fl_row* rows, int n_rows, const int32_t* req_tok, const int32_t* req_pos,
+                  int32_t* req_ngen, int R, const void* wte, const void* wpe, int d, int dtype,
+                  float* x, int32_t* row_tok, int32_t* row_pos, int32_t* row_ctx, cudaStream_t s) {
+  if (n_rows <= 0) return;
+  if (dtype == FL_DTYPE_BF16)
+    k_embed<bf16><<<n_rows, 128, 0, s>>>(rows, req_tok, req_pos, req_ngen, R, (const bf16*)wte,
+                                         (const bf16*)wpe, d, x, row_tok, row_pos, row_ctx);
+  else
+    k_embed<float><<<n_rows, 128, 0, s>>>(rows, req_tok, req_pos, req_ngen, R, (const float*)wte,
+                                          (const float*)wpe, d, x, row_tok, row_pos, row_ctx);
+}
+
+// ---------------------------------------------------------------- K2 LayerNorm
+// One CTA per row, values kept in registers (d <= 256 threads * 4 * 8).
+template <typename T, int PER>
+__global__ void __launch_bounds__(256) k_layernorm(const float* __restrict__ x,
+                                                   const T* __restrict__ g,
+                                                   const T* __restrict__ b, T* __restrict__ out,
+                                                   int d, float eps) {
+  __shared__ float red[32];
+  const int r = blockIdx.x;
+  const float* xr = x + static_cast<size_t>(r) * d;
+  float v[PER * 4];
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < PER; ++c) {
+    const int i = (c * blockDim.x + threadIdx.x) * 4;
+    float4 t = i < d ? *reinterpret_cast<const float4*>(xr + i) : make_float4(0, 0, 0, 0);
+    v[4 * c] = t.x; v[4 * c + 1] = t.y; v[4 * c + 2] = t.z; v[4 * c + 3] = t.w;
+    s += t.x + t.y + t.z + t.w;
+  }
+  const float mean = block_sum(s, red) / d;
+  float q = 0.f;
+#pragma unroll
+  for (int c = 0; c < PER; ++c) {
+    const int i = (c * blockDim.x + threadIdx.x) * 4;
+    if (i < d) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float t = v[4 * c + j] - mean;
+        q += t * t;
+      }
+    }
+  }
+  const float rstd = rsqrtf(block_sum(q, red) / d + eps);
+  T* o = out + static_cast<size_t>(r) * d;
+#pragma unroll
+  for (int c = 0; c < PER; ++c) {
+    const int i = (c * blockDim.x + threadIdx.x) * 4;
+    if (i < d) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        o[i + j] = from_f<T>((v[4 * c + j] - mean) * rstd * to_f(g[i + j]) + to_f(b[i + j]));
+    }
+  }
+}
+
+template <typename T>
+static void ln_dispatch(const float* x, const void* g, const void* b, void* out, int M, int d,
+                        float eps, cudaStream_t s) {
+  const int per = (d + 1023) / 1024;  // float4 chunks per thread at 256 threads
+  const T* G = (const T*)g;
+  const T* B = (const T*)b;
+  T* O = (T*)out;
+  switch (per) {
+    case 1: k_layernorm<T, 1><<<M, 256, 0, s>>>(x, G, B, O, d, eps); break;
+    case 2: k_layernorm<T, 2><<<M, 256, 0, s>>>(x, G, B, O, d, eps); break;
+    case 3: k_layernorm<T, 3><<<M, 256, 0, s>>>(x, G, B, O, d, eps); break;
+    case 4: k_layernorm<T, 4><<<M, 256, 0, s>>>(x, G, B, O, d, eps); break;
+    case 5: case 6: k_layernorm<T, 6><<<M, 256, 0, s>>>(x, G, B, O, d, eps); break;
+    default: k_layernorm<T, 8><<<M, 256, 0, s>>>(x, G, B, O, d, eps); break;
+  }
+}
+
+void launch_layernorm(const float* x, const void* g, const void* b, void* out, int M, int d,
+                      float eps, int dtype, cudaStream_t s) {
+  if (M <= 0) return;
+  if (dtype == FL_DTYPE_BF16) ln_dispatch<bf16>(x, g, b, out, M, d, eps, s);
+  else ln_dispatch<float>(x, g, b, out, M, d, eps, s);
+}
+
+// ---------------------------------------------------------------- residual add
+template <typename T>
+__global__ void k_add_partial(float* __restrict__ x, const float* __restrict__ y,
+                              const T* __restrict__ b1, const T* __restrict__ b2, int M, int d) {
+  const size_t n = static_cast<size_t>(M) * d;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const int c = static_cast<int>(i % d);
+    float v = x[i] + y[i];
+    if (b1) v += to_f(b1[c]);
+    if (b2) v += to_f(b2[c]);
+    x[i] = v;
+  }
+}
+
+void launch_add_partial(float* x, const float* y, const void* b1, const void* b2, int M, int d,
+                        int dtype, cudaStream_t s) {
+  if (M <= 0) return;
+  const size_t n = (size_t)M * d;
+  const int grid = (int)((n + 255) / 256 < 148 * 8 ? (n + 255) / 256 : 148 * 8);
+  if (dtype == FL_DTYPE_BF16)
+    k_add_partial<bf16><<<grid, 256, 0, s>>>(x, y, (const bf16*)b1, (const bf16*)b2, M, d);
+  else
+    k_add_partial<float><<<grid, 256, 0, s>>>(x, y, (const float*)b1, (const float*)b2, M, d);
+}
+
+// ---------------------------------------------------------------- rotary + KV append
+// grid (M, Hl), block hd threads: thread i owns element i of q, k and v.
+template <typename T>
+__global__ void k_rope_append(const T* __restrict__ qkv, const fl_row* __restrict__ rows,
+                              const int32_t* __restrict__ row_pos, int Hl, int hd, int rot,
+                              int family, T* __restrict__ kv_layer, int C, int S,
+                              T* __restrict__ qout) {
+  const int r = blockIdx.x, h = blockIdx.y, i = threadIdx.x;
+  const int D = Hl * hd;
+  const T* base = qkv + static_cast<size_t>(r) * 3 * D + h * hd;
+  float q = to_f(base[i]);
+  float k = to_f(base[D + i]);
+  const float v = to_f(base[2 * D + i]);
+  const int pos = row_pos[r];
+  if (rot > 0 && i < rot) {
+    // pair partner and frequency index: GPT-J interleaves (2j, 2j+1);
+    // NeoX rotates halves (j, j + rot/2).  inv_freq_j = 10000^(-2j/rot).
+    int j, partner;
+    float sign;
+    if (family == FL_FAMILY_GPTJ) {
+      j = i >> 1;
+      partner = i ^ 1;
+      sign = (i & 1) ? 1.f : -1.f;
+    } else {
+      const int half = rot >> 1;
+      j = i < half ? i : i - half;
+      partner = i < half ? i + half : i - half;
+      sign = i < half ? -1.f : 1.f;
+    }
+    const float inv_freq = exp2f(-(2.f * j / rot) * 13.287712379549449f);  // log2(10000)
+    float sn, cs;
+    sincosf(static_cast<float>(pos) * inv_freq, &sn, &cs);
+    const float qp = to_f(base[partner]);
+    const float kp = to_f(base[D + partner]);
+    q = q * cs + sign * qp * sn;
+    k = k * cs + sign * kp * sn;
+  }
+  qout[static_cast<size_t>(r) * D + h * hd + i] = from_f<T>(q);
+  const fl_row row = rows[r];
+  if (row.kind != FL_ROW_ORPHAN) {
+    const size_t kb = ((static_cast<size_t>(row.slot) * 2 + 0) * Hl + h) * S + pos;
+    const size_t vb = ((static_cast<size_t>(row.slot) * 2 + 1) * Hl + h) * S + pos;
+    kv_layer[kb * hd + i] = from_f<T>(k);
+    kv_layer[vb * hd + i] = from_f<T>(v);
+  }
+}
+
+void launch_rope_append(const void* qkv, const fl_row* rows, const int32_t* row_pos, int M,
+                        int Hl, int hd, int rot, int family, void* kv_layer, int C, int S,
+                        void* qout, int dtype, cudaStream_t s) {
+  if (M <= 0) return;
+  dim3 grid(M, Hl);
+  if (family == FL_FAMILY_GPT2) rot = 0;
+  if (dtype == FL_DTYPE_BF16)
+    k_rope_append<bf16><<<grid, hd, 0, s>>>((const bf16*)qkv, rows, row_pos, Hl, hd, rot, family,
+                                            (bf16*)kv_layer, C, S, (bf16*)qout);
+  else
+    k_rope_append<float><<<grid, hd, 0, s>>>((const float*)qkv, rows, row_pos, Hl, hd, rot,
+                                             family, (float*)kv_layer, C, S, (float*)qout);
+}
+
+// ---------------------------------------------------------------- K8 greedy argmax
+__global__ void __launch_bounds__(1024) k_argmax(const float* __restrict__ logits, int V, int ldl,
+                                                 int index_base,
+                                                 unsigned long long* __restrict__ keys) {
+  __shared__ unsigned long long red[32];
+  const int r = blockIdx.x;
+  const float* l = logits + static_cast<size_t>(r) * ldl;
+  unsigned long long best = 0ull;
+  for (int i = threadIdx.x; i < V; i += blockDim.x) {
+    const unsigned long long k = argmax_key(l[i], index_base + i);
+    best = k > best ? k : best;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
+    best = t > best ? t : best;
+  }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    best = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
+      best = t > best ? t : best;
+    }
+    if (threadIdx.x == 0) keys[r] = best;
+  }
+}
+
+void launch_argmax(const float* logits, int M, int V, int ldl, int index_base,
+                   unsigned long long* keys, cudaStream_t s) {
+  if (M <= 0) return;
+  k_argmax<<<M, 1024, 0, s>>>(logits, V, ldl, index_base, keys);
+}
+
+// ---------------------------------------------------------------- K9 state step
+__global__ void k_apply_tokens(const unsigned long long* __restrict__ keys,
+                               const fl_row* __restrict__ rows, const int32_t* __restrict__ row_pos,
+                               int n_dec, int32_t* __restrict__ req_tok,
+                               int32_t* __restrict__ req_pos, int32_t* __restrict__ req_ngen,
+                               int32_t* __restrict__ tok_hist, int R, int max_new) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_dec) return;
+  const fl_row row = rows[r];
+  if (row.kind != FL_ROW_DECODE) return;
+  const int q = row.rid % R;
+  const int tok = argmax_key_index(keys[r]);
+  req_tok[q] = tok;
+  req_pos[q] = row_pos[r] + 1;
+  const int g = req_ngen[q];
+  if (g < max_new) tok_hist[static_cast<size_t>(q) * max_new + g] = tok;
+  req_ngen[q] = g + 1;
+}
+
+void launch_apply_tokens(const unsigned long long* keys, const fl_row* rows,
+                         const int32_t* row_pos, int n_dec, int32_t* req_tok, int32_t* req_pos,
+                         int32_t* req_ngen, int32_t* tok_hist, int R, int max_new, cudaStream_t s) {
+  if (n_dec <= 0) return;
+  k_apply_tokens<<<(n_dec + 127) / 128, 128, 0, s>>>(keys, rows, row_pos, n_dec, req_tok, req_pos,
+                                                     req_ngen, tok_hist, R, max_new);
+}
+
+}  // namespace fl

@@ -1,0 +1,299 @@
+"""CudaExecutor: runs the fused stream's iterations on the B200 via the C-ABI.
+
+Plugged into ``FusionStream(..., executor=CudaExecutor(...))``, it realises
+each modelled action of the reference loop on the device:
+
+* ``try_fuse_pending`` (engine.py:97-124) -> ``on_fuse``: the request's prompt
+  is queued as PREFILL rows of the next fused iteration (positions
+  0..P-2) and its first DECODE row carries prompt token P-1 explicitly.
+* ``step_iteration`` (engine.py:128-160) -> ``run_iteration``: one
+  ``fl_step`` over the live window [buffer_offset, +buffer_size) in window
+  order (orphaned slots of fusion_noshuffle become ORPHAN rows that are
+  computed over stale KV and discarded -- the paper's naive scheme,
+  PAPER.md:254) followed by the prefill rows.
+* ``apply_shuffle`` (buffer.py:261-278) -> ``on_shuffle``: the plan's moves
+  become (src, dst, live-length) triples for the K10 kernel.
+
+Device memory is owned here through PyTorch: weights, the KV pool
+[L][C][2][H/tp][S][hd], per-request state (next token / position / count /
+token history, indexed rid % R) and the library workspace.  Logical slot s
+lives in physical slot s % C; the live window never spans more than C slots
+(checked every iteration, ``CapacityExceeded`` otherwise).
+
+Because stop lengths are pre-sampled, the host never needs a generated token
+to schedule: steady-state iterations upload nothing and read nothing back.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _lib
+from .errors import CapacityExceeded, InvalidParam
+from .models import LAYER_KEYS, ModelSpec, init_weights
+
+_TORCH_DTYPE = {"f32": torch.float32, "bf16": torch.bfloat16}
+
+
+class CudaExecutor:
+    def __init__(self, spec: ModelSpec, prompts, *, dtype: str = "bf16", pool_slots: int = 128,
+                 max_rows: int | None = None, max_seq: int | None = None,
+                 max_new_tokens: int = 1024, input_len: int | None = None,
+                 state_slots: int = 4096, tp_rank: int = 0, tp_size: int = 1, seed: int = 0,
+                 weights: dict | None = None, use_tensor_cores: bool | None = None,
+                 capture_logits: bool = False, device: str = "cuda", comm_id: bytes | None = None,
+                 time_steps: bool = False):
+        if dtype not in _TORCH_DTYPE:
+            raise InvalidParam(f"dtype must be f32 or bf16, got {dtype}")
+        self.lib = _lib.load()
+        self.spec = spec
+        self.prompts = prompts
+        self.dtype = dtype
+        self.tp_rank, self.tp_size = tp_rank, tp_size
+        self.device = torch.device(device)
+        self.C = pool_slots
+        self.R = state_slots
+        self.max_new = max_new_tokens
+        if max_seq is None:
+            if input_len is None:
+                raise InvalidParam("need max_seq or input_len")
+            max_seq = input_len + max_new_tokens - 1
+        self.S = max_seq
+        self.max_rows = max_rows or (pool_slots + 16 * (input_len or 32))
+        if use_tensor_cores is None:
+            use_tensor_cores = dtype == "bf16"
+        self.use_tc = bool(use_tensor_cores)
+        tdt = _TORCH_DTYPE[dtype]
+        hl = spec.n_head // tp_size
+
+        # ---- weights (this rank's shard)
+        if weights is None:
+            weights = init_weights(spec, seed=seed, device=self.device, dtype=tdt, rank=tp_rank,
+                                   world=tp_size)
+        self.w = {k: v.to(self.device, tdt).contiguous() for k, v in weights.items()}
+        ptrs = []
+        for layer in range(spec.n_layer):
+            for key in LAYER_KEYS:
+                t = self.w.get(f"layers.{layer}.{key}")
+                ptrs.append(t.data_ptr() if t is not None else None)
+        self._layer_ptrs = (C.c_void_p * len(ptrs))(*ptrs)
+
+        def ptr(name):
+            t = self.w.get(name)
+            return t.data_ptr() if t is not None else None
+
+        self.mdesc = _lib.ModelDesc(
+            _lib.FL_FAMILY[spec.family], _lib.FL_DTYPE[dtype], spec.n_layer, spec.d_model,
+            spec.n_head, spec.head_dim, spec.d_ff, spec.vocab, spec.max_pos, spec.rotary_dim,
+            spec.ln_eps, tp_rank, tp_size, ptr("wte"), ptr("wpe"), ptr("lnf_g"), ptr("lnf_b"),
+            ptr("w_lm"), ptr("b_lm"), C.cast(self._layer_ptrs, C.POINTER(C.c_void_p)))
+
+        # ---- KV pool and per-request state
+        self.kv = torch.empty((spec.n_layer, self.C, 2, hl, self.S, spec.head_dim), dtype=tdt,
+                              device=self.device)
+        i32 = dict(dtype=torch.int32, device=self.device)
+        self.req_tok = torch.zeros(self.R, **i32)
+        self.req_pos = torch.zeros(self.R, **i32)
+        self.req_ngen = torch.zeros(self.R, **i32)
+        self.tok_hist = torch.zeros((self.R, self.max_new), **i32)
+        self.pdesc = _lib.PoolDesc(self.C, self.S, self.max_rows, self.R, self.max_new,
+                                   int(self.use_tc), self.kv.data_ptr(), self.req_tok.data_ptr(),
+                                   self.req_pos.data_ptr(), self.req_ngen.data_ptr(),
+                                   self.tok_hist.data_ptr(), None, 0)
+        nbytes = self.lib.fl_workspace_bytes(C.byref(self.mdesc), C.byref(self.pdesc))
+        if nbytes == 0:
+            _lib.check(-1)
+        self.ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        self.pdesc.workspace = self.ws.data_ptr()
+        self.pdesc.workspace_bytes = nbytes
+        h = C.c_void_p()
+        _lib.check(self.lib.fl_create(C.byref(self.mdesc), C.byref(self.pdesc), C.byref(h)))
+        self.handle = h
+        if tp_size > 1:
+            if comm_id is None:
+                raise InvalidParam("tp_size > 1 needs comm_id (see tp.make_comm_id)")
+            buf = C.create_string_buffer(bytes(comm_id), 128)
+            _lib.check(self.lib.fl_comm_init(self.handle, buf, tp_rank, tp_size))
+
+        # ---- host bookkeeping
+        self.capture_logits = capture_logits
+        self.vl = (spec.vocab + tp_size - 1) // tp_size
+        if capture_logits:
+            self.logits_buf = torch.empty((self.C, self.vl), dtype=torch.float32, device=self.device)
+        self.logits_log = []             # [(iteration, [rid per decode row], cpu tensor)]
+        self.time_steps = time_steps
+        self._events = []
+        self._new = []                    # rids fused at this boundary, in order
+        self._live = {}                   # rid -> dict(P, stop, slot)
+        self._orphans = {}                # logical slot -> stale context length
+        self._prev_had_new = False
+        self._rows_version = None
+        self._rows = None
+        self._n_rows = self._n_dec = 0
+        self.iterations = 0
+        self.rows_total = 0
+        self.prefill_rows_total = 0
+        self.decode_rows_total = 0
+        self.orphan_rows_total = 0
+        self.shuffles = 0
+        self.moved_kv_bytes = 0
+        self.seen = []
+
+    # ----------------------------------------------------------------- utils
+    @property
+    def stream(self):
+        return torch.cuda.current_stream(self.device)
+
+    def launches(self) -> int:
+        return int(self.lib.fl_kernel_launches(self.handle))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.fl_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ----------------------------------------------------------------- hooks
+    def on_fuse(self, rid, slot, request):
+        prompt = self.prompts[rid]
+        P = len(prompt)
+        if request is not None and P != request.input_len:
+            raise InvalidParam(f"request {rid}: prompt has {P} tokens, input_len {request.input_len}")
+        stop = min(request.actual_output_length, request.max_output_length) if request else self.max_new
+        if P + stop - 1 > self.S:
+            raise CapacityExceeded(f"request {rid} needs {P + stop - 1} positions > max_seq {self.S}")
+        if stop > self.max_new:
+            raise CapacityExceeded(f"request {rid} stops at {stop} > max_new_tokens {self.max_new}")
+        for other in self._live:
+            if other % self.R == rid % self.R:
+                raise CapacityExceeded(f"state ring collision between requests {rid} and {other}")
+        self._live[rid] = {"P": P, "stop": stop, "gen": 0}
+        self._new.append(rid)
+        self.seen.append(rid)
+
+    def on_evict(self, rid, slot):
+        info = self._live.pop(rid)
+        # KV positions written: prefill 0..P-2 plus one per generated token
+        self._orphans[slot] = info["P"] + info["stop"] - 1
+
+    def _build_rows(self, layout):
+        lo, n = layout.buffer_offset, layout.buffer_size
+        if n > self.C:
+            raise CapacityExceeded(f"live window of {n} slots exceeds the KV pool ({self.C})")
+        slots = layout.slots
+        new = set(self._new)
+        for s in [k for k in self._orphans if k < lo]:
+            del self._orphans[s]
+        rows = []
+        prefill = []
+        for s in range(lo, lo + n):
+            occ = slots[s].occupant
+            phys = s % self.C
+            if occ is None:
+                rows.append((phys, -1, -1, -1, _lib.ROW_ORPHAN, self._orphans.get(s, 1)))
+            elif occ in new:
+                pr = self.prompts[occ]
+                P = len(pr)
+                rows.append((phys, occ, P - 1, pr[P - 1], _lib.ROW_DECODE, 0))
+                prefill.extend((phys, occ, j, pr[j], _lib.ROW_PREFILL, 0) for j in range(P - 1))
+            else:
+                rows.append((phys, occ, -1, -1, _lib.ROW_DECODE, 0))
+        n_dec = len(rows)
+        rows.extend(prefill)
+        if len(rows) > self.max_rows:
+            raise CapacityExceeded(f"{len(rows)} rows in one iteration > max_rows {self.max_rows}")
+        arr = (_lib.Row * len(rows))(*[_lib.Row(*r) for r in rows])
+        return arr, len(rows), n_dec
+
+    def run_iteration(self, stream) -> float | None:
+        layout = stream.layout
+        self._device_clock = stream.clock == "device"
+        has_new = bool(self._new)
+        changed = has_new or self._prev_had_new or layout.version != self._rows_version
+        if changed:
+            self._rows, self._n_rows, self._n_dec = self._build_rows(layout)
+            self._rows_version = layout.version
+        cs = self.stream
+        timed = stream.clock == "device" or self.time_steps
+        if timed:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(cs)
+        logits_ptr = self.logits_buf.data_ptr() if self.capture_logits else None
+        _lib.check(self.lib.fl_step(self.handle, self._rows, self._n_rows, self._n_dec, int(changed),
+                                    logits_ptr, C.c_void_p(cs.cuda_stream)))
+        self.iterations += 1
+        self.rows_total += self._n_rows
+        self.prefill_rows_total += self._n_rows - self._n_dec
+        n_orph = sum(1 for s in range(layout.buffer_offset, layout.buffer_offset + layout.buffer_size)
+                     if layout.slots[s].occupant is None) if changed else self._last_orph
+        self._last_orph = n_orph
+        self.orphan_rows_total += n_orph
+        self.decode_rows_total += self._n_dec - n_orph
+        if self.capture_logits:
+            rids = [r.rid for r in self._rows[:self._n_dec]]
+            kinds = [r.kind for r in self._rows[:self._n_dec]]
+            self.logits_log.append((stream.iteration_index, rids, kinds,
+                                    self.logits_buf[:self._n_dec].float().cpu()))
+        self._prev_had_new = has_new
+        self._new = []
+        for info in self._live.values():
+            info["gen"] += 1
+        if timed:
+            e1.record(cs)
+            if stream.clock == "device":
+                e1.synchronize()
+                return e0.elapsed_time(e1)
+            self._events.append((e0, e1))
+        return None
+
+    def on_shuffle(self, plan) -> float | None:
+        moves = []
+        for m in plan.moves:
+            info = self._live[m.request_id]
+            ctx = info["P"] + info["gen"] - 1      # KV positions written so far
+            moves.append((m.src_slot % self.C, m.dst_slot % self.C, ctx))
+            self.moved_kv_bytes += 2 * ctx * self.spec.kv_bytes_per_token(
+                2 if self.dtype == "bf16" else 4, self.tp_size)
+        flat = (C.c_int32 * (3 * len(moves)))(*[v for mv in moves for v in mv])
+        cs = self.stream
+        e0 = e1 = None
+        if self.time_steps or getattr(self, "_device_clock", False):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(cs)
+        _lib.check(self.lib.fl_shuffle(self.handle, flat, len(moves), C.c_void_p(cs.cuda_stream)))
+        self.shuffles += 1
+        for s in [m.src_slot for m in plan.moves]:
+            self._orphans.pop(s, None)
+        if e0 is not None:
+            e1.record(cs)
+            e1.synchronize()
+            return e0.elapsed_time(e1)
+        return None
+
+    def on_drain(self, stream):
+        torch.cuda.current_stream(self.device).synchronize()
+
+    # ----------------------------------------------------------------- results
+    def step_times_ms(self) -> list:
+        torch.cuda.current_stream(self.device).synchronize()
+        return [a.elapsed_time(b) for a, b in self._events]
+
+    def tokens(self, rids=None) -> dict:
+        """rid -> generated token ids (device history, one D2H copy)."""
+        rids = list(self.seen if rids is None else rids)
+        hist = self.tok_hist.cpu()
+        ngen = self.req_ngen.cpu()
+        out = {}
+        for rid in rids:
+            q = rid % self.R
+            out[rid] = hist[q, :int(ngen[q])].tolist()
+        return out

@@ -1,0 +1,104 @@
+"""Kernel-level parity on the B200 (through the C-ABI).
+
+* projection GEMM (tcgen05 and SIMT) vs an fp32 torch reference of the same op
+* K10 shuffle vs a torch slice-copy reference -- bit exact
+"""
+
+import ctypes as C
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+from paper_2305_13484_b200 import _lib  # noqa: E402
+
+EPI_STORE, EPI_GELU, EPI_ACC, EPI_F32 = 0, 1, 2, 3
+
+
+def _gelu(x):
+    return 0.5 * x * (1.0 + torch.tanh(0.7978845608028654 * (x + 0.044715 * x ** 3)))
+
+
+def _gemm(x, w, bias, out, epi, use_tc, dtype):
+    lib = _lib.load()
+    ws = torch.empty(lib.fl_gemm_workspace_bytes(), dtype=torch.uint8, device="cuda")
+    M, K = x.shape
+    N = w.shape[0]
+    s = torch.cuda.current_stream()
+    _lib.check(lib.fl_gemm(x.data_ptr(), x.stride(0), w.data_ptr(),
+                           bias.data_ptr() if bias is not None else None, out.data_ptr(),
+                           out.stride(0), M, N, K, epi, dtype, int(use_tc), ws.data_ptr(),
+                           C.c_void_p(s.cuda_stream)))
+    torch.cuda.synchronize()
+    return ws
+
+
+SHAPES = [(1, 768, 768), (7, 2304, 768), (16, 512, 1024), (55, 3072, 768), (64, 768, 3072),
+          (100, 50257, 768), (129, 1536, 4096), (256, 4096, 512), (300, 1000, 256), (17, 128, 64)]
+
+
+@pytest.mark.parametrize("M,N,K", SHAPES)
+@pytest.mark.parametrize("epi", [EPI_STORE, EPI_GELU, EPI_ACC, EPI_F32])
+def test_tcgen05_gemm_matches_fp32_reference(M, N, K, epi):
+    g = torch.Generator(device="cuda").manual_seed(M * 131 + N * 7 + K)
+    x = (torch.randn(M, K, device="cuda", generator=g) * 0.5).bfloat16()
+    w = (torch.randn(N, K, device="cuda", generator=g) * 0.05).bfloat16()
+    b = (torch.randn(N, device="cuda", generator=g) * 0.1).bfloat16()
+    ref = x.float() @ w.float().T + b.float()
+    if epi in (EPI_STORE, EPI_GELU):
+        out = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+        if epi == EPI_GELU:
+            ref = _gelu(ref)
+    else:
+        out = torch.randn(M, N, device="cuda", generator=g)
+        if epi == EPI_ACC:
+            ref = ref + out
+    _gemm(x, w, b, out, epi, True, 1)
+    # fp32 accumulation of bf16 products: error ~ sqrt(K) * 2^-9 * |x||w|;
+    # bf16 outputs add one rounding (2^-8 relative)
+    tol = 2e-3 * (K / 256) ** 0.5 + (2.0 ** -8) * ref.abs().max().item() * (epi in (0, 1))
+    err = (out.float() - ref).abs().max().item()
+    assert err <= tol, (err, tol)
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 256, 256), (33, 1000, 512), (70, 768, 3072)])
+def test_simt_gemm_fp32_matches_reference(M, N, K):
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.randn(M, K, device="cuda", generator=g)
+    w = torch.randn(N, K, device="cuda", generator=g) * 0.05
+    b = torch.randn(N, device="cuda", generator=g)
+    out = torch.empty(M, N, device="cuda")
+    _gemm(x, w, b, out, EPI_F32, False, 0)
+    ref = (x.double() @ w.double().T + b.double()).float()
+    assert (out - ref).abs().max().item() < 1e-4 * (K / 256) ** 0.5
+
+
+def test_tcgen05_split_k_counters_self_reset():
+    """Two identical split-K GEMMs through one workspace give identical results."""
+    x = torch.randn(3, 4096, device="cuda").bfloat16()
+    w = (torch.randn(512, 4096, device="cuda") * 0.02).bfloat16()
+    o1 = torch.empty(3, 512, device="cuda")
+    o2 = torch.empty(3, 512, device="cuda")
+    _gemm(x, w, None, o1, EPI_F32, True, 1)
+    _gemm(x, w, None, o2, EPI_F32, True, 1)
+    assert torch.equal(o1, o2)
+
+
+def test_shuffle_kernel_bit_exact():
+    from paper_2305_13484_b200.executor import CudaExecutor
+    from paper_2305_13484_b200.models import get_spec
+    spec = get_spec("gpt2-mini")
+    ex = CudaExecutor(spec, {}, dtype="bf16", pool_slots=8, max_seq=40, max_new_tokens=8)
+    ex.kv.copy_(torch.randn_like(ex.kv, dtype=torch.float32).bfloat16())
+    before = ex.kv.clone()
+    moves = [(6, 1, 33), (7, 2, 5), (0, 3, 40)]
+    flat = (C.c_int32 * 9)(*[v for m in moves for v in m])
+    _lib.check(ex.lib.fl_shuffle(ex.handle, flat, 3, C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    ref = before.clone()
+    for s, d, n in moves:
+        ref[:, d, :, :, :n] = before[:, s, :, :, :n]
+    assert torch.equal(ex.kv, ref)
+    ex.close()
