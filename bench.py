@@ -1,0 +1,427 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 temporally fused decode loop (Flover, arXiv 2305.13484).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+Metric (BASELINE.json): decode tokens/s + p50/p99 request latency under Poisson
+arrivals.  One *step* = one complete serve of the config's request stream
+(every request from arrival to eviction) through the drop-in API
+(``run_fusion``-style FusionStream + CudaExecutor) with the DEVICE clock: the
+stream's ``now`` advances by the CUDA-event time of each real fused iteration
+and shuffle, arrivals come from the reference generator, idle gaps are
+skipped (engine.py:200-201).
+
+* value     -- generated tokens of all timed steps / CUDA-event time of the
+               timed region (host bookkeeping between launches included);
+* e2e       -- the same through the public API with host buffers: prompts
+               uploaded from host memory and every step's generated token ids
+               read back to the host inside the timed region;
+* latency   -- p50/p99 of (evicted - arrived) on the device clock
+               (metrics.percentile, reference metrics.py:16-28);
+* roofline  -- live CUDA-event time of the dominant kernel class vs its
+               algorithmic bytes, against MEASURED_PEAKS.json;
+* cpu_baseline -- the CPU port of the same path (schedule oracle + numpy model
+               oracle) on a bounded sample on this host's cores.
+
+``--impl reference`` times that CPU path alone (there is no GPU reference:
+the reference is a pure-Python simulator with no model math).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "c1": dict(workload="C1: tiny GPT (4L, d=256, 4 heads) fp32, 32 Poisson requests (mean gap 20 ms), "
+                        "U(8,64) outputs, input_len 16", spec="tiny", n=32, mean=20.0, lo=8, hi=64,
+               max_out=64, input_len=16, dtype="f32", pool=64),
+    "c2": dict(workload="C2: GPT-2 small (12L, d=768, 12 heads) bf16, 128 Poisson requests (mean gap "
+                        "20 ms), U(32,512) outputs, input_len 32, 1 B200", spec="gpt2-small", n=128,
+               mean=20.0, lo=32, hi=512, max_out=512, input_len=32, dtype="bf16", pool=160),
+    "c3": dict(workload="C3: GPT-J 6B shape (28L, d=4096, 16 heads) bf16, 512 Poisson requests (mean gap "
+                        "20 ms), U(128,1024) outputs, input_len 32, tensor-parallel", spec="gptj-6b",
+               n=512, mean=20.0, lo=128, hi=1024, max_out=1024, input_len=32, dtype="bf16", pool=192),
+    "c4": dict(workload="C4: GPT-NeoX 20B shape (44L, d=6144, 64 heads) bf16, 64 Poisson requests, "
+                        "U(128,1024) outputs (long, shuffle-heavy), input_len 32", spec="neox-20b",
+               n=64, mean=20.0, lo=128, hi=1024, max_out=1024, input_len=32, dtype="bf16", pool=72),
+}
+
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d, "measured"
+    except Exception:
+        return dict(FALLBACK_PEAKS), "fallback"
+
+
+def cpu_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, val in zip(self.NAMES, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        under = [v for v in sm if v > 500] or sm
+        return {"sm_mhz": statistics.median(under) if under else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------- workload
+def make_requests(cfg, seed):
+    import paper_2305_13484_b200 as fl
+    sc = fl.Scenario(cfg["spec"], fl.Discipline.FUSION, cfg["n"], fl.PoissonArrival(cfg["mean"]),
+                     fl.UniformLength(cfg["lo"], cfg["hi"]), cfg["max_out"],
+                     input_len=cfg["input_len"])
+    return fl.build_requests(sc, seed)
+
+
+def cpu_port_sample(cfg, seed, budget_s):
+    """The reference's CPU path restated (oracle/): the fused schedule of the
+    reference loop (cost clock, reference CostParams) driving the numpy model
+    oracle, for as many iterations as fit in ``budget_s``.  Returns
+    (decode tokens, seconds, iterations, threads)."""
+    import numpy as np
+    import torch
+
+    import paper_2305_13484_b200 as fl
+    from oracle import schedule_oracle as so
+    from oracle.model_oracle import GPTOracle
+    from paper_2305_13484_b200.models import get_spec, init_weights
+
+    spec = get_spec(cfg["spec"])
+    reqs = make_requests(cfg, seed)
+    prompts = fl.synthetic_prompts(reqs, spec.vocab, seed)
+    oreq = [so.Req(r.request_id, r.batch_size, r.input_len, r.max_output_length,
+                   r.actual_output_length, r.arrival_time) for r in reqs]
+    sched = so.fused_schedule(oreq, so.Cost(), record_tokens=False)
+    w = init_weights(spec, seed=0, device="cpu", dtype=torch.float32)
+    w = {k: v.numpy() for k, v in w.items()}
+    orc = GPTOracle.from_spec(spec, w, cfg["input_len"] + cfg["max_out"] - 1)
+    gen = {}
+    last = {}
+    toks = 0
+    t0 = time.perf_counter()
+    n_it = 0
+    for rec in sched.iters:
+        rows, want, rids = [], [], []
+        new = {rid for rid, _ in rec.admitted}
+        for _, rid in rec.rows:
+            if rid is None:
+                continue
+            P = len(prompts[rid])
+            c = gen.get(rid, 0)
+            if rid in new:
+                rows.extend((rid, j, prompts[rid][j]) for j in range(P - 1))
+                tok = prompts[rid][P - 1]
+            else:
+                tok = last[rid]
+            want.append(len(rows))
+            rows.append((rid, P - 1 + c, tok))
+            rids.append(rid)
+        lg = orc.step(rows, want_logits=want)
+        for k, rid in enumerate(rids):
+            last[rid] = int(np.argmax(lg[k]))
+            gen[rid] = gen.get(rid, 0) + 1
+        for rid in rec.finished:
+            orc.release(rid)
+        toks += len(rids)
+        n_it += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    return toks, time.perf_counter() - t0, n_it, cpu_cores()
+
+
+# ----------------------------------------------------------------- reference arm
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    for _ in range(args.warmup):
+        cpu_port_sample(cfg, args.seed, args.ref_budget)
+    toks = secs = 0.0
+    iters = []
+    for _ in range(args.steps):
+        t, s, n, cores = cpu_port_sample(cfg, args.seed, args.ref_budget)
+        toks += t
+        secs += s
+        iters.append(n)
+    v = toks / secs
+    line = {
+        "impl": "reference", "metric": "decode tokens/s (Poisson arrivals, fused decode loop)",
+        "value": v, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000.0 * secs / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (reference request generator, seeded prompts, random-init weights)",
+        "config": {"workload": cfg["workload"], "model": cfg["spec"], "requests": cfg["n"],
+                   "sample": f"first {min(iters)}-{max(iters)} iterations of the reference schedule"},
+        "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cpu_cores(), "kind": "port",
+                         "sample": f"oracle/ schedule restatement + numpy fp32 model oracle, "
+                                   f"first ~{max(iters)} fused iterations per step "
+                                   f"({args.ref_budget:.0f} s budget)"},
+        "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- our arm
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2305_13484_b200 as fl
+    from paper_2305_13484_b200.executor import CudaExecutor
+    from paper_2305_13484_b200.models import get_spec
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    comm_id = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        from paper_2305_13484_b200.tp import make_comm_id
+        comm_id = make_comm_id(rank)
+    spec = get_spec(cfg["spec"])
+    reqs = make_requests(cfg, args.seed)
+    prompts = fl.synthetic_prompts(reqs, spec.vocab, args.seed)
+    params = fl.CostParams(preprocess_ms=0.0)   # prefill runs inside the fused step
+    ex = CudaExecutor(spec, prompts, dtype=cfg["dtype"], pool_slots=cfg["pool"],
+                      input_len=cfg["input_len"], max_new_tokens=cfg["max_out"],
+                      state_slots=max(1024, cfg["n"]), tp_rank=rank, tp_size=world,
+                      comm_id=comm_id, seed=0)
+    if world > 1:
+        from paper_2305_13484_b200.tp import max_reduce_clock
+        ex.clock_reduce = max_reduce_clock(local)
+
+    def serve(read_tokens=False):
+        ex.reset()
+        st = fl.FusionStream(reqs, params, fl.TPConfig(tp_size=world), shuffle_enabled=True,
+                             record_tokens=True, executor=ex, clock="device")
+        fl.drive(st)
+        toks = ex.tokens() if read_tokens else None
+        return st, toks
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        serve()
+    # ---- timed region (device-resident inputs)
+    barrier()
+    torch.cuda.synchronize()
+    ex.profile(True)
+    l0 = ex.launches()
+    ctx0, rows0, it0, mv0 = ex.attn_ctx_rows, ex.rows_total, ex.iterations, ex.moved_kv_bytes
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    streams = []
+    with ClockSampler(local) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            st, _ = serve()
+            streams.append(st)
+        e1.record()
+        torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    launches = ex.launches() - l0
+    prof = ex.profile_read()
+    ex.profile(False)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    tokens = sum(r.actual_output_length for r in reqs) * args.steps
+    value = tokens / (ms / 1000.0)
+    iters = ex.iterations - it0
+    lat = [fl.compute_metrics(fl.Trace("fusion", s.events), len(reqs)) for s in streams]
+
+    # ---- end to end through the public API with host buffers
+    barrier()
+    torch.cuda.synchronize()
+    h0 = ex.h2d_bytes
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    d2h = 0
+    e2.record()
+    for _ in range(args.steps):
+        _, toks = serve(read_tokens=True)
+        d2h += ex.d2h_bytes
+    e3.record()
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = e2.elapsed_time(e3)
+    h2d = (ex.h2d_bytes - h0 + sum(4 * len(p) for p in prompts.values()) * args.steps)
+
+    # ---- roofline of the dominant kernel class
+    peaks, peak_src = load_peaks()
+    hbm = float(peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"]))
+    tf_sus = float(peaks.get("bf16_tflops_sustained", FALLBACK_PEAKS["bf16_tflops_sustained"]))
+    att_bytes = ex.attention_bytes() * 1.0
+    # attention_bytes() is cumulative since construction: scale to the timed region
+    frac_rows = (ex.attn_ctx_rows - ctx0) / max(1, ex.attn_ctx_rows)
+    es = 2 if cfg["dtype"] == "bf16" else 4
+    hl = spec.n_head // world
+    att_bytes = spec.n_layer * ((ex.attn_ctx_rows - ctx0) * 2 * hl * spec.head_dim * es
+                                + (ex.rows_total - rows0) * 2 * hl * spec.head_dim * es)
+    kern = {}
+    a = prof["attention"]
+    if a["records"]:
+        kern["attention"] = {"bound": "hbm", "records": a["records"], "ms": a["ms"],
+                             "bytes_per_launch": att_bytes / a["records"],
+                             "achieved": att_bytes / (a["ms"] / 1e3) / 1e9, "peak": hbm,
+                             "unit": "GB/s"}
+    g = prof["gemm"]
+    if g["records"]:
+        kern["gemm"] = {"bound": "hbm", "records": g["records"], "ms": g["ms"],
+                        "bytes_per_launch": g["bytes"] / g["records"],
+                        "achieved": g["bytes"] / (g["ms"] / 1e3) / 1e9, "peak": hbm, "unit": "GB/s"}
+    sh = prof["shuffle"]
+    if sh["records"]:
+        mv = ex.moved_kv_bytes - mv0
+        kern["shuffle"] = {"bound": "hbm", "records": sh["records"], "ms": sh["ms"],
+                           "bytes_per_launch": mv / sh["records"],
+                           "achieved": mv / (sh["ms"] / 1e3) / 1e9, "peak": hbm, "unit": "GB/s"}
+    for k in kern.values():
+        k["frac"] = k["achieved"] / k["peak"]
+        k["share_of_step"] = k["ms"] / max(prof["step"]["ms"] + sh["ms"], 1e-9)
+    dom_name = max(kern, key=lambda k: kern[k]["ms"]) if kern else None
+    dom = kern.get(dom_name, {})
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(dom_name)
+        except Exception:
+            traffic = None
+    roofline = {"kernel": dom_name, "bound": dom.get("bound"), "achieved": dom.get("achieved"),
+                "peak": dom.get("peak"), "unit": dom.get("unit"), "frac": dom.get("frac"),
+                "traffic": traffic, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": dom.get("bytes_per_launch")}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        t, s, n, cores = cpu_port_sample(cfg, args.seed, args.cpu_budget)
+        cpu = {"value": t / s, "unit": "tokens/s", "cores": cores, "kind": "port",
+               "sample": f"oracle/ schedule restatement + numpy fp32 model oracle, first {n} "
+                         f"fused iterations of the same request stream ({t} decode tokens, {s:.1f} s)"}
+
+    if rank == 0:
+        c = clk.summary()
+        line = {
+            "metric": "decode tokens/s (Poisson arrivals, fused decode loop)", "value": value,
+            "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": cfg["dtype"],
+            "data": "synthetic (reference Poisson request generator, seeded prompts, random-init "
+                    "weights)",
+            "config": {"workload": cfg["workload"], "model": cfg["spec"], "requests": cfg["n"],
+                       "parallelism": f"tp{world}", "clock": "device",
+                       "l2": "KV + weights per step exceed L2 (126 MB); no flush",
+                       "step": "one complete serve of the request stream"},
+            "latency_ms": {"p50": statistics.fmean(m.p50_latency_ms for m in lat),
+                           "p99": statistics.fmean(m.p99_latency_ms for m in lat),
+                           "mean": statistics.fmean(m.mean_latency_ms for m in lat)},
+            "iterations_per_step": iters / args.steps,
+            "mean_rows_per_iteration": (ex.rows_total - rows0) / max(1, iters),
+            "e2e": {"value": tokens / (e2e_ms / 1000.0), "unit": "tokens/s",
+                    "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps},
+            "gpu_launches": launches,
+            "roofline": roofline,
+            "kernels": kern,
+            "cpu_baseline": cpu,
+            "clocks": c,
+        }
+        print(json.dumps(line), flush=True)
+    ex.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--ref-budget", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.config is None:
+        args.config = "c2" if args.gpus == 1 else "c3"
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

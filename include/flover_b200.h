@@ -153,6 +153,21 @@ int fl_shuffle(fl_handle* h, const int32_t* moves, int n, void* cuda_stream);
 /* Number of kernels fl_step / fl_shuffle launched since fl_create. */
 int64_t fl_kernel_launches(const fl_handle* h);
 
+/* Live kernel timing (CUDA events on the launch stream, bracketing each launch
+ * group) for roofline reporting.  Classes: */
+enum fl_prof_class {
+  FL_PROF_ATTENTION = 0, /* K4 split + combine, one record per layer          */
+  FL_PROF_GEMM = 1,      /* K3/K5/K6/K7/K8, one record per GEMM                */
+  FL_PROF_SHUFFLE = 2,   /* K10, one record per fl_shuffle                     */
+  FL_PROF_STEP = 3,      /* the whole fl_step                                  */
+  FL_PROF_CLASSES = 4
+};
+int fl_profile(fl_handle* h, int enable);
+/* Drains pending records (synchronises on them) and returns the totals since the
+ * last fl_profile(h, 1): summed milliseconds, launch records and algorithmic
+ * bytes (GEMM: weights + activations in + out; other classes report 0). */
+int fl_profile_read(fl_handle* h, int cls, double* total_ms, int64_t* records, double* bytes);
+
 /* Diagnostic entry for kernel-level parity tests: one projection GEMM
  * out[M,N] (=|+=) X[M,K] . W[N,K]^T + bias through the same kernels fl_step
  * uses (use_tc: 1 tcgen05, 0 SIMT).  epi: 0 store(dtype) 1 gelu(dtype)

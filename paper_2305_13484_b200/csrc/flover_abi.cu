@@ -93,7 +93,49 @@ struct fl_handle {
   fl::TcWorkspace tcws;
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;
+  // live profiling
+  struct Rec { int cls; cudaEvent_t a, b; double bytes; };
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<Rec> pending;
+  double tot_ms[FL_PROF_CLASSES] = {};
+  double tot_bytes[FL_PROF_CLASSES] = {};
+  int64_t tot_n[FL_PROF_CLASSES] = {};
+  cudaEvent_t ev() {
+    if (ev_pool.empty()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      return e;
+    }
+    cudaEvent_t e = ev_pool.back();
+    ev_pool.pop_back();
+    return e;
+  }
 };
+
+namespace {
+// Brackets a group of launches with a pair of events when profiling is on.
+struct ProfScope {
+  fl_handle* h;
+  int cls;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr;
+  double bytes = 0;
+  ProfScope(fl_handle* h_, int c, cudaStream_t st) : h(h_), cls(c), s(st) {
+    if (h->prof) {
+      a = h->ev();
+      cudaEventRecord(a, s);
+    }
+  }
+  ~ProfScope() {
+    if (a) {
+      cudaEvent_t b = h->ev();
+      cudaEventRecord(b, s);
+      h->pending.push_back({cls, a, b, bytes});
+    }
+  }
+};
+}  // namespace
 
 namespace {
 
@@ -231,6 +273,11 @@ int fl_create(const fl_model_desc* m, const fl_pool_desc* p, fl_handle** out) {
 int fl_destroy(fl_handle* h) {
   if (!h) return FL_OK;
   if (h->comm && g_nccl.commDestroy) g_nccl.commDestroy(h->comm);
+  for (auto& r : h->pending) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (auto e : h->ev_pool) cudaEventDestroy(e);
   fl::tc_destroy(&h->tcws);
   delete h;
   return FL_OK;
@@ -262,6 +309,37 @@ int fl_comm_init(fl_handle* h, const void* idp, int rank, int world) {
 
 int64_t fl_kernel_launches(const fl_handle*) { return fl::g_launches.load(); }
 
+int fl_profile(fl_handle* h, int enable) {
+  if (!h) return fail(FL_EINVAL, "null handle");
+  for (auto& r : h->pending) {
+    h->ev_pool.push_back(r.a);
+    h->ev_pool.push_back(r.b);
+  }
+  h->pending.clear();
+  for (int c = 0; c < FL_PROF_CLASSES; ++c) h->tot_ms[c] = h->tot_bytes[c] = 0, h->tot_n[c] = 0;
+  h->prof = enable != 0;
+  return FL_OK;
+}
+
+int fl_profile_read(fl_handle* h, int cls, double* total_ms, int64_t* records, double* bytes) {
+  if (!h || cls < 0 || cls >= FL_PROF_CLASSES) return fail(FL_EINVAL, "bad profile query");
+  for (auto& r : h->pending) {
+    FL_CUDA(cudaEventSynchronize(r.b));
+    float ms = 0.f;
+    FL_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+    h->tot_ms[r.cls] += ms;
+    h->tot_bytes[r.cls] += r.bytes;
+    h->tot_n[r.cls] += 1;
+    h->ev_pool.push_back(r.a);
+    h->ev_pool.push_back(r.b);
+  }
+  h->pending.clear();
+  if (total_ms) *total_ms = h->tot_ms[cls];
+  if (records) *records = h->tot_n[cls];
+  if (bytes) *bytes = h->tot_bytes[cls];
+  return FL_OK;
+}
+
 }  // extern "C"
 
 namespace {
@@ -272,6 +350,10 @@ int gemm(fl_handle* h, const void* x, int ldx, const void* w, const void* bias, 
           int ldo, int M, int N, int K, int epi, cudaStream_t s) {
   GemmArgs a{x, w, bias, out, M, N, K, ldx, ldo, epi, h->m.dtype, h->p.max_rows};
   fl::g_launches += 1;
+  ProfScope ps(h, FL_PROF_GEMM, s);
+  const double oes = (epi == fl::EPI_STORE || epi == fl::EPI_GELU) ? h->es : 4.0;
+  ps.bytes = (double)N * K * h->es + (double)M * K * h->es + (double)M * N * oes *
+             (epi == fl::EPI_ACC_F32 ? 2.0 : 1.0);
   if (h->p.use_tensor_cores) return fl::gemm_tc(&h->tcws, a, s) ? FL_ECUDA : FL_OK;
   fl::gemm_simt(a, s);
   return FL_OK;
@@ -311,6 +393,7 @@ extern "C" int fl_step(fl_handle* h, const fl_row* rows, int n_rows, int n_dec, 
   }
   const size_t kv_layer_elems = (size_t)p.pool_slots * 2 * Hl * p.max_seq * hd;
   char* kv = static_cast<char*>(p.kv);
+  ProfScope step_scope(h, FL_PROF_STEP, s);
 
   fl::launch_embed(h->rows, n_rows, p.req_tok, p.req_pos, p.req_ngen, p.state_slots, m.wte, m.wpe,
                    d, dt, h->x, h->row_tok, h->row_pos, h->row_ctx, s);
@@ -324,8 +407,11 @@ extern "C" int fl_step(fl_handle* h, const fl_row* rows, int n_rows, int n_dec, 
     fl::launch_rope_append(h->qkv, h->rows, h->row_pos, n_rows, Hl, hd, m.rotary_dim, m.family, kvl,
                            p.pool_slots, p.max_seq, h->q, dt, s);
     // K4
+    {
+    ProfScope ps(h, FL_PROF_ATTENTION, s);
     fl::launch_attention(h->q, h->rows, h->row_ctx, n_rows, Hl, hd, kvl, p.pool_slots, p.max_seq,
                          h->a, h->att_o, h->att_ml, dt, s);
+    }
     fl::g_launches += 3 + (h->ms > 1 ? 1 : 0);
     // MLP input: GPT-2 = LN2 of the updated residual; GPT-J = LN1 output;
     // NeoX = LN2 of the residual *before* the attention update.
@@ -392,6 +478,7 @@ extern "C" int fl_shuffle(fl_handle* h, const int32_t* moves, int n, void* strea
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   FL_CUDA(cudaMemcpyAsync(h->moves, moves, sizeof(int32_t) * 3 * n, cudaMemcpyHostToDevice, s));
+  ProfScope ps(h, FL_PROF_SHUFFLE, s);
   fl::launch_shuffle(h->moves, n, h->p.kv, h->m.n_layer, h->p.pool_slots, h->Hl, h->p.max_seq,
                      h->m.head_dim, h->m.dtype, s);
   fl::g_launches += 1;
@@ -413,12 +500,12 @@ extern "C" int fl_gemm(const void* x, int ldx, const void* w, const void* bias, 
   fl::GemmArgs a{x, w, bias, out, M, N, K, ldx, ldo, epi, dtype, M};
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (use_tc) {
-    if (g_dbg_base != workspace) {
-      if (g_dbg_base) fl::tc_destroy(&g_dbg_ws);
-      if (fl::tc_init(&g_dbg_ws, workspace, fl::tc_workspace_bytes(0, 0)))
-        return fail(FL_ECUDA, "%s", fl::tc_last_error());
-      g_dbg_base = workspace;
-    }
+    // the caller's scratch may have been reused by the allocator: re-arm the
+    // split-K counters every call (diagnostic path only)
+    if (g_dbg_base) fl::tc_destroy(&g_dbg_ws);
+    if (fl::tc_init(&g_dbg_ws, workspace, fl::tc_workspace_bytes(0, 0)))
+      return fail(FL_ECUDA, "%s", fl::tc_last_error());
+    g_dbg_base = workspace;
     if (fl::gemm_tc(&g_dbg_ws, a, s)) return fail(FL_EINVAL, "%s", fl::tc_last_error());
   } else {
     fl::gemm_simt(a, s);

@@ -140,6 +140,27 @@ class CudaExecutor:
         self.shuffles = 0
         self.moved_kv_bytes = 0
         self.seen = []
+        self.h2d_bytes = 0
+        self.d2h_bytes = 0
+        self.attn_ctx_rows = 0            # sum over iterations of sum_rows ctx_r
+        self._live_ctx = 0                # sum over live requests of (P + gen)
+        self._orphan_ctx = 0
+        self._prefill_ctx = 0
+        self.clock_reduce = None          # callable(ms) -> ms agreed across TP ranks
+
+    def reset(self):
+        """Forget host bookkeeping between independent runs (device buffers,
+        weights and the KV pool are reused; request state is re-armed at
+        admission)."""
+        self._new, self._live, self._orphans = [], {}, {}
+        self._prev_had_new = False
+        self._rows_version = None
+        self._rows = None
+        self._n_rows = self._n_dec = 0
+        self._live_ctx = self._orphan_ctx = self._prefill_ctx = 0
+        self.seen = []
+        self.logits_log = []
+        self._events = []
 
     # ----------------------------------------------------------------- utils
     @property
@@ -175,11 +196,14 @@ class CudaExecutor:
             if other % self.R == rid % self.R:
                 raise CapacityExceeded(f"state ring collision between requests {rid} and {other}")
         self._live[rid] = {"P": P, "stop": stop, "gen": 0}
+        self._live_ctx += P
+        self._prefill_ctx += (P - 1) * P // 2
         self._new.append(rid)
         self.seen.append(rid)
 
     def on_evict(self, rid, slot):
         info = self._live.pop(rid)
+        self._live_ctx -= info["P"] + info["gen"]
         # KV positions written: prefill 0..P-2 plus one per generated token
         self._orphans[slot] = info["P"] + info["stop"] - 1
 
@@ -220,6 +244,11 @@ class CudaExecutor:
         if changed:
             self._rows, self._n_rows, self._n_dec = self._build_rows(layout)
             self._rows_version = layout.version
+            self.h2d_bytes += self._n_rows * C.sizeof(_lib.Row)
+            self._orphan_ctx = sum(r.ctx for r in self._rows[:self._n_dec] if r.kind == _lib.ROW_ORPHAN)
+        self.attn_ctx_rows += self._live_ctx + self._orphan_ctx + (self._prefill_ctx if has_new else 0)
+        if has_new:
+            self._prefill_ctx = 0
         cs = self.stream
         timed = stream.clock == "device" or self.time_steps
         if timed:
@@ -246,11 +275,13 @@ class CudaExecutor:
         self._new = []
         for info in self._live.values():
             info["gen"] += 1
+        self._live_ctx += len(self._live)
         if timed:
             e1.record(cs)
             if stream.clock == "device":
                 e1.synchronize()
-                return e0.elapsed_time(e1)
+                ms = e0.elapsed_time(e1)
+                return self.clock_reduce(ms) if self.clock_reduce else ms
             self._events.append((e0, e1))
         return None
 
@@ -263,6 +294,7 @@ class CudaExecutor:
             self.moved_kv_bytes += 2 * ctx * self.spec.kv_bytes_per_token(
                 2 if self.dtype == "bf16" else 4, self.tp_size)
         flat = (C.c_int32 * (3 * len(moves)))(*[v for mv in moves for v in mv])
+        self.h2d_bytes += 12 * len(moves)
         cs = self.stream
         e0 = e1 = None
         if self.time_steps or getattr(self, "_device_clock", False):
@@ -276,7 +308,8 @@ class CudaExecutor:
         if e0 is not None:
             e1.record(cs)
             e1.synchronize()
-            return e0.elapsed_time(e1)
+            ms = e0.elapsed_time(e1)
+            return self.clock_reduce(ms) if self.clock_reduce else ms
         return None
 
     def on_drain(self, stream):
@@ -288,12 +321,33 @@ class CudaExecutor:
         return [a.elapsed_time(b) for a, b in self._events]
 
     def tokens(self, rids=None) -> dict:
-        """rid -> generated token ids (device history, one D2H copy)."""
+        """rid -> generated token ids: one gather on the device, one D2H copy
+        of exactly the requested histories (counted in ``d2h_bytes``)."""
         rids = list(self.seen if rids is None else rids)
-        hist = self.tok_hist.cpu()
-        ngen = self.req_ngen.cpu()
+        if not rids:
+            return {}
+        idx = torch.tensor([r % self.R for r in rids], device=self.device, dtype=torch.long)
+        packed = torch.cat([self.req_ngen[idx].unsqueeze(1), self.tok_hist[idx]], dim=1).cpu()
+        self.d2h_bytes = packed.numel() * 4
+        return {rid: packed[i, 1:1 + int(packed[i, 0])].tolist() for i, rid in enumerate(rids)}
+
+    def attention_bytes(self) -> float:
+        """Algorithmic HBM bytes of K4 summed over all launches so far:
+        K and V of every row's context plus q in / out."""
+        es = 2 if self.dtype == "bf16" else 4
+        hl = self.spec.n_head // self.tp_size
+        per_pos = 2 * hl * self.spec.head_dim * es
+        return float(self.spec.n_layer) * (self.attn_ctx_rows * per_pos
+                                           + self.rows_total * 2 * hl * self.spec.head_dim * es)
+
+    def profile(self, enable: bool):
+        _lib.check(self.lib.fl_profile(self.handle, int(enable)))
+
+    def profile_read(self) -> dict:
         out = {}
-        for rid in rids:
-            q = rid % self.R
-            out[rid] = hist[q, :int(ngen[q])].tolist()
+        for name, cls in (("attention", _lib.PROF_ATTENTION), ("gemm", _lib.PROF_GEMM),
+                          ("shuffle", _lib.PROF_SHUFFLE), ("step", _lib.PROF_STEP)):
+            ms, n, b = C.c_double(), C.c_int64(), C.c_double()
+            _lib.check(self.lib.fl_profile_read(self.handle, cls, C.byref(ms), C.byref(n), C.byref(b)))
+            out[name] = {"ms": ms.value, "records": n.value, "bytes": b.value}
         return out
