@@ -162,6 +162,10 @@ enum fl_prof_class {
   FL_PROF_STEP = 3,      /* the whole fl_step                                  */
   FL_PROF_CLASSES = 4
 };
+/* Execution options: use_graphs (default 1) replays each (rows, window) shape
+ * of fl_step as one CUDA graph; profile_every (default 8) samples one step in N
+ * with event-bracketed launch groups while profiling is enabled. */
+int fl_configure(fl_handle* h, int use_graphs, int profile_every);
 int fl_profile(fl_handle* h, int enable);
 /* Drains pending records (synchronises on them) and returns the totals since the
  * last fl_profile(h, 1): summed milliseconds, launch records and algorithmic

@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "../../include/flover_b200.h"
 
 #define FL_DEV __device__ __forceinline__
@@ -104,9 +106,45 @@ FL_DEV int argmax_key_index(unsigned long long k) {
   return static_cast<int>(0xFFFFFFFFu - static_cast<uint32_t>(k & 0xFFFFFFFFull));
 }
 
+// Programmatic dependent launch: every kernel of the step lets its successor
+// start its prologue early (launch_dependents) and waits for its
+// predecessor's results (wait) before touching them.  Both are no-ops when a
+// kernel is launched without the PDL attribute.
+FL_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+FL_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // Row descriptor resolved on the device for every kernel of the step.
 struct RowInfo {
   int slot, rid, pos, tok, kind, ctx;
 };
+
+// Host: launch with the PDL attribute (and an optional cluster along z).
+extern bool g_use_pdl;
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                            cudaStream_t s, unsigned cluster_z, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  unsigned n = 0;
+  if (g_use_pdl) {
+    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  if (cluster_z > 1) {
+    at[n].id = cudaLaunchAttributeClusterDimension;
+    at[n].val.clusterDim.x = 1;
+    at[n].val.clusterDim.y = 1;
+    at[n].val.clusterDim.z = cluster_z;
+    ++n;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
 
 }  // namespace fl

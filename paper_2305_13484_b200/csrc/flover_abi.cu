@@ -18,8 +18,11 @@
 #include <nccl.h>
 
 #include <atomic>
+#include <map>
+#include <tuple>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -77,6 +80,7 @@ size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
 namespace fl {
 std::atomic<int64_t> g_launches{0};
+bool g_use_pdl = getenv("FL_NO_PDL") == nullptr;
 }
 
 struct fl_handle {
@@ -101,7 +105,24 @@ struct fl_handle {
   double tot_ms[FL_PROF_CLASSES] = {};
   double tot_bytes[FL_PROF_CLASSES] = {};
   int64_t tot_n[FL_PROF_CLASSES] = {};
+  // CUDA graphs of the step, keyed by (n_rows, n_dec, logits, profiled)
+  struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    std::vector<Rec> recs;   // event pairs baked into a profiled graph
+    bool pending = false;    // recs hold an unread replay
+  };
+  std::map<std::tuple<int, int, int, int>, GraphEntry> graphs;
+  bool use_graphs = true;
+  int prof_every = 8;
+  int64_t step_counter = 0;
+  std::vector<Rec>* sink = nullptr;   // where ProfScope records go (null: pending)
+  bool capturing = false;
   cudaEvent_t ev() {
+    if (capturing) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      return e;
+    }
     if (ev_pool.empty()) {
       cudaEvent_t e;
       cudaEventCreate(&e);
@@ -114,6 +135,8 @@ struct fl_handle {
 };
 
 namespace {
+void harvest(fl_handle* h, std::vector<fl_handle::Rec>& recs);
+
 // Brackets a group of launches with a pair of events when profiling is on.
 struct ProfScope {
   fl_handle* h;
@@ -131,7 +154,7 @@ struct ProfScope {
     if (a) {
       cudaEvent_t b = h->ev();
       cudaEventRecord(b, s);
-      h->pending.push_back({cls, a, b, bytes});
+      (h->sink ? *h->sink : h->pending).push_back({cls, a, b, bytes});
     }
   }
 };
@@ -176,7 +199,7 @@ Layout plan(const fl_model_desc* m, const fl_pool_desc* p) {
   const int es = m->dtype == FL_DTYPE_BF16 ? 2 : 4;
   const int Hl = m->n_head / m->tp_size, Dl = Hl * m->head_dim, Fl = m->d_ff / m->tp_size;
   const int Vl = (m->vocab + m->tp_size - 1) / m->tp_size;
-  const size_t Mr = p->max_rows, Md = p->pool_slots < p->max_rows ? p->pool_slots : p->max_rows;
+  const size_t Mr = p->max_rows, Md = p->max_rows;   // window rows incl. bucket padding
   const int ms = fl::attn_max_splits(p->max_seq);
   const size_t d = m->d_model;
   Carve c;
@@ -240,6 +263,7 @@ int fl_create(const fl_model_desc* m, const fl_pool_desc* p, fl_handle** out) {
   h->Vl = (m->vocab + m->tp_size - 1) / m->tp_size;
   h->Vloc = m->vocab - m->tp_rank * h->Vl < h->Vl ? m->vocab - m->tp_rank * h->Vl : h->Vl;
   h->ms = fl::attn_max_splits(p->max_seq);
+  h->use_graphs = getenv("FL_NO_GRAPH") == nullptr;
   char* w = static_cast<char*>(p->workspace);
   h->rows = (fl_row*)(w + L.rows);
   h->row_tok = (int32_t*)(w + L.row_tok);
@@ -278,6 +302,13 @@ int fl_destroy(fl_handle* h) {
     cudaEventDestroy(r.b);
   }
   for (auto e : h->ev_pool) cudaEventDestroy(e);
+  for (auto& kv : h->graphs) {
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    for (auto& r : kv.second.recs) {
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+  }
   fl::tc_destroy(&h->tcws);
   delete h;
   return FL_OK;
@@ -309,6 +340,13 @@ int fl_comm_init(fl_handle* h, const void* idp, int rank, int world) {
 
 int64_t fl_kernel_launches(const fl_handle*) { return fl::g_launches.load(); }
 
+int fl_configure(fl_handle* h, int use_graphs, int profile_every) {
+  if (!h || profile_every < 1) return fail(FL_EINVAL, "bad configure arguments");
+  h->use_graphs = use_graphs != 0;
+  h->prof_every = profile_every;
+  return FL_OK;
+}
+
 int fl_profile(fl_handle* h, int enable) {
   if (!h) return fail(FL_EINVAL, "null handle");
   for (auto& r : h->pending) {
@@ -316,13 +354,21 @@ int fl_profile(fl_handle* h, int enable) {
     h->ev_pool.push_back(r.b);
   }
   h->pending.clear();
+  for (auto& kv : h->graphs) kv.second.pending = false;
   for (int c = 0; c < FL_PROF_CLASSES; ++c) h->tot_ms[c] = h->tot_bytes[c] = 0, h->tot_n[c] = 0;
   h->prof = enable != 0;
+  h->step_counter = 0;
   return FL_OK;
 }
 
 int fl_profile_read(fl_handle* h, int cls, double* total_ms, int64_t* records, double* bytes) {
   if (!h || cls < 0 || cls >= FL_PROF_CLASSES) return fail(FL_EINVAL, "bad profile query");
+  for (auto& kv : h->graphs) {
+    if (kv.second.pending) {
+      harvest(h, kv.second.recs);
+      kv.second.pending = false;
+    }
+  }
   for (auto& r : h->pending) {
     FL_CUDA(cudaEventSynchronize(r.b));
     float ms = 0.f;
@@ -349,9 +395,14 @@ using fl::GemmArgs;
 int gemm(fl_handle* h, const void* x, int ldx, const void* w, const void* bias, void* out,
           int ldo, int M, int N, int K, int epi, cudaStream_t s) {
   GemmArgs a{x, w, bias, out, M, N, K, ldx, ldo, epi, h->m.dtype, h->p.max_rows};
+  if (epi == fl::EPI_ARGMAX) {
+    a.keys = h->keys;
+    a.index_base = h->m.tp_rank * h->Vl;
+  }
   fl::g_launches += 1;
   ProfScope ps(h, FL_PROF_GEMM, s);
-  const double oes = (epi == fl::EPI_STORE || epi == fl::EPI_GELU) ? h->es : 4.0;
+  const double oes = (epi == fl::EPI_STORE || epi == fl::EPI_GELU) ? h->es
+                     : epi == fl::EPI_ARGMAX ? 0.0 : 4.0;
   ps.bytes = (double)N * K * h->es + (double)M * K * h->es + (double)M * N * oes *
              (epi == fl::EPI_ACC_F32 ? 2.0 : 1.0);
   if (h->p.use_tensor_cores) return fl::gemm_tc(&h->tcws, a, s) ? FL_ECUDA : FL_OK;
@@ -367,52 +418,43 @@ int allreduce_f32(fl_handle* h, float* buf, size_t n, cudaStream_t s) {
 
 }  // namespace
 
-extern "C" int fl_step(fl_handle* h, const fl_row* rows, int n_rows, int n_dec, int rows_changed,
-                       float* logits_out, void* stream) {
-  if (!h) return fail(FL_EINVAL, "null handle");
-  if (n_rows < 1 || n_dec < 0 || n_dec > n_rows) return fail(FL_EINVAL, "bad row counts");
-  if (n_rows > h->p.max_rows) return fail(FL_ECAPACITY, "%d rows > max_rows %d", n_rows, h->p.max_rows);
-  if (n_dec > h->p.pool_slots) return fail(FL_ECAPACITY, "window %d > pool %d", n_dec, h->p.pool_slots);
-  if (h->m.tp_size > 1 && !h->comm) return fail(FL_EINVAL, "tp_size > 1 needs fl_comm_init");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+namespace {
+
+// The launch sequence of one fused iteration (captured into a CUDA graph).
+int enqueue_step(fl_handle* h, int n_rows, int n_dec, bool want_logits, cudaStream_t s) {
   const fl_model_desc& m = h->m;
   const fl_pool_desc& p = h->p;
   const int d = m.d_model, hd = m.head_dim, L = m.n_layer, dt = m.dtype, es = h->es;
   const int Hl = h->Hl, Dl = h->Dl, Fl = h->Fl;
   const bool tp = m.tp_size > 1;
-  if (rows_changed) {
-    if (!rows) return fail(FL_EINVAL, "rows_changed with null rows");
-    for (int i = 0; i < n_rows; ++i) {
-      const fl_row& r = rows[i];
-      if (r.slot < 0 || r.slot >= p.pool_slots) return fail(FL_EINVAL, "row %d slot %d", i, r.slot);
-      if (r.kind != FL_ROW_ORPHAN && r.pos >= p.max_seq)
-        return fail(FL_ECAPACITY, "row %d position %d >= max_seq %d", i, r.pos, p.max_seq);
-      if ((r.kind == FL_ROW_PREFILL) != (i >= n_dec)) return fail(FL_EINVAL, "row %d kind order", i);
-    }
-    FL_CUDA(cudaMemcpyAsync(h->rows, rows, sizeof(fl_row) * n_rows, cudaMemcpyHostToDevice, s));
-  }
   const size_t kv_layer_elems = (size_t)p.pool_slots * 2 * Hl * p.max_seq * hd;
   char* kv = static_cast<char*>(p.kv);
+  // greedy argmax fused into the LM-head GEMM epilogue (tensor-core path)
+  const bool fused_argmax = p.use_tensor_cores && !want_logits && n_dec > 0;
   ProfScope step_scope(h, FL_PROF_STEP, s);
+#define FL_GEMM(...) \
+  if (gemm(h, __VA_ARGS__)) return fail(FL_ECUDA, "tensor-core GEMM: %s", fl::tc_last_error())
 
-  fl::launch_embed(h->rows, n_rows, p.req_tok, p.req_pos, p.req_ngen, p.state_slots, m.wte, m.wpe,
-                   d, dt, h->x, h->row_tok, h->row_pos, h->row_ctx, s);
+  fl::launch_embed(h->rows, n_rows, n_dec, p.req_tok, p.req_pos, p.req_ngen, p.state_slots, m.wte,
+                   m.wpe, d, dt, h->x, h->row_tok, h->row_pos, h->row_ctx, h->keys, s);
   fl::g_launches += 1;
+  const int att_keys = fl::attn_keys_per_split(n_rows * Hl, p.max_seq);
   for (int l = 0; l < L; ++l) {
     const void* const* W = m.layers + (size_t)l * FL_W_LAYER_COUNT;
     void* kvl = kv + kv_layer_elems * es * l;
     // K2 + K3
     fl::launch_layernorm(h->x, W[FL_W_LN1_G], W[FL_W_LN1_B], h->h, n_rows, d, m.ln_eps, dt, s);
-    if (gemm(h, h->h, d, W[FL_W_QKV], W[FL_W_QKV_B], h->qkv, 3 * Dl, n_rows, 3 * Dl, d, fl::EPI_STORE, s)) return fail(FL_ECUDA, "tensor-core GEMM: %s", fl::tc_last_error());
+    FL_GEMM(h->h, d, W[FL_W_QKV], W[FL_W_QKV_B], h->qkv, 3 * Dl, n_rows, 3 * Dl, d, fl::EPI_STORE, s);
     fl::launch_rope_append(h->qkv, h->rows, h->row_pos, n_rows, Hl, hd, m.rotary_dim, m.family, kvl,
                            p.pool_slots, p.max_seq, h->q, dt, s);
     // K4
     {
-    ProfScope ps(h, FL_PROF_ATTENTION, s);
-    fl::launch_attention(h->q, h->rows, h->row_ctx, n_rows, Hl, hd, kvl, p.pool_slots, p.max_seq,
-                         h->a, h->att_o, h->att_ml, dt, s);
+      ProfScope ps(h, FL_PROF_ATTENTION, s);
+      fl::g_launches += fl::launch_attention(h->q, h->rows, h->row_ctx, n_rows, Hl, hd, kvl,
+                                             p.pool_slots, p.max_seq, att_keys, h->a, h->att_o,
+                                             h->att_ml, dt, s);
     }
-    fl::g_launches += 3 + (h->ms > 1 ? 1 : 0);
+    fl::g_launches += 2;
     // MLP input: GPT-2 = LN2 of the updated residual; GPT-J = LN1 output;
     // NeoX = LN2 of the residual *before* the attention update.
     if (m.family == FL_FAMILY_NEOX) {
@@ -421,36 +463,41 @@ extern "C" int fl_step(fl_handle* h, const fl_row* rows, int n_rows, int n_dec, 
     }
     // K5 attn-out (+ all-reduce)
     if (tp) {
-      if (gemm(h, h->a, Dl, W[FL_W_O], nullptr, h->y, d, n_rows, d, Dl, fl::EPI_STORE_F32, s)) return fail(FL_ECUDA, "tensor-core GEMM: %s", fl::tc_last_error());
+      FL_GEMM(h->a, Dl, W[FL_W_O], nullptr, h->y, d, n_rows, d, Dl, fl::EPI_STORE_F32, s);
       if (int e = allreduce_f32(h, h->y, (size_t)n_rows * d, s)) return e;
       fl::launch_add_partial(h->x, h->y, W[FL_W_O_B], nullptr, n_rows, d, dt, s);
       fl::g_launches += 1;
     } else {
-      if (gemm(h, h->a, Dl, W[FL_W_O], W[FL_W_O_B], h->x, d, n_rows, d, Dl, fl::EPI_ACC_F32, s)) return fail(FL_ECUDA, "tensor-core GEMM: %s", fl::tc_last_error());
+      FL_GEMM(h->a, Dl, W[FL_W_O], W[FL_W_O_B], h->x, d, n_rows, d, Dl, fl::EPI_ACC_F32, s);
     }
     const void* mlp_in = h->h;  // GPT-J: LN1 output
     if (m.family == FL_FAMILY_GPT2) {
       fl::launch_layernorm(h->x, W[FL_W_LN2_G], W[FL_W_LN2_B], h->h, n_rows, d, m.ln_eps, dt, s);
       fl::g_launches += 1;
     } else if (m.family == FL_FAMILY_NEOX) {
-      mlp_in = h->h2;   // LN2 of the residual before the attention update
+      mlp_in = h->h2;
     }
     // K6 + K7 (+ all-reduce)
-    if (gemm(h, mlp_in, d, W[FL_W_FC], W[FL_W_FC_B], h->f, Fl, n_rows, Fl, d, fl::EPI_GELU, s)) return fail(FL_ECUDA, "tensor-core GEMM: %s", fl::tc_last_error());
+    FL_GEMM(mlp_in, d, W[FL_W_FC], W[FL_W_FC_B], h->f, Fl, n_rows, Fl, d, fl::EPI_GELU, s);
     if (tp) {
-      if (gemm(h, h->f, Fl, W[FL_W_PROJ], nullptr, h->y, d, n_rows, d, Fl, fl::EPI_STORE_F32, s)) return fail(FL_ECUDA, "tensor-core GEMM: %s", fl::tc_last_error());
+      FL_GEMM(h->f, Fl, W[FL_W_PROJ], nullptr, h->y, d, n_rows, d, Fl, fl::EPI_STORE_F32, s);
       if (int e = allreduce_f32(h, h->y, (size_t)n_rows * d, s)) return e;
       fl::launch_add_partial(h->x, h->y, W[FL_W_PROJ_B], nullptr, n_rows, d, dt, s);
       fl::g_launches += 1;
     } else {
-      if (gemm(h, h->f, Fl, W[FL_W_PROJ], W[FL_W_PROJ_B], h->x, d, n_rows, d, Fl, fl::EPI_ACC_F32, s)) return fail(FL_ECUDA, "tensor-core GEMM: %s", fl::tc_last_error());
+      FL_GEMM(h->f, Fl, W[FL_W_PROJ], W[FL_W_PROJ_B], h->x, d, n_rows, d, Fl, fl::EPI_ACC_F32, s);
     }
   }
   if (n_dec > 0) {
     fl::launch_layernorm(h->x, m.lnf_g, m.lnf_b, h->h, n_dec, d, m.ln_eps, dt, s);
-    if (gemm(h, h->h, d, m.w_lm, m.b_lm, h->logits, h->Vl, n_dec, h->Vloc, d, fl::EPI_STORE_F32, s)) return fail(FL_ECUDA, "tensor-core GEMM: %s", fl::tc_last_error());
-    fl::launch_argmax(h->logits, n_dec, h->Vloc, h->Vl, m.tp_rank * h->Vl, h->keys, s);
-    fl::g_launches += 2;
+    fl::g_launches += 1;
+    if (fused_argmax) {
+      FL_GEMM(h->h, d, m.w_lm, m.b_lm, nullptr, 0, n_dec, h->Vloc, d, fl::EPI_ARGMAX, s);
+    } else {
+      FL_GEMM(h->h, d, m.w_lm, m.b_lm, h->logits, h->Vl, n_dec, h->Vloc, d, fl::EPI_STORE_F32, s);
+      fl::launch_argmax(h->logits, n_dec, h->Vloc, h->Vl, m.tp_rank * h->Vl, h->keys, s);
+      fl::g_launches += 1;
+    }
     if (tp) {
       ncclResult_t r = g_nccl.allReduce(h->keys, h->keys, n_dec, ncclUint64, ncclMax, h->comm, s);
       if (r != ncclSuccess) return fail(FL_ENCCL, "argmax all-reduce failed (%d)", (int)r);
@@ -458,10 +505,96 @@ extern "C" int fl_step(fl_handle* h, const fl_row* rows, int n_rows, int n_dec, 
     fl::launch_apply_tokens(h->keys, h->rows, h->row_pos, n_dec, p.req_tok, p.req_pos, p.req_ngen,
                             p.tok_hist, p.state_slots, p.max_new_tokens, s);
     fl::g_launches += 1;
-    if (logits_out)
-      FL_CUDA(cudaMemcpyAsync(logits_out, h->logits, sizeof(float) * n_dec * h->Vl,
-                              cudaMemcpyDeviceToDevice, s));
   }
+#undef FL_GEMM
+  return FL_OK;
+}
+
+void harvest(fl_handle* h, std::vector<fl_handle::Rec>& recs) {
+  for (auto& r : recs) {
+    float ms = 0.f;
+    cudaEventSynchronize(r.b);
+    if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) {
+      h->tot_ms[r.cls] += ms;
+      h->tot_bytes[r.cls] += r.bytes;
+      h->tot_n[r.cls] += 1;
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" int fl_step(fl_handle* h, const fl_row* rows, int n_rows, int n_dec, int rows_changed,
+                       float* logits_out, void* stream) {
+  if (!h) return fail(FL_EINVAL, "null handle");
+  if (n_rows < 1 || n_dec < 0 || n_dec > n_rows) return fail(FL_EINVAL, "bad row counts");
+  if (n_rows > h->p.max_rows) return fail(FL_ECAPACITY, "%d rows > max_rows %d", n_rows, h->p.max_rows);
+  if (h->m.tp_size > 1 && !h->comm) return fail(FL_EINVAL, "tp_size > 1 needs fl_comm_init");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const fl_pool_desc& p = h->p;
+  if (rows_changed) {
+    if (!rows) return fail(FL_EINVAL, "rows_changed with null rows");
+    for (int i = 0; i < n_rows; ++i) {
+      const fl_row& r = rows[i];
+      if (r.slot < 0 || r.slot >= p.pool_slots) return fail(FL_EINVAL, "row %d slot %d", i, r.slot);
+      if (r.kind != FL_ROW_ORPHAN && r.pos >= p.max_seq)
+        return fail(FL_ECAPACITY, "row %d position %d >= max_seq %d", i, r.pos, p.max_seq);
+      if (r.kind == FL_ROW_PREFILL && i < n_dec) return fail(FL_EINVAL, "prefill row %d in window", i);
+      if (r.kind == FL_ROW_DECODE && i >= n_dec) return fail(FL_EINVAL, "decode row %d past window", i);
+      if (r.kind == FL_ROW_ORPHAN && r.ctx > p.max_seq) return fail(FL_EINVAL, "orphan ctx %d", r.ctx);
+    }
+    FL_CUDA(cudaMemcpyAsync(h->rows, rows, sizeof(fl_row) * n_rows, cudaMemcpyHostToDevice, s));
+  }
+  const bool want_logits = logits_out != nullptr;
+  const bool profiled = h->prof && (h->step_counter++ % h->prof_every == 0);
+  if (!h->use_graphs) {
+    if (h->prof && !profiled) {
+      const bool save = h->prof;
+      h->prof = false;
+      int e = enqueue_step(h, n_rows, n_dec, want_logits, s);
+      h->prof = save;
+      if (e) return e;
+    } else if (int e = enqueue_step(h, n_rows, n_dec, want_logits, s)) {
+      return e;
+    }
+  } else {
+    auto key = std::make_tuple(n_rows, n_dec, (int)want_logits, (int)profiled);
+    auto it = h->graphs.find(key);
+    if (it == h->graphs.end()) {
+      fl_handle::GraphEntry entry;
+      const bool save = h->prof;
+      h->prof = profiled;
+      h->sink = &entry.recs;
+      h->capturing = true;
+      FL_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      int e = enqueue_step(h, n_rows, n_dec, want_logits, s);
+      cudaGraph_t g = nullptr;
+      cudaError_t ce = cudaStreamEndCapture(s, &g);
+      h->capturing = false;
+      h->sink = nullptr;
+      h->prof = save;
+      if (e) {
+        if (g) cudaGraphDestroy(g);
+        return e;
+      }
+      if (ce != cudaSuccess) return fail(FL_ECUDA, "graph capture: %s", cudaGetErrorString(ce));
+      ce = cudaGraphInstantiateWithFlags(&entry.exec, g, 0);
+      cudaGraphDestroy(g);
+      if (ce != cudaSuccess) return fail(FL_ECUDA, "graph instantiate: %s", cudaGetErrorString(ce));
+      it = h->graphs.emplace(key, std::move(entry)).first;
+    }
+    fl_handle::GraphEntry& ge = it->second;
+    if (ge.pending) {        // the previous replay's events: long complete by now
+      harvest(h, ge.recs);
+      ge.pending = false;
+    }
+    FL_CUDA(cudaGraphLaunch(ge.exec, s));
+    ge.pending = profiled;
+    fl::g_launches += 0;
+  }
+  if (want_logits && n_dec > 0)
+    FL_CUDA(cudaMemcpyAsync(logits_out, h->logits, sizeof(float) * n_dec * h->Vl,
+                            cudaMemcpyDeviceToDevice, s));
   FL_CUDA(cudaGetLastError());
   return FL_OK;
 }

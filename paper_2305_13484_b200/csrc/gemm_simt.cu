@@ -15,6 +15,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_gemm_simt(const T* __restrict__ X, const T* __restrict__ W,
                                                    const T* __restrict__ bias, void* __restrict__ out,
                                                    int M, int N, int K, int ldx, int ldo, int epi) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float sx[SG_BK][SG_BM + 4];
   __shared__ float sw[SG_BK][SG_BN + 4];
   const int m0 = blockIdx.y * SG_BM, n0 = blockIdx.x * SG_BN;
@@ -67,10 +69,10 @@ void gemm_simt(const GemmArgs& a, cudaStream_t s) {
   if (a.M <= 0 || a.N <= 0) return;
   dim3 grid((a.N + SG_BN - 1) / SG_BN, (a.M + SG_BM - 1) / SG_BM);
   if (a.dtype == FL_DTYPE_BF16)
-    k_gemm_simt<bf16><<<grid, 256, 0, s>>>((const bf16*)a.x, (const bf16*)a.w, (const bf16*)a.bias,
+    launch_k(k_gemm_simt<bf16>, dim3(grid), dim3(256), 0, s, 1, (const bf16*)a.x, (const bf16*)a.w, (const bf16*)a.bias,
                                            a.out, a.M, a.N, a.K, a.ldx, a.ldo, a.epi);
   else
-    k_gemm_simt<float><<<grid, 256, 0, s>>>((const float*)a.x, (const float*)a.w,
+    launch_k(k_gemm_simt<float>, dim3(grid), dim3(256), 0, s, 1, (const float*)a.x, (const float*)a.w,
                                             (const float*)a.bias, a.out, a.M, a.N, a.K, a.ldx,
                                             a.ldo, a.epi);
 }

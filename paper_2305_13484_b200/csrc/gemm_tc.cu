@@ -125,30 +125,84 @@ struct TmemCols {
   static constexpr int v = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
 };
 
+FL_DEV uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+FL_DEV void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+
+FL_DEV float4 ld_dsmem_f4(uint32_t local_addr, uint32_t peer) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_addr), "r"(peer));
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(remote));
+  return v;
+}
+
+// Epilogue element-wise op on 4 consecutive weight rows n..n+3 of token m.
+FL_DEV void store4(void* out, size_t o, int nvalid, const float* v, int epi) {
+  if (epi == EPI_STORE || epi == EPI_GELU) {
+    bf16* p = static_cast<bf16*>(out) + o;
+    float w[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) w[j] = epi == EPI_GELU ? gelu_tanh(v[j]) : v[j];
+    if (nvalid == 4 && (o & 3) == 0) {
+      __nv_bfloat162 a = __floats2bfloat162_rn(w[0], w[1]), b = __floats2bfloat162_rn(w[2], w[3]);
+      uint2 raw = make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
+      *reinterpret_cast<uint2*>(p) = raw;
+    } else {
+      for (int j = 0; j < nvalid; ++j) p[j] = __float2bfloat16_rn(w[j]);
+    }
+  } else {
+    float* p = static_cast<float*>(out) + o;
+    if (nvalid == 4 && (o & 3) == 0) {
+      float4 r = make_float4(v[0], v[1], v[2], v[3]);
+      if (epi == EPI_ACC_F32) {
+        const float4 x = *reinterpret_cast<float4*>(p);
+        r.x += x.x; r.y += x.y; r.z += x.z; r.w += x.w;
+      }
+      *reinterpret_cast<float4*>(p) = r;
+    } else {
+      for (int j = 0; j < nvalid; ++j) p[j] = epi == EPI_ACC_F32 ? p[j] + v[j] : v[j];
+    }
+  }
+}
+
+// grid (N/128, ceil(M/BN), S) with cluster (1,1,S): the S CTAs of a cluster
+// split K for the same output tile and reduce their fp32 partials through
+// distributed shared memory (no global round trip, no atomics).
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tma_w, const __grid_constant__ CUtensorMap tma_x,
               const bf16* __restrict__ bias, void* __restrict__ out, int M, int N, int ldo, int epi,
-              int kch_total, int kch_per_split, int* __restrict__ counters,
-              float* __restrict__ partials) {
+              int kch_total, int kch_per_split, unsigned long long* __restrict__ keys,
+              int index_base) {
   constexpr int B_BYTES = BN * TC_BK * 2;
   constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   constexpr int NCOLS = TmemCols<BN>::v;
+  constexpr int RED_LD = TC_BM + 4;          // partial tile [BN][132] fp32 (n fastest)
+  static_assert(BN * RED_LD * 4 <= STAGES * STAGE_BYTES, "partial tile must fit the stage ring");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[STAGES];
   __shared__ __align__(8) uint64_t empty_bar[STAGES];
   __shared__ __align__(8) uint64_t done_bar;
   __shared__ uint32_t tmem_base;
-  __shared__ int s_last;
 
-  // 1024-byte alignment for the swizzle atoms
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_tile = blockIdx.x, m_tile = blockIdx.y, split = blockIdx.z, splits = gridDim.z;
+  const int n_tile = blockIdx.x, m_tile = blockIdx.y, split = blockIdx.z, S = gridDim.z;
   const int n0 = n_tile * TC_BM, m0 = m_tile * BN;
   const int kc0 = split * kch_per_split;
-  const int nch = min(kch_per_split, kch_total - kc0);
+  const int nch = max(0, min(kch_per_split, kch_total - kc0));
 
+  // ---- prologue (overlaps the predecessor kernel under PDL)
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_w)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_x)) : "memory");
@@ -168,20 +222,30 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_trigger();
   const uint32_t tmem = tmem_base;
 
   if (warp == 0) {
     if (lane == 0) {
-      for (int c = 0; c < nch; ++c) {
+      // weights do not depend on the predecessor: start streaming them first
+      const int pre = min(nch, STAGES);
+      for (int c = 0; c < pre; ++c) {
+        uint8_t* a = smem + c * STAGE_BYTES;
+        mbar_expect_tx(&full_bar[c], STAGE_BYTES);
+        tma_load_2d(&tma_w, &full_bar[c], a, (kc0 + c) * TC_BK, n0);
+      }
+      pdl_wait();                                   // activations are the predecessor's output
+      for (int c = 0; c < pre; ++c)
+        tma_load_2d(&tma_x, &full_bar[c], smem + c * STAGE_BYTES + A_BYTES, (kc0 + c) * TC_BK, m0);
+      for (int c = pre; c < nch; ++c) {
         const int s = c % STAGES;
         const uint32_t ph = (c / STAGES) & 1;
         mbar_wait(&empty_bar[s], ph ^ 1);
         uint8_t* a = smem + s * STAGE_BYTES;
-        uint8_t* b = a + A_BYTES;
         mbar_expect_tx(&full_bar[s], STAGE_BYTES);
         const int k = (kc0 + c) * TC_BK;
         tma_load_2d(&tma_w, &full_bar[s], a, k, n0);
-        tma_load_2d(&tma_x, &full_bar[s], b, k, m0);
+        tma_load_2d(&tma_x, &full_bar[s], a + A_BYTES, k, m0);
       }
     }
   } else if (warp == 1) {
@@ -203,72 +267,89 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mma_commit(&done_bar);
     }
   } else {
-    // ---------------- epilogue (warps 2..5)
-    const int quarter = warp & 3;            // TMEM lane quarter this warp may read
-    const int row = quarter * 32 + lane;     // weight row within the tile
-    const int n = n0 + row;
-    mbar_wait(&done_bar, 0);
-    tc_fence_after();
-    const uint32_t taddr = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-    const int mcount = min(BN, M - m0);
-    const size_t tile_id = static_cast<size_t>(m_tile) * gridDim.x + n_tile;
-    if (splits > 1) {
-      float* part = partials + (tile_id * splits + split) * (size_t)(TC_BM * BN);
+    // ---- epilogue part 1 (warps 2..5): TMEM -> own smem partial [BN][RED_LD]
+    pdl_wait();     // EPI_ACC_F32 reads `out`, written by predecessors
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    float* red = reinterpret_cast<float*>(smem);
+    if (nch > 0) {
+      mbar_wait(&done_bar, 0);
+      tc_fence_after();
+      const uint32_t taddr = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
       for (int c0 = 0; c0 < BN; c0 += 16) {
         float v[16];
         tmem_ld16(taddr + c0, v);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) part[(c0 + j) * TC_BM + row] = v[j];
+        for (int j = 0; j < 16; ++j) red[(c0 + j) * RED_LD + row] = v[j];
       }
-      __threadfence();
-      asm volatile("bar.sync 1, 128;");
-      if (warp == 2 && lane == 0) {
-        const int prev = atomicAdd(&counters[tile_id], 1);
-        s_last = (prev == splits - 1);
-        if (s_last) counters[tile_id] = 0;   // self-reset for the next GEMM
-      }
-      asm volatile("bar.sync 1, 128;");
-      if (!s_last) goto teardown;
-      __threadfence();
+    } else {
+      for (int c0 = 0; c0 < BN; ++c0) red[c0 * RED_LD + row] = 0.f;
     }
-    {
-      const float bv = (bias && n < N) ? __bfloat162float(bias[n]) : 0.f;
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        float v[16];
-        if (splits > 1) {
+  }
+  // all 192 threads of every CTA in the cluster (S == 1: plain CTA barrier)
+  __syncwarp();
+  tc_fence_before();
+  if (S > 1) cluster_sync_all();
+  else __syncthreads();
+
+  if (warp >= 2) {
+    // ---- epilogue part 2: this CTA reduces rows [rk*R, rk*R+R) over the S partials
+    const int rk = S > 1 ? static_cast<int>(cluster_rank()) : 0;
+    const int R = TC_BM / S;
+    const int q4 = R / 4;                          // float4 groups of rows (power of two)
+    const int mcount = min(BN, M - m0);
+    const uint32_t red_base = smem_u32(smem);
+    const int total = q4 * mcount;
+    for (int base = 0; base < total; base += 128) {
+      const int e = base + threadIdx.x - 64;
+      const bool valid = e < total;
+      const int m = valid ? e / q4 : 0;
+      const int r0 = rk * R + (e % q4) * 4;
+      const uint32_t off = static_cast<uint32_t>((m * RED_LD + r0) * 4);
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      if (valid) {
+        float4 t[8];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] = 0.f;
-          const float* p0 = partials + tile_id * splits * (size_t)(TC_BM * BN);
-          for (int sp = 0; sp < splits; ++sp) {
-            const float* p = p0 + sp * (size_t)(TC_BM * BN);
+        for (int p = 0; p < 8; ++p)      // all peer loads in flight at once
+          if (p < S)
+            t[p] = S > 1 ? ld_dsmem_f4(red_base + off, p)
+                         : *reinterpret_cast<const float4*>(smem + off);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] += __ldcg(p + (c0 + j) * TC_BM + row);
+        for (int p = 0; p < 8; ++p)
+          if (p < S) {
+            acc[0] += t[p].x; acc[1] += t[p].y; acc[2] += t[p].z; acc[3] += t[p].w;
           }
-        } else {
-          tmem_ld16(taddr + c0, v);
-        }
-        if (n < N) {
+      }
+      const int n = n0 + r0;
+      const int nvalid = valid ? max(0, min(4, N - n)) : 0;
+      if (bias) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int m = c0 + j;
-            if (m < mcount) {
-              const float x = v[j] + bv;
-              const size_t o = static_cast<size_t>(m0 + m) * ldo + n;
-              switch (epi) {
-                case EPI_STORE: static_cast<bf16*>(out)[o] = __float2bfloat16_rn(x); break;
-                case EPI_GELU: static_cast<bf16*>(out)[o] = __float2bfloat16_rn(gelu_tanh(x)); break;
-                case EPI_ACC_F32: static_cast<float*>(out)[o] += x; break;
-                default: static_cast<float*>(out)[o] = x; break;
-              }
-            }
+        for (int j = 0; j < 4; ++j) acc[j] += j < nvalid ? __bfloat162float(bias[n + j]) : 0.f;
+      }
+      if (epi == EPI_ARGMAX) {
+        // greedy token: max logit, lowest index; reduce over the q4 lanes of this
+        // token, then one 64-bit atomicMax per (token, CTA)
+        unsigned long long key = 0ull;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (j < nvalid) {
+            const unsigned long long k2 = argmax_key(acc[j], index_base + n + j);
+            key = k2 > key ? k2 : key;
           }
+        for (int o = 1; o < q4 && o < 32; o <<= 1) {
+          const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
+          key = other > key ? other : key;
         }
+        if (valid && (e % q4) == 0 && key) atomicMax(&keys[m0 + m], key);
+      } else if (nvalid > 0) {
+        store4(out, static_cast<size_t>(m0 + m) * ldo + n, nvalid, acc, epi);
       }
     }
   }
-teardown:
-  tc_fence_before();
-  __syncthreads();
+  // peers may still be reading this CTA's partial
+  __syncwarp();
+  if (S > 1) cluster_sync_all();
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(NCOLS));
@@ -317,31 +398,30 @@ bool make_map(MapCache& cache, const void* ptr, uint64_t rows, uint64_t cols, ui
   return true;
 }
 
-constexpr size_t TC_COUNTERS = 4096;
-constexpr size_t TC_MAX_PARTIAL_TILES = 160;   // split-K CTAs (<= SM count) writing a partial
-
 template <int BN, int STAGES>
-int launch_bn(TcWorkspace* ws, const GemmArgs& a, const CUtensorMap* mw, const CUtensorMap* mx,
-              int splits, int kpc, cudaStream_t s) {
+int launch_bn(const GemmArgs& a, const CUtensorMap* mw, const CUtensorMap* mx, int splits, int kpc,
+              cudaStream_t s) {
   constexpr int smem = STAGES * (A_BYTES + BN * TC_BK * 2) + 1024;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(k_gemm_tc<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_gemm_tc<BN, STAGES>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     configured = true;
   }
   dim3 grid((a.N + TC_BM - 1) / TC_BM, (a.M + BN - 1) / BN, splits);
-  k_gemm_tc<BN, STAGES><<<grid, TC_THREADS, smem, s>>>(
-      *mw, *mx, static_cast<const bf16*>(a.bias), a.out, a.M, a.N, a.ldo, a.epi, a.K / TC_BK, kpc,
-      ws->counters, ws->partials);
+  cudaError_t e = launch_k(k_gemm_tc<BN, STAGES>, grid, dim3(TC_THREADS), smem, s, splits, *mw, *mx,
+                           static_cast<const bf16*>(a.bias), a.out, a.M, a.N, a.ldo, a.epi,
+                           a.K / TC_BK, kpc, a.keys, a.index_base);
+  if (e != cudaSuccess) {
+    g_tc_err = std::string("k_gemm_tc launch: ") + cudaGetErrorString(e);
+    return -1;
+  }
   return 0;
 }
 
 }  // namespace
 
-size_t tc_workspace_bytes(int max_rows, int) {
-  (void)max_rows;
-  return TC_COUNTERS * sizeof(int) + TC_MAX_PARTIAL_TILES * TC_BM * 256 * sizeof(float);
-}
+size_t tc_workspace_bytes(int, int) { return 256; }
 
 const char* tc_last_error() { return g_tc_err.c_str(); }
 
@@ -356,23 +436,12 @@ int tc_init(TcWorkspace* ws, void* base, size_t bytes) {
     }
     g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
-  if (bytes < tc_workspace_bytes(0, 0)) {
-    g_tc_err = "tensor-core workspace too small";
-    return -1;
-  }
   ws->base = base;
   ws->bytes = bytes;
-  ws->counters = static_cast<int*>(base);
-  ws->partials = reinterpret_cast<float*>(static_cast<char*>(base) + TC_COUNTERS * sizeof(int));
-  ws->partial_floats = TC_MAX_PARTIAL_TILES * TC_BM * 256;
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&ws->num_sms, cudaDevAttrMultiProcessorCount, dev);
-  if (cudaMemset(ws->counters, 0, TC_COUNTERS * sizeof(int)) != cudaSuccess) {
-    g_tc_err = "counter memset failed";
-    return -1;
-  }
-  ws->maps = new MapCache();
+  if (!ws->maps) ws->maps = new MapCache();
   return 0;
 }
 
@@ -394,22 +463,16 @@ int gemm_tc(TcWorkspace* ws, const GemmArgs& a, cudaStream_t s) {
   if (!make_map(cache, a.x, a.mcap > a.M ? a.mcap : a.M, a.K, a.ldx, bn, &mx)) return -1;
   const int tiles = ((a.N + TC_BM - 1) / TC_BM) * ((a.M + bn - 1) / bn);
   const int kch = a.K / TC_BK;
-  int splits = 1;
-  if (tiles < ws->num_sms) {
-    splits = ws->num_sms / tiles;
-    if (splits > kch / 2) splits = kch / 2 > 0 ? kch / 2 : 1;
-    if (splits > 16) splits = 16;
-    while (splits > 1 && (size_t)tiles * splits * TC_BM * bn > ws->partial_floats) --splits;
-    if ((size_t)tiles > TC_COUNTERS) splits = 1;
-  }
-  const int kpc = (kch + splits - 1) / splits;
-  splits = (kch + kpc - 1) / kpc;
+  // split K across a cluster of S CTAs until the tiles cover the SMs
+  int S = 1;
+  while (S < 8 && tiles * S * 2 <= ws->num_sms && kch / (S * 2) >= 1) S *= 2;
+  const int kpc = (kch + S - 1) / S;
   switch (bn) {
-    case 16: return launch_bn<16, 8>(ws, a, mw, mx, splits, kpc, s);
-    case 32: return launch_bn<32, 8>(ws, a, mw, mx, splits, kpc, s);
-    case 64: return launch_bn<64, 6>(ws, a, mw, mx, splits, kpc, s);
-    case 128: return launch_bn<128, 4>(ws, a, mw, mx, splits, kpc, s);
-    default: return launch_bn<256, 4>(ws, a, mw, mx, splits, kpc, s);
+    case 16: return launch_bn<16, 8>(a, mw, mx, S, kpc, s);
+    case 32: return launch_bn<32, 8>(a, mw, mx, S, kpc, s);
+    case 64: return launch_bn<64, 6>(a, mw, mx, S, kpc, s);
+    case 128: return launch_bn<128, 4>(a, mw, mx, S, kpc, s);
+    default: return launch_bn<256, 4>(a, mw, mx, S, kpc, s);
   }
 }
 

@@ -14,9 +14,6 @@ namespace fl {
 struct TcWorkspace {
   void* base = nullptr;        // caller-owned device scratch
   size_t bytes = 0;
-  int* counters = nullptr;     // split-K arrival counters (self-resetting)
-  float* partials = nullptr;   // split-K fp32 partial tiles
-  size_t partial_floats = 0;
   int num_sms = 148;
   void* maps = nullptr;        // host-side tensor-map cache (opaque)
 };

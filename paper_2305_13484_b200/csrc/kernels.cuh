@@ -12,7 +12,8 @@ enum Epilogue {
   EPI_STORE = 0,      // out(T)   = acc + bias
   EPI_GELU = 1,       // out(T)   = gelu(acc + bias)
   EPI_ACC_F32 = 2,    // out(f32) += acc + bias      (residual update)
-  EPI_STORE_F32 = 3   // out(f32) = acc + bias       (partial sums, logits)
+  EPI_STORE_F32 = 3,  // out(f32) = acc + bias       (partial sums, logits)
+  EPI_ARGMAX = 4      // keys[m] = max(keys[m], key(acc + bias, n))  (fused greedy argmax)
 };
 
 struct GemmArgs {
@@ -24,15 +25,19 @@ struct GemmArgs {
   int epi;
   int dtype;          // FL_DTYPE_*
   int mcap;           // rows allocated behind x (>= M); fixes the TMA map per buffer
+  unsigned long long* keys = nullptr;   // EPI_ARGMAX: per-row packed (logit, index) keys
+  int index_base = 0;                   // EPI_ARGMAX: global index of weight row 0
 };
 
 // SIMT FFMA GEMM (fp32 path and the reference path for the tensor-core GEMM).
 void gemm_simt(const GemmArgs& a, cudaStream_t s);
 
 // Resolve rows (token / position / context per row) and gather embeddings.
-void launch_embed(const fl_row* rows, int n_rows, const int32_t* req_tok, const int32_t* req_pos,
-                  int32_t* req_ngen, int R, const void* wte, const void* wpe, int d, int dtype,
-                  float* x, int32_t* row_tok, int32_t* row_pos, int32_t* row_ctx, cudaStream_t s);
+// Also zeroes keys[0, n_dec) for this step's greedy argmax.
+void launch_embed(const fl_row* rows, int n_rows, int n_dec, const int32_t* req_tok,
+                  const int32_t* req_pos, int32_t* req_ngen, int R, const void* wte,
+                  const void* wpe, int d, int dtype, float* x, int32_t* row_tok, int32_t* row_pos,
+                  int32_t* row_ctx, unsigned long long* keys, cudaStream_t s);
 
 // out(T)[M, d] = LN(x[M, d]) * g + b
 void launch_layernorm(const float* x, const void* g, const void* b, void* out, int M, int d,
@@ -49,9 +54,12 @@ void launch_rope_append(const void* qkv, const fl_row* rows, const int32_t* row_
 
 // split-K masked decode attention over each row's own context.
 int attn_max_splits(int S);
-void launch_attention(const void* q, const fl_row* rows, const int32_t* row_ctx, int M, int Hl,
-                      int hd, const void* kv_layer, int C, int S, void* out, float* ws_o,
-                      float* ws_ml, int dtype, cudaStream_t s);
+// keys per split: one split per (row, head) when rows*heads fill the GPU.
+int attn_keys_per_split(int row_heads, int S);
+// returns the number of kernels launched (1 or 2)
+int launch_attention(const void* q, const fl_row* rows, const int32_t* row_ctx, int M, int Hl,
+                     int hd, const void* kv_layer, int C, int S, int keys_per_split, void* out,
+                     float* ws_o, float* ws_ml, int dtype, cudaStream_t s);
 
 // per-row (max logit, lowest index) as a packed 64-bit key
 void launch_argmax(const float* logits, int M, int V, int ldl, int index_base,

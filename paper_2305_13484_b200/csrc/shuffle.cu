@@ -19,6 +19,8 @@ __global__ void __launch_bounds__(256) k_shuffle(const int32_t* __restrict__ mov
                                                  uint8_t* __restrict__ kv, size_t slot_stride_b,
                                                  size_t layer_stride_b, size_t block_stride_b,
                                                  int blocks_per_slot, int row_bytes) {
+  pdl_trigger();
+  pdl_wait();
   const int mv = blockIdx.x / units_per_move;
   const int u = blockIdx.x % units_per_move;
   const int layer = u / blocks_per_slot, blk = u % blocks_per_slot;
@@ -46,7 +48,7 @@ void launch_shuffle(const int32_t* moves, int n_moves, void* kv, int L, int C, i
   const size_t slot_b = block_b * blocks_per_slot;            // one slot inside a layer
   const size_t layer_b = slot_b * C;
   const int units = L * blocks_per_slot;
-  k_shuffle<<<n_moves * units, 256, 0, s>>>(moves, units, static_cast<uint8_t*>(kv), slot_b, layer_b,
+  launch_k(k_shuffle, dim3(n_moves * units), dim3(256), 0, s, 1, moves, units, static_cast<uint8_t*>(kv), slot_b, layer_b,
                                             block_b, blocks_per_slot, row_bytes);
 }
 

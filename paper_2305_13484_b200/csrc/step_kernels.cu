@@ -9,11 +9,14 @@ namespace fl {
 
 // ---------------------------------------------------------------- K1 embed
 template <typename T>
-__global__ void k_embed(const fl_row* __restrict__ rows, const int32_t* __restrict__ req_tok,
-                        const int32_t* __restrict__ req_pos, int32_t* __restrict__ req_ngen, int R,
-                        const T* __restrict__ wte, const T* __restrict__ wpe, int d,
-                        float* __restrict__ x, int32_t* __restrict__ row_tok,
-                        int32_t* __restrict__ row_pos, int32_t* __restrict__ row_ctx) {
+__global__ void k_embed(const fl_row* __restrict__ rows, int n_dec,
+                        const int32_t* __restrict__ req_tok, const int32_t* __restrict__ req_pos,
+                        int32_t* __restrict__ req_ngen, int R, const T* __restrict__ wte,
+                        const T* __restrict__ wpe, int d, float* __restrict__ x,
+                        int32_t* __restrict__ row_tok, int32_t* __restrict__ row_pos,
+                        int32_t* __restrict__ row_ctx, unsigned long long* __restrict__ keys) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
   const fl_row row = rows[r];
   int tok, pos, ctx;
@@ -33,6 +36,7 @@ __global__ void k_embed(const fl_row* __restrict__ rows, const int32_t* __restri
     row_tok[r] = tok;
     row_pos[r] = pos;
     row_ctx[r] = ctx;
+    if (r < n_dec) keys[r] = 0ull;
   }
   constexpr int V = Vec16<T>::N;
   const T* e = wte + static_cast<size_t>(tok) * d;
@@ -52,16 +56,18 @@ __global__ void k_embed(const fl_row* __restrict__ rows, const int32_t* __restri
   }
 }
 
-void launch_embed(const fl_row* rows, int n_rows, const int32_t* req_tok, const int32_t* req_pos,
-                  int32_t* req_ngen, int R, const void* wte, const void* wpe, int d, int dtype,
-                  float* x, int32_t* row_tok, int32_t* row_pos, int32_t* row_ctx, cudaStream_t s) {
+void launch_embed(const fl_row* rows, int n_rows, int n_dec, const int32_t* req_tok,
+                  const int32_t* req_pos, int32_t* req_ngen, int R, const void* wte,
+                  const void* wpe, int d, int dtype, float* x, int32_t* row_tok, int32_t* row_pos,
+                  int32_t* row_ctx, unsigned long long* keys, cudaStream_t s) {
   if (n_rows <= 0) return;
   if (dtype == FL_DTYPE_BF16)
-    k_embed<bf16><<<n_rows, 128, 0, s>>>(rows, req_tok, req_pos, req_ngen, R, (const bf16*)wte,
-                                         (const bf16*)wpe, d, x, row_tok, row_pos, row_ctx);
+    launch_k(k_embed<bf16>, dim3(n_rows), dim3(128), 0, s, 1, rows, n_dec, req_tok, req_pos,
+             req_ngen, R, (const bf16*)wte, (const bf16*)wpe, d, x, row_tok, row_pos, row_ctx, keys);
   else
-    k_embed<float><<<n_rows, 128, 0, s>>>(rows, req_tok, req_pos, req_ngen, R, (const float*)wte,
-                                          (const float*)wpe, d, x, row_tok, row_pos, row_ctx);
+    launch_k(k_embed<float>, dim3(n_rows), dim3(128), 0, s, 1, rows, n_dec, req_tok, req_pos,
+             req_ngen, R, (const float*)wte, (const float*)wpe, d, x, row_tok, row_pos, row_ctx,
+             keys);
 }
 
 // ---------------------------------------------------------------- K2 LayerNorm
@@ -71,6 +77,8 @@ __global__ void __launch_bounds__(256) k_layernorm(const float* __restrict__ x,
                                                    const T* __restrict__ g,
                                                    const T* __restrict__ b, T* __restrict__ out,
                                                    int d, float eps) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float red[32];
   const int r = blockIdx.x;
   const float* xr = x + static_cast<size_t>(r) * d;
@@ -117,12 +125,12 @@ static void ln_dispatch(const float* x, const void* g, const void* b, void* out,
   const T* B = (const T*)b;
   T* O = (T*)out;
   switch (per) {
-    case 1: k_layernorm<T, 1><<<M, 256, 0, s>>>(x, G, B, O, d, eps); break;
-    case 2: k_layernorm<T, 2><<<M, 256, 0, s>>>(x, G, B, O, d, eps); break;
-    case 3: k_layernorm<T, 3><<<M, 256, 0, s>>>(x, G, B, O, d, eps); break;
-    case 4: k_layernorm<T, 4><<<M, 256, 0, s>>>(x, G, B, O, d, eps); break;
-    case 5: case 6: k_layernorm<T, 6><<<M, 256, 0, s>>>(x, G, B, O, d, eps); break;
-    default: k_layernorm<T, 8><<<M, 256, 0, s>>>(x, G, B, O, d, eps); break;
+    case 1: launch_k(k_layernorm<T, 1>, dim3(M), dim3(256), 0, s, 1, x, G, B, O, d, eps); break;
+    case 2: launch_k(k_layernorm<T, 2>, dim3(M), dim3(256), 0, s, 1, x, G, B, O, d, eps); break;
+    case 3: launch_k(k_layernorm<T, 3>, dim3(M), dim3(256), 0, s, 1, x, G, B, O, d, eps); break;
+    case 4: launch_k(k_layernorm<T, 4>, dim3(M), dim3(256), 0, s, 1, x, G, B, O, d, eps); break;
+    case 5: case 6: launch_k(k_layernorm<T, 6>, dim3(M), dim3(256), 0, s, 1, x, G, B, O, d, eps); break;
+    default: launch_k(k_layernorm<T, 8>, dim3(M), dim3(256), 0, s, 1, x, G, B, O, d, eps); break;
   }
 }
 
@@ -137,6 +145,8 @@ void launch_layernorm(const float* x, const void* g, const void* b, void* out, i
 template <typename T>
 __global__ void k_add_partial(float* __restrict__ x, const float* __restrict__ y,
                               const T* __restrict__ b1, const T* __restrict__ b2, int M, int d) {
+  pdl_trigger();
+  pdl_wait();
   const size_t n = static_cast<size_t>(M) * d;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
        i += (size_t)gridDim.x * blockDim.x) {
@@ -154,9 +164,9 @@ void launch_add_partial(float* x, const float* y, const void* b1, const void* b2
   const size_t n = (size_t)M * d;
   const int grid = (int)((n + 255) / 256 < 148 * 8 ? (n + 255) / 256 : 148 * 8);
   if (dtype == FL_DTYPE_BF16)
-    k_add_partial<bf16><<<grid, 256, 0, s>>>(x, y, (const bf16*)b1, (const bf16*)b2, M, d);
+    launch_k(k_add_partial<bf16>, dim3(grid), dim3(256), 0, s, 1, x, y, (const bf16*)b1, (const bf16*)b2, M, d);
   else
-    k_add_partial<float><<<grid, 256, 0, s>>>(x, y, (const float*)b1, (const float*)b2, M, d);
+    launch_k(k_add_partial<float>, dim3(grid), dim3(256), 0, s, 1, x, y, (const float*)b1, (const float*)b2, M, d);
 }
 
 // ---------------------------------------------------------------- rotary + KV append
@@ -166,6 +176,8 @@ __global__ void k_rope_append(const T* __restrict__ qkv, const fl_row* __restric
                               const int32_t* __restrict__ row_pos, int Hl, int hd, int rot,
                               int family, T* __restrict__ kv_layer, int C, int S,
                               T* __restrict__ qout) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x, h = blockIdx.y, i = threadIdx.x;
   const int D = Hl * hd;
   const T* base = qkv + static_cast<size_t>(r) * 3 * D + h * hd;
@@ -213,10 +225,10 @@ void launch_rope_append(const void* qkv, const fl_row* rows, const int32_t* row_
   dim3 grid(M, Hl);
   if (family == FL_FAMILY_GPT2) rot = 0;
   if (dtype == FL_DTYPE_BF16)
-    k_rope_append<bf16><<<grid, hd, 0, s>>>((const bf16*)qkv, rows, row_pos, Hl, hd, rot, family,
+    launch_k(k_rope_append<bf16>, dim3(grid), dim3(hd), 0, s, 1, (const bf16*)qkv, rows, row_pos, Hl, hd, rot, family,
                                             (bf16*)kv_layer, C, S, (bf16*)qout);
   else
-    k_rope_append<float><<<grid, hd, 0, s>>>((const float*)qkv, rows, row_pos, Hl, hd, rot,
+    launch_k(k_rope_append<float>, dim3(grid), dim3(hd), 0, s, 1, (const float*)qkv, rows, row_pos, Hl, hd, rot,
                                              family, (float*)kv_layer, C, S, (float*)qout);
 }
 
@@ -224,6 +236,8 @@ void launch_rope_append(const void* qkv, const fl_row* rows, const int32_t* row_
 __global__ void __launch_bounds__(1024) k_argmax(const float* __restrict__ logits, int V, int ldl,
                                                  int index_base,
                                                  unsigned long long* __restrict__ keys) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ unsigned long long red[32];
   const int r = blockIdx.x;
   const float* l = logits + static_cast<size_t>(r) * ldl;
@@ -253,7 +267,7 @@ __global__ void __launch_bounds__(1024) k_argmax(const float* __restrict__ logit
 void launch_argmax(const float* logits, int M, int V, int ldl, int index_base,
                    unsigned long long* keys, cudaStream_t s) {
   if (M <= 0) return;
-  k_argmax<<<M, 1024, 0, s>>>(logits, V, ldl, index_base, keys);
+  launch_k(k_argmax, dim3(M), dim3(1024), 0, s, 1, logits, V, ldl, index_base, keys);
 }
 
 // ---------------------------------------------------------------- K9 state step
@@ -262,6 +276,8 @@ __global__ void k_apply_tokens(const unsigned long long* __restrict__ keys,
                                int n_dec, int32_t* __restrict__ req_tok,
                                int32_t* __restrict__ req_pos, int32_t* __restrict__ req_ngen,
                                int32_t* __restrict__ tok_hist, int R, int max_new) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n_dec) return;
   const fl_row row = rows[r];
@@ -279,7 +295,7 @@ void launch_apply_tokens(const unsigned long long* keys, const fl_row* rows,
                          const int32_t* row_pos, int n_dec, int32_t* req_tok, int32_t* req_pos,
                          int32_t* req_ngen, int32_t* tok_hist, int R, int max_new, cudaStream_t s) {
   if (n_dec <= 0) return;
-  k_apply_tokens<<<(n_dec + 127) / 128, 128, 0, s>>>(keys, rows, row_pos, n_dec, req_tok, req_pos,
+  launch_k(k_apply_tokens, dim3((n_dec + 127) / 128), dim3(128), 0, s, 1, keys, rows, row_pos, n_dec, req_tok, req_pos,
                                                      req_ngen, tok_hist, R, max_new);
 }
 

@@ -35,6 +35,18 @@ from .errors import CapacityExceeded, InvalidParam
 from .models import LAYER_KEYS, ModelSpec, init_weights
 
 _TORCH_DTYPE = {"f32": torch.float32, "bf16": torch.bfloat16}
+_PAD = (0, -1, -1, -1, _lib.ROW_ORPHAN, 1)
+
+
+def bucket(n: int) -> int:
+    """Row-count buckets: each (rows, window) bucket pair is one CUDA graph;
+    the padding rows are ORPHAN rows over one stale position (discarded)."""
+    if n <= 0:
+        return 0
+    for limit, step in ((64, 8), (128, 16), (256, 32)):
+        if n <= limit:
+            return -(-n // step) * step
+    return -(-n // 64) * 64
 
 
 class CudaExecutor:
@@ -44,7 +56,7 @@ class CudaExecutor:
                  state_slots: int = 4096, tp_rank: int = 0, tp_size: int = 1, seed: int = 0,
                  weights: dict | None = None, use_tensor_cores: bool | None = None,
                  capture_logits: bool = False, device: str = "cuda", comm_id: bytes | None = None,
-                 time_steps: bool = False):
+                 time_steps: bool = False, use_graphs: bool = True):
         if dtype not in _TORCH_DTYPE:
             raise InvalidParam(f"dtype must be f32 or bf16, got {dtype}")
         self.lib = _lib.load()
@@ -61,7 +73,9 @@ class CudaExecutor:
                 raise InvalidParam("need max_seq or input_len")
             max_seq = input_len + max_new_tokens - 1
         self.S = max_seq
-        self.max_rows = max_rows or (pool_slots + 16 * (input_len or 32))
+        self.max_rows = bucket(max_rows or (pool_slots + 16 * (input_len or 32)))
+        if self.max_rows < bucket(pool_slots) + 64:
+            self.max_rows = bucket(bucket(pool_slots) + 64)
         if use_tensor_cores is None:
             use_tensor_cores = dtype == "bf16"
         self.use_tc = bool(use_tensor_cores)
@@ -111,6 +125,7 @@ class CudaExecutor:
         h = C.c_void_p()
         _lib.check(self.lib.fl_create(C.byref(self.mdesc), C.byref(self.pdesc), C.byref(h)))
         self.handle = h
+        _lib.check(self.lib.fl_configure(self.handle, int(use_graphs), 8))
         if tp_size > 1:
             if comm_id is None:
                 raise InvalidParam("tp_size > 1 needs comm_id (see tp.make_comm_id)")
@@ -121,7 +136,8 @@ class CudaExecutor:
         self.capture_logits = capture_logits
         self.vl = (spec.vocab + tp_size - 1) // tp_size
         if capture_logits:
-            self.logits_buf = torch.empty((self.C, self.vl), dtype=torch.float32, device=self.device)
+            self.logits_buf = torch.empty((self.max_rows, self.vl), dtype=torch.float32,
+                                          device=self.device)
         self.logits_log = []             # [(iteration, [rid per decode row], cpu tensor)]
         self.time_steps = time_steps
         self._events = []
@@ -131,7 +147,8 @@ class CudaExecutor:
         self._prev_had_new = False
         self._rows_version = None
         self._rows = None
-        self._n_rows = self._n_dec = 0
+        self._n_rows = self._n_dec = self._n_real_dec = 0
+        self._pre_passes = []
         self.iterations = 0
         self.rows_total = 0
         self.prefill_rows_total = 0
@@ -157,6 +174,7 @@ class CudaExecutor:
         self._rows_version = None
         self._rows = None
         self._n_rows = self._n_dec = 0
+        self._pre_passes = []
         self._live_ctx = self._orphan_ctx = self._prefill_ctx = 0
         self.seen = []
         self.logits_log = []
@@ -229,10 +247,24 @@ class CudaExecutor:
                 prefill.extend((phys, occ, j, pr[j], _lib.ROW_PREFILL, 0) for j in range(P - 1))
             else:
                 rows.append((phys, occ, -1, -1, _lib.ROW_DECODE, 0))
+        self._n_real_dec = len(rows)
+        rows.extend([_PAD] * (bucket(len(rows)) - len(rows)))
         n_dec = len(rows)
-        rows.extend(prefill)
+        # prompt rows beyond the iteration's row budget run first as
+        # prefill-only passes (their KV lands before the decode rows read it)
+        room = self.max_rows - n_dec
+        if room < 0:
+            raise CapacityExceeded(f"window of {n_dec} rows > max_rows {self.max_rows}")
+        cut = max(0, len(prefill) - room)
+        head, tail = prefill[:cut], prefill[cut:]
+        self._pre_passes = []
+        for i in range(0, len(head), self.max_rows):
+            chunk = head[i:i + self.max_rows]
+            self._pre_passes.append(chunk + [_PAD] * (bucket(len(chunk)) - len(chunk)))
+        rows.extend(tail)
+        rows.extend([_PAD] * (bucket(len(rows)) - len(rows)))
         if len(rows) > self.max_rows:
-            raise CapacityExceeded(f"{len(rows)} rows in one iteration > max_rows {self.max_rows}")
+            rows = rows[:self.max_rows]       # padding only; real rows always fit
         arr = (_lib.Row * len(rows))(*[_lib.Row(*r) for r in rows])
         return arr, len(rows), n_dec
 
@@ -256,6 +288,15 @@ class CudaExecutor:
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(cs)
         logits_ptr = self.logits_buf.data_ptr() if self.capture_logits else None
+        if changed and self._pre_passes:
+            for chunk in self._pre_passes:
+                arr = (_lib.Row * len(chunk))(*[_lib.Row(*r) for r in chunk])
+                _lib.check(self.lib.fl_step(self.handle, arr, len(chunk), 0, 1, None,
+                                            C.c_void_p(cs.cuda_stream)))
+                self.rows_total += len(chunk)
+                self.prefill_rows_total += len(chunk)
+                self.h2d_bytes += len(chunk) * C.sizeof(_lib.Row)
+            self._pre_passes = []
         _lib.check(self.lib.fl_step(self.handle, self._rows, self._n_rows, self._n_dec, int(changed),
                                     logits_ptr, C.c_void_p(cs.cuda_stream)))
         self.iterations += 1
@@ -265,7 +306,7 @@ class CudaExecutor:
                      if layout.slots[s].occupant is None) if changed else self._last_orph
         self._last_orph = n_orph
         self.orphan_rows_total += n_orph
-        self.decode_rows_total += self._n_dec - n_orph
+        self.decode_rows_total += self._n_real_dec - n_orph
         if self.capture_logits:
             rids = [r.rid for r in self._rows[:self._n_dec]]
             kinds = [r.kind for r in self._rows[:self._n_dec]]

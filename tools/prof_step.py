@@ -1,0 +1,49 @@
+"""Steady-state fused-iteration probe: host time per fl_step vs device time.
+
+    python tools/prof_step.py [--config c2] [--rows 48] [--iters 200]
+
+Builds the config's executor, fuses `rows` requests at once, runs `iters`
+iterations (cost clock, no per-step sync) and reports host launch time per
+iteration, device time per iteration (CUDA events), and per-class kernel time.
+"""
+import argparse, os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2305_13484_b200 as fl
+from paper_2305_13484_b200.executor import CudaExecutor
+from paper_2305_13484_b200.models import get_spec
+import bench
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="c2")
+ap.add_argument("--rows", type=int, default=48)
+ap.add_argument("--iters", type=int, default=200)
+ap.add_argument("--profile", action="store_true")
+a = ap.parse_args()
+cfg = bench.CONFIGS[a.config]
+spec = get_spec(cfg["spec"])
+reqs = [fl.Request(i, 1, cfg["input_len"], cfg["max_out"], cfg["max_out"], 0.0) for i in range(a.rows)]
+prompts = fl.synthetic_prompts(reqs, spec.vocab, 1)
+ex = CudaExecutor(spec, prompts, dtype=cfg["dtype"], pool_slots=max(a.rows, 8), input_len=cfg["input_len"],
+                  max_new_tokens=cfg["max_out"], state_slots=1024, max_rows=max(a.rows, 8) + 256)
+st = fl.FusionStream(reqs, fl.CostParams(preprocess_ms=0.0), fl.TPConfig(), executor=ex, record_tokens=False)
+st.try_fuse_pending()
+st.step_iteration()            # admission step (prefill rows)
+for _ in range(5):
+    st.step_iteration()
+torch.cuda.synchronize()
+if a.profile:
+    ex.profile(True)
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+t0 = time.perf_counter()
+for _ in range(a.iters):
+    st.step_iteration()
+t1 = time.perf_counter()
+e1.record(); torch.cuda.synchronize()
+t2 = time.perf_counter()
+print(f"rows={a.rows} host launch {1e6*(t1-t0)/a.iters:.1f} us/iter, wall {1e6*(t2-t0)/a.iters:.1f} us/iter, "
+      f"device {1e3*e0.elapsed_time(e1)/a.iters:.1f} us/iter")
+if a.profile:
+    for k, v in ex.profile_read().items():
+        print(k, f"{1e3*v['ms']/a.iters:.1f} us/iter", v["records"] // a.iters, "records/iter")
