@@ -164,8 +164,12 @@ enum fl_prof_class {
 };
 /* Execution options: use_graphs (default 1) replays each (rows, window) shape
  * of fl_step as one CUDA graph; profile_every (default 8) samples one step in N
- * with event-bracketed launch groups while profiling is enabled. */
-int fl_configure(fl_handle* h, int use_graphs, int profile_every);
+ * with event-bracketed launch groups while profiling is enabled; time_steps
+ * brackets every fl_step / fl_shuffle with a pair of events (after any graph
+ * capture work), read back by fl_last_duration_ms -- the engine's device clock. */
+int fl_configure(fl_handle* h, int use_graphs, int profile_every, int time_steps);
+/* Device time of the last fl_step or fl_shuffle (synchronises on it). */
+int fl_last_duration_ms(fl_handle* h, float* ms);
 int fl_profile(fl_handle* h, int enable);
 /* Drains pending records (synchronises on them) and returns the totals since the
  * last fl_profile(h, 1): summed milliseconds, launch records and algorithmic

@@ -113,6 +113,8 @@ struct fl_handle {
   };
   std::map<std::tuple<int, int, int, int>, GraphEntry> graphs;
   bool use_graphs = true;
+  bool time_steps = false;            // device clock: bracket each step/shuffle with events
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
   int prof_every = 8;
   int64_t step_counter = 0;
   std::vector<Rec>* sink = nullptr;   // where ProfScope records go (null: pending)
@@ -147,13 +149,15 @@ struct ProfScope {
   ProfScope(fl_handle* h_, int c, cudaStream_t st) : h(h_), cls(c), s(st) {
     if (h->prof) {
       a = h->ev();
-      cudaEventRecord(a, s);
+      // inside stream capture a plain record is only a capture dependency;
+      // External makes it a real event-record node that can be timed
+      cudaEventRecordWithFlags(a, s, h->capturing ? cudaEventRecordExternal : 0);
     }
   }
   ~ProfScope() {
     if (a) {
       cudaEvent_t b = h->ev();
-      cudaEventRecord(b, s);
+      cudaEventRecordWithFlags(b, s, h->capturing ? cudaEventRecordExternal : 0);
       (h->sink ? *h->sink : h->pending).push_back({cls, a, b, bytes});
     }
   }
@@ -302,6 +306,8 @@ int fl_destroy(fl_handle* h) {
     cudaEventDestroy(r.b);
   }
   for (auto e : h->ev_pool) cudaEventDestroy(e);
+  if (h->t0) cudaEventDestroy(h->t0);
+  if (h->t1) cudaEventDestroy(h->t1);
   for (auto& kv : h->graphs) {
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
     for (auto& r : kv.second.recs) {
@@ -340,10 +346,22 @@ int fl_comm_init(fl_handle* h, const void* idp, int rank, int world) {
 
 int64_t fl_kernel_launches(const fl_handle*) { return fl::g_launches.load(); }
 
-int fl_configure(fl_handle* h, int use_graphs, int profile_every) {
+int fl_configure(fl_handle* h, int use_graphs, int profile_every, int time_steps) {
   if (!h || profile_every < 1) return fail(FL_EINVAL, "bad configure arguments");
   h->use_graphs = use_graphs != 0;
   h->prof_every = profile_every;
+  h->time_steps = time_steps != 0;
+  if (h->time_steps && !h->t0) {
+    FL_CUDA(cudaEventCreate(&h->t0));
+    FL_CUDA(cudaEventCreate(&h->t1));
+  }
+  return FL_OK;
+}
+
+int fl_last_duration_ms(fl_handle* h, float* ms) {
+  if (!h || !ms || !h->t0) return fail(FL_EINVAL, "timing not enabled (fl_configure)");
+  FL_CUDA(cudaEventSynchronize(h->t1));
+  FL_CUDA(cudaEventElapsedTime(ms, h->t0, h->t1));
   return FL_OK;
 }
 
@@ -548,6 +566,7 @@ extern "C" int fl_step(fl_handle* h, const fl_row* rows, int n_rows, int n_dec, 
   const bool want_logits = logits_out != nullptr;
   const bool profiled = h->prof && (h->step_counter++ % h->prof_every == 0);
   if (!h->use_graphs) {
+    if (h->time_steps) FL_CUDA(cudaEventRecord(h->t0, s));
     if (h->prof && !profiled) {
       const bool save = h->prof;
       h->prof = false;
@@ -588,10 +607,11 @@ extern "C" int fl_step(fl_handle* h, const fl_row* rows, int n_rows, int n_dec, 
       harvest(h, ge.recs);
       ge.pending = false;
     }
+    if (h->time_steps) FL_CUDA(cudaEventRecord(h->t0, s));   // after any capture work
     FL_CUDA(cudaGraphLaunch(ge.exec, s));
     ge.pending = profiled;
-    fl::g_launches += 0;
   }
+  if (h->time_steps) FL_CUDA(cudaEventRecord(h->t1, s));
   if (want_logits && n_dec > 0)
     FL_CUDA(cudaMemcpyAsync(logits_out, h->logits, sizeof(float) * n_dec * h->Vl,
                             cudaMemcpyDeviceToDevice, s));
@@ -611,9 +631,13 @@ extern "C" int fl_shuffle(fl_handle* h, const int32_t* moves, int n, void* strea
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   FL_CUDA(cudaMemcpyAsync(h->moves, moves, sizeof(int32_t) * 3 * n, cudaMemcpyHostToDevice, s));
+  if (h->time_steps) FL_CUDA(cudaEventRecord(h->t0, s));
+  {
   ProfScope ps(h, FL_PROF_SHUFFLE, s);
   fl::launch_shuffle(h->moves, n, h->p.kv, h->m.n_layer, h->p.pool_slots, h->Hl, h->p.max_seq,
                      h->m.head_dim, h->m.dtype, s);
+  }
+  if (h->time_steps) FL_CUDA(cudaEventRecord(h->t1, s));
   fl::g_launches += 1;
   FL_CUDA(cudaGetLastError());
   return FL_OK;

@@ -19,6 +19,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <string>
 #include <tuple>
@@ -464,14 +465,16 @@ int gemm_tc(TcWorkspace* ws, const GemmArgs& a, cudaStream_t s) {
   const int tiles = ((a.N + TC_BM - 1) / TC_BM) * ((a.M + bn - 1) / bn);
   const int kch = a.K / TC_BK;
   // split K across a cluster of S CTAs until the tiles cover the SMs
+  static const int force_s = getenv("FL_TC_SPLIT") ? atoi(getenv("FL_TC_SPLIT")) : 0;
   int S = 1;
-  while (S < 8 && tiles * S * 2 <= ws->num_sms && kch / (S * 2) >= 1) S *= 2;
+  while (S < 4 && tiles * S * 2 <= ws->num_sms && kch / (S * 2) >= 1) S *= 2;
+  if (force_s > 0) S = force_s;
   const int kpc = (kch + S - 1) / S;
   switch (bn) {
-    case 16: return launch_bn<16, 8>(a, mw, mx, S, kpc, s);
-    case 32: return launch_bn<32, 8>(a, mw, mx, S, kpc, s);
-    case 64: return launch_bn<64, 6>(a, mw, mx, S, kpc, s);
-    case 128: return launch_bn<128, 4>(a, mw, mx, S, kpc, s);
+    case 16: return launch_bn<16, 12>(a, mw, mx, S, kpc, s);
+    case 32: return launch_bn<32, 10>(a, mw, mx, S, kpc, s);
+    case 64: return launch_bn<64, 8>(a, mw, mx, S, kpc, s);
+    case 128: return launch_bn<128, 6>(a, mw, mx, S, kpc, s);
     default: return launch_bn<256, 4>(a, mw, mx, S, kpc, s);
   }
 }

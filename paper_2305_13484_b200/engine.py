@@ -91,7 +91,8 @@ class FusionStream:
 
     def __init__(self, requests, params: CostParams, tp: TPConfig,
                  shuffle_enabled: bool = True, record_tokens: bool = True,
-                 slot_capacity: int | None = None, *, executor=None, clock: str = "cost"):
+                 slot_capacity: int | None = None, *, executor=None, clock: str = "cost",
+                 max_window: int | None = None):
         if clock not in ("cost", "device"):
             raise InvalidParam(f"clock must be 'cost' or 'device', got {clock!r}")
         if clock == "device" and executor is None:
@@ -102,6 +103,10 @@ class FusionStream:
         self.record_tokens = record_tokens
         self.executor = executor
         self.clock = clock
+        # admission control (extension; None = reference semantics): contexts
+        # stay queued while the live window already spans max_window slots,
+        # i.e. while the device KV pool is full
+        self.max_window = max_window
         self.now = 0.0
         self.iteration_index = 0
         self.layout = BufferLayout(capacity=slot_capacity)
@@ -115,6 +120,7 @@ class FusionStream:
         self._finish_at: dict = {}    # iteration index -> [rid] in fusion order
         self._finish_of: dict = {}    # rid -> iteration index
         self.device_ms: list = []     # per-iteration device time (executor runs)
+        self.widest_window = 0        # widest live window seen (rows per iteration)
 
         pending = []
         for req in sorted(requests, key=lambda r: (r.arrival_time, r.request_id)):
@@ -171,7 +177,10 @@ class FusionStream:
         """Admit, in FIFO order, every context ready at or before ``now``."""
         n = 0
         pend = self.pending
+        cap = self.max_window
         while self._next_pending < len(pend) and pend[self._next_pending].ready_time <= self.now:
+            if cap is not None and self.layout.buffer_size >= cap:
+                break
             ctx = pend[self._next_pending]
             self._next_pending += 1
             rid = ctx.request_id
@@ -192,6 +201,8 @@ class FusionStream:
         if not self.active:
             raise EmptyStream("no fused requests to iterate")
         lay = self.layout
+        if lay.buffer_size > self.widest_window:
+            self.widest_window = lay.buffer_size
         dev = None
         if self.executor is not None:
             dev = self.executor.run_iteration(self)
@@ -243,10 +254,11 @@ class FusionStream:
 
 def run_fusion(requests, params: CostParams, tp: TPConfig | None = None,
                shuffle_enabled: bool = True, record_tokens: bool = True, *,
-               executor=None, clock: str = "cost") -> Trace:
+               executor=None, clock: str = "cost", max_window: int | None = None) -> Trace:
     """Serve every request to completion on one fused stream."""
     stream = FusionStream(requests, params, tp or TPConfig(), shuffle_enabled=shuffle_enabled,
-                          record_tokens=record_tokens, executor=executor, clock=clock)
+                          record_tokens=record_tokens, executor=executor, clock=clock,
+                          max_window=max_window)
     drive(stream)
     trace = Trace("fusion" if shuffle_enabled else "fusion_noshuffle", stream.events)
     trace.sort()

@@ -65,7 +65,8 @@ class CudaExecutor:
         self.dtype = dtype
         self.tp_rank, self.tp_size = tp_rank, tp_size
         self.device = torch.device(device)
-        self.C = pool_slots
+        self._auto_pool = not pool_slots
+        self.C = pool_slots or 1
         self.R = state_slots
         self.max_new = max_new_tokens
         if max_seq is None:
@@ -105,6 +106,16 @@ class CudaExecutor:
             ptr("w_lm"), ptr("b_lm"), C.cast(self._layer_ptrs, C.POINTER(C.c_void_p)))
 
         # ---- KV pool and per-request state
+        if self._auto_pool:
+            # as many slots as fit in free HBM after weights, keeping 6 GB for
+            # the workspace and the allocator
+            es = 2 if dtype == "bf16" else 4
+            slot = spec.n_layer * 2 * hl * self.S * spec.head_dim * es
+            free, _ = torch.cuda.mem_get_info(self.device)
+            self.C = max(1, min(state_slots, int((free - 6 * 2**30) // slot)))
+            self.max_rows = bucket(max_rows or (self.C + 16 * (input_len or 32)))
+            if self.max_rows < bucket(self.C) + 64:
+                self.max_rows = bucket(bucket(self.C) + 64)
         self.kv = torch.empty((spec.n_layer, self.C, 2, hl, self.S, spec.head_dim), dtype=tdt,
                               device=self.device)
         i32 = dict(dtype=torch.int32, device=self.device)
@@ -125,12 +136,17 @@ class CudaExecutor:
         h = C.c_void_p()
         _lib.check(self.lib.fl_create(C.byref(self.mdesc), C.byref(self.pdesc), C.byref(h)))
         self.handle = h
-        _lib.check(self.lib.fl_configure(self.handle, int(use_graphs), 8))
+        self.use_graphs = use_graphs
+        self._lib_timing = False
+        _lib.check(self.lib.fl_configure(self.handle, int(use_graphs), 8, 0))
         if tp_size > 1:
             if comm_id is None:
                 raise InvalidParam("tp_size > 1 needs comm_id (see tp.make_comm_id)")
             buf = C.create_string_buffer(bytes(comm_id), 128)
             _lib.check(self.lib.fl_comm_init(self.handle, buf, tp_rank, tp_size))
+
+        self.cs = torch.cuda.Stream(device=self.device)
+        torch.cuda.synchronize(self.device)      # weights / pool written on the default stream
 
         # ---- host bookkeeping
         self.capture_logits = capture_logits
@@ -183,7 +199,9 @@ class CudaExecutor:
     # ----------------------------------------------------------------- utils
     @property
     def stream(self):
-        return torch.cuda.current_stream(self.device)
+        """The executor's own (non-default) stream: CUDA graphs cannot be
+        captured on the legacy default stream."""
+        return self.cs
 
     def launches(self) -> int:
         return int(self.lib.fl_kernel_launches(self.handle))
@@ -270,7 +288,6 @@ class CudaExecutor:
 
     def run_iteration(self, stream) -> float | None:
         layout = stream.layout
-        self._device_clock = stream.clock == "device"
         has_new = bool(self._new)
         changed = has_new or self._prev_had_new or layout.version != self._rows_version
         if changed:
@@ -282,17 +299,22 @@ class CudaExecutor:
         if has_new:
             self._prefill_ctx = 0
         cs = self.stream
-        timed = stream.clock == "device" or self.time_steps
+        dev_clock = stream.clock == "device"
+        self._set_timing(dev_clock)
+        timed = not dev_clock and self.time_steps
         if timed:
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(cs)
+        dev_ms = 0.0
         logits_ptr = self.logits_buf.data_ptr() if self.capture_logits else None
         if changed and self._pre_passes:
             for chunk in self._pre_passes:
                 arr = (_lib.Row * len(chunk))(*[_lib.Row(*r) for r in chunk])
                 _lib.check(self.lib.fl_step(self.handle, arr, len(chunk), 0, 1, None,
                                             C.c_void_p(cs.cuda_stream)))
+                if dev_clock:
+                    dev_ms += self._last_ms()
                 self.rows_total += len(chunk)
                 self.prefill_rows_total += len(chunk)
                 self.h2d_bytes += len(chunk) * C.sizeof(_lib.Row)
@@ -310,21 +332,31 @@ class CudaExecutor:
         if self.capture_logits:
             rids = [r.rid for r in self._rows[:self._n_dec]]
             kinds = [r.kind for r in self._rows[:self._n_dec]]
-            self.logits_log.append((stream.iteration_index, rids, kinds,
-                                    self.logits_buf[:self._n_dec].float().cpu()))
+            with torch.cuda.stream(cs):
+                lg = self.logits_buf[:self._n_dec].float().cpu()
+            self.logits_log.append((stream.iteration_index, rids, kinds, lg))
         self._prev_had_new = has_new
         self._new = []
         for info in self._live.values():
             info["gen"] += 1
         self._live_ctx += len(self._live)
+        if dev_clock:
+            dev_ms += self._last_ms()
+            return self.clock_reduce(dev_ms) if self.clock_reduce else dev_ms
         if timed:
             e1.record(cs)
-            if stream.clock == "device":
-                e1.synchronize()
-                ms = e0.elapsed_time(e1)
-                return self.clock_reduce(ms) if self.clock_reduce else ms
             self._events.append((e0, e1))
         return None
+
+    def _set_timing(self, on: bool):
+        if on != self._lib_timing:
+            _lib.check(self.lib.fl_configure(self.handle, int(self.use_graphs), 8, int(on)))
+            self._lib_timing = on
+
+    def _last_ms(self) -> float:
+        ms = C.c_float()
+        _lib.check(self.lib.fl_last_duration_ms(self.handle, C.byref(ms)))
+        return float(ms.value)
 
     def on_shuffle(self, plan) -> float | None:
         moves = []
@@ -337,28 +369,21 @@ class CudaExecutor:
         flat = (C.c_int32 * (3 * len(moves)))(*[v for mv in moves for v in mv])
         self.h2d_bytes += 12 * len(moves)
         cs = self.stream
-        e0 = e1 = None
-        if self.time_steps or getattr(self, "_device_clock", False):
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(cs)
         _lib.check(self.lib.fl_shuffle(self.handle, flat, len(moves), C.c_void_p(cs.cuda_stream)))
         self.shuffles += 1
         for s in [m.src_slot for m in plan.moves]:
             self._orphans.pop(s, None)
-        if e0 is not None:
-            e1.record(cs)
-            e1.synchronize()
-            ms = e0.elapsed_time(e1)
+        if self._lib_timing:
+            ms = self._last_ms()
             return self.clock_reduce(ms) if self.clock_reduce else ms
         return None
 
     def on_drain(self, stream):
-        torch.cuda.current_stream(self.device).synchronize()
+        self.cs.synchronize()
 
     # ----------------------------------------------------------------- results
     def step_times_ms(self) -> list:
-        torch.cuda.current_stream(self.device).synchronize()
+        self.cs.synchronize()
         return [a.elapsed_time(b) for a, b in self._events]
 
     def tokens(self, rids=None) -> dict:
@@ -367,8 +392,9 @@ class CudaExecutor:
         rids = list(self.seen if rids is None else rids)
         if not rids:
             return {}
-        idx = torch.tensor([r % self.R for r in rids], device=self.device, dtype=torch.long)
-        packed = torch.cat([self.req_ngen[idx].unsqueeze(1), self.tok_hist[idx]], dim=1).cpu()
+        with torch.cuda.stream(self.cs):
+            idx = torch.tensor([r % self.R for r in rids], device=self.device, dtype=torch.long)
+            packed = torch.cat([self.req_ngen[idx].unsqueeze(1), self.tok_hist[idx]], dim=1).cpu()
         self.d2h_bytes = packed.numel() * 4
         return {rid: packed[i, 1:1 + int(packed[i, 0])].tolist() for i, rid in enumerate(rids)}
 

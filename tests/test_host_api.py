@@ -232,3 +232,24 @@ def test_metrics_percentile_convention():
     assert fl.percentile([5.0], 99.0) == 5.0
     with pytest.raises(fl.InvalidParam):
         fl.percentile([], 50.0)
+
+
+def test_admission_control_caps_the_window():
+    """Extension: max_window keeps contexts queued while the KV pool is full."""
+    sc = fl.Scenario("x", fl.Discipline.FUSION, 40, fl.PoissonArrival(2.0), fl.UniformLength(3, 30), 30)
+    reqs = fl.build_requests(sc, 3)
+    for shuffle in (True, False):
+        st = fl.FusionStream(reqs, fl.CostParams(), fl.TPConfig(), shuffle_enabled=shuffle,
+                             max_window=5)
+        fl.drive(st)
+        assert st.widest_window <= 5
+        tr = fl.Trace("f", st.events)
+        toks = {}
+        for e in tr.events:
+            if e.kind is EK.TOKEN_GENERATED:
+                toks[e.request_id] = toks.get(e.request_id, 0) + 1
+        assert toks == {r.request_id: r.actual_output_length for r in reqs}
+    # None keeps the reference schedule
+    a = fl.run_fusion(reqs, fl.CostParams()).format_lines()
+    b = fl.run_fusion(reqs, fl.CostParams(), max_window=None).format_lines()
+    assert a == b

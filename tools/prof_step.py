@@ -27,6 +27,7 @@ prompts = fl.synthetic_prompts(reqs, spec.vocab, 1)
 ex = CudaExecutor(spec, prompts, dtype=cfg["dtype"], pool_slots=max(a.rows, 8), input_len=cfg["input_len"],
                   max_new_tokens=cfg["max_out"], state_slots=1024, max_rows=max(a.rows, 8) + 256)
 st = fl.FusionStream(reqs, fl.CostParams(preprocess_ms=0.0), fl.TPConfig(), executor=ex, record_tokens=False)
+torch.cuda.set_stream(ex.cs)
 st.try_fuse_pending()
 st.step_iteration()            # admission step (prefill rows)
 for _ in range(5):
