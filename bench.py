@@ -279,7 +279,7 @@ def run_ours(args, cfg):
     torch.cuda.synchronize()
     ex.profile(True)
     l0 = ex.launches()
-    ctx0, rows0, it0, mv0 = ex.attn_ctx_rows, ex.rows_total, ex.iterations, ex.moved_kv_bytes
+    rows0, it0, mv0 = ex.rows_total, ex.iterations, ex.moved_kv_bytes
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     streams = []
     with ClockSampler(local) as clk:
@@ -293,6 +293,7 @@ def run_ours(args, cfg):
     ms = e0.elapsed_time(e1)
     launches = ex.launches() - l0
     prof = ex.profile_read()
+    att_bytes = ex.attn_bytes_profiled     # K4 bytes of exactly the profiled steps
     ex.profile(False)
     if world > 1:
         t = torch.tensor([ms], device="cuda")
@@ -323,13 +324,6 @@ def run_ours(args, cfg):
     peaks, peak_src = load_peaks()
     hbm = float(peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"]))
     tf_sus = float(peaks.get("bf16_tflops_sustained", FALLBACK_PEAKS["bf16_tflops_sustained"]))
-    att_bytes = ex.attention_bytes() * 1.0
-    # attention_bytes() is cumulative since construction: scale to the timed region
-    frac_rows = (ex.attn_ctx_rows - ctx0) / max(1, ex.attn_ctx_rows)
-    es = 2 if cfg["dtype"] == "bf16" else 4
-    hl = spec.n_head // world
-    att_bytes = spec.n_layer * ((ex.attn_ctx_rows - ctx0) * 2 * hl * spec.head_dim * es
-                                + (ex.rows_total - rows0) * 2 * hl * spec.head_dim * es)
     kern = {}
     a = prof["attention"]
     if a["records"]:

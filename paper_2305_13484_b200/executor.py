@@ -177,6 +177,12 @@ class CudaExecutor:
         self.d2h_bytes = 0
         self.attn_ctx_rows = 0            # sum over iterations of sum_rows ctx_r
         self._live_ctx = 0                # sum over live requests of (P + gen)
+        self._tail_ctx = 0
+        self.attn_bytes_total = 0.0
+        self.attn_bytes_profiled = 0.0
+        self._fl_calls = 0
+        self._profiling = False
+        self.prof_every = 8
         self._orphan_ctx = 0
         self._prefill_ctx = 0
         self.clock_reduce = None          # callable(ms) -> ms agreed across TP ranks
@@ -280,6 +286,7 @@ class CudaExecutor:
             chunk = head[i:i + self.max_rows]
             self._pre_passes.append(chunk + [_PAD] * (bucket(len(chunk)) - len(chunk)))
         rows.extend(tail)
+        self._tail_ctx = sum(r[2] + 1 for r in tail)
         rows.extend([_PAD] * (bucket(len(rows)) - len(rows)))
         if len(rows) > self.max_rows:
             rows = rows[:self.max_rows]       # padding only; real rows always fit
@@ -295,9 +302,8 @@ class CudaExecutor:
             self._rows_version = layout.version
             self.h2d_bytes += self._n_rows * C.sizeof(_lib.Row)
             self._orphan_ctx = sum(r.ctx for r in self._rows[:self._n_dec] if r.kind == _lib.ROW_ORPHAN)
-        self.attn_ctx_rows += self._live_ctx + self._orphan_ctx + (self._prefill_ctx if has_new else 0)
-        if has_new:
-            self._prefill_ctx = 0
+        main_ctx = self._live_ctx + self._orphan_ctx + (self._tail_ctx if changed else 0)
+        self._tail_ctx = 0
         cs = self.stream
         dev_clock = stream.clock == "device"
         self._set_timing(dev_clock)
@@ -313,6 +319,7 @@ class CudaExecutor:
                 arr = (_lib.Row * len(chunk))(*[_lib.Row(*r) for r in chunk])
                 _lib.check(self.lib.fl_step(self.handle, arr, len(chunk), 0, 1, None,
                                             C.c_void_p(cs.cuda_stream)))
+                self._account(sum(r[2] + 1 for r in chunk), len(chunk))
                 if dev_clock:
                     dev_ms += self._last_ms()
                 self.rows_total += len(chunk)
@@ -321,6 +328,7 @@ class CudaExecutor:
             self._pre_passes = []
         _lib.check(self.lib.fl_step(self.handle, self._rows, self._n_rows, self._n_dec, int(changed),
                                     logits_ptr, C.c_void_p(cs.cuda_stream)))
+        self._account(main_ctx, self._n_rows)
         self.iterations += 1
         self.rows_total += self._n_rows
         self.prefill_rows_total += self._n_rows - self._n_dec
@@ -347,6 +355,19 @@ class CudaExecutor:
             e1.record(cs)
             self._events.append((e0, e1))
         return None
+
+    def _account(self, ctx_sum: int, n_rows: int):
+        """Algorithmic HBM bytes of this fl_step's K4 launches: K and
+        V over every row's context plus q in / out, for all layers."""
+        es = 2 if self.dtype == "bf16" else 4
+        hl = self.spec.n_head // self.tp_size
+        b = self.spec.n_layer * (ctx_sum * 2 * hl * self.spec.head_dim * es
+                                 + n_rows * 2 * hl * self.spec.head_dim * es)
+        self.attn_ctx_rows += ctx_sum
+        self.attn_bytes_total += b
+        if self._profiling and self._fl_calls % self.prof_every == 0:
+            self.attn_bytes_profiled += b
+        self._fl_calls += 1
 
     def _set_timing(self, on: bool):
         if on != self._lib_timing:
@@ -398,17 +419,14 @@ class CudaExecutor:
         self.d2h_bytes = packed.numel() * 4
         return {rid: packed[i, 1:1 + int(packed[i, 0])].tolist() for i, rid in enumerate(rids)}
 
-    def attention_bytes(self) -> float:
-        """Algorithmic HBM bytes of K4 summed over all launches so far:
-        K and V of every row's context plus q in / out."""
-        es = 2 if self.dtype == "bf16" else 4
-        hl = self.spec.n_head // self.tp_size
-        per_pos = 2 * hl * self.spec.head_dim * es
-        return float(self.spec.n_layer) * (self.attn_ctx_rows * per_pos
-                                           + self.rows_total * 2 * hl * self.spec.head_dim * es)
-
     def profile(self, enable: bool):
+        """Live kernel timing: the library brackets launch groups with events on
+        one fl_step in ``prof_every`` (counting from here); the executor keeps
+        the algorithmic attention bytes of exactly those steps."""
         _lib.check(self.lib.fl_profile(self.handle, int(enable)))
+        self._profiling = bool(enable)
+        self._fl_calls = 0
+        self.attn_bytes_profiled = 0.0
 
     def profile_read(self) -> dict:
         out = {}
