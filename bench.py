@@ -259,9 +259,9 @@ def run_ours(args, cfg):
         from paper_2305_13484_b200.tp import max_reduce_clock
         ex.clock_reduce = max_reduce_clock(local)
 
-    def serve(read_tokens=False):
+    def serve(read_tokens=False, subset=None):
         ex.reset()
-        st = fl.FusionStream(reqs, params, fl.TPConfig(tp_size=world), shuffle_enabled=True,
+        st = fl.FusionStream(reqs if subset is None else reqs[:subset], params, fl.TPConfig(tp_size=world), shuffle_enabled=True,
                              record_tokens=True, executor=ex, clock="device", max_window=ex.C)
         fl.drive(st)
         toks = ex.tokens() if read_tokens else None
@@ -272,8 +272,10 @@ def run_ours(args, cfg):
             dist.barrier()
 
     torch.cuda.set_stream(ex.cs)       # every event below is on the executor's stream
-    for _ in range(args.warmup):
-        serve()
+    # warm-up: one full serve (captures the CUDA graph of every step shape),
+    # then serves of a 1/4 prefix of the stream
+    for i in range(args.warmup):
+        serve(subset=None if i == 0 else max(1, len(reqs) // 4))
     # ---- timed region (device-resident inputs)
     barrier()
     torch.cuda.synchronize()
@@ -310,15 +312,16 @@ def run_ours(args, cfg):
     h0 = ex.h2d_bytes
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     d2h = 0
+    e2e_steps = min(args.steps, 2)
     e2.record()
-    for _ in range(args.steps):
+    for _ in range(e2e_steps):
         _, toks = serve(read_tokens=True)
         d2h += ex.d2h_bytes
     e3.record()
     torch.cuda.synchronize()
     barrier()
     e2e_ms = e2.elapsed_time(e3)
-    h2d = (ex.h2d_bytes - h0 + sum(4 * len(p) for p in prompts.values()) * args.steps)
+    h2d = (ex.h2d_bytes - h0 + sum(4 * len(p) for p in prompts.values()) * e2e_steps)
 
     # ---- roofline of the dominant kernel class
     peaks, peak_src = load_peaks()
@@ -386,8 +389,9 @@ def run_ours(args, cfg):
             "pool_slots": ex.C,
             "widest_window": max(s.widest_window for s in streams),
             "mean_rows_per_iteration": (ex.rows_total - rows0) / max(1, iters),
-            "e2e": {"value": tokens / (e2e_ms / 1000.0), "unit": "tokens/s",
-                    "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps},
+            "e2e": {"value": tokens / args.steps * e2e_steps / (e2e_ms / 1000.0), "unit": "tokens/s",
+                    "h2d_bytes_per_step": h2d // e2e_steps, "d2h_bytes_per_step": d2h // e2e_steps,
+                    "steps": e2e_steps},
             "gpu_launches": launches,
             "roofline": roofline,
             "kernels": kern,
@@ -413,7 +417,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.config is None:
-        args.config = "c2" if args.gpus == 1 else "c3"
+        args.config = "c3"      # the TP 1/2/4/8 config BASELINE's metric is quoted on
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)
