@@ -181,6 +181,13 @@ int fl_profile_read(fl_handle* h, int cls, double* total_ms, int64_t* records, d
  * uses (use_tc: 1 tcgen05, 0 SIMT).  epi: 0 store(dtype) 1 gelu(dtype)
  * 2 accumulate(f32) 3 store(f32).  workspace: >= fl_gemm_workspace_bytes(). */
 size_t fl_gemm_workspace_bytes(void);
+/* Diagnostic entry: K4 alone.  q [M, Hl*hd]; rows (device) give the slot of each
+ * row, row_ctx (device) its context length; kv_layer is one layer of the pool
+ * [C][2][Hl][S][hd]; out [M, Hl*hd].  workspace >= fl_attention_workspace_bytes. */
+size_t fl_attention_workspace_bytes(int M, int Hl, int hd, int S);
+int fl_attention(const void* q, const fl_row* rows, const int32_t* row_ctx, int M, int Hl, int hd,
+                 const void* kv_layer, int C, int S, void* out, void* workspace, int dtype,
+                 void* cuda_stream);
 int fl_gemm(const void* x, int ldx, const void* w, const void* bias, void* out, int ldo, int M,
             int N, int K, int epi, int dtype, int use_tc, void* workspace, void* cuda_stream);
 

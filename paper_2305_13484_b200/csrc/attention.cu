@@ -35,161 +35,275 @@ int attn_keys_per_split(int row_heads, int S) {
   return (keys + ATT_CHUNK - 1) / ATT_CHUNK * ATT_CHUNK;
 }
 
+// ---------------------------------------------------------------------------
+// Persistent, TMA-staged decode attention.
+//
+// Work items are (row, head, split) triples; a grid of ~2 CTAs per SM walks
+// them round-robin.  Warp CW (the producer) streams each item's K and V rows
+// tile by tile with 1-D bulk copies (cp.async.bulk ... mbarrier::complete_tx)
+// into a STAGES-deep shared-memory ring and runs ahead across item
+// boundaries, so HBM sees a continuous stream.  CW consumer warps read the
+// tiles from shared memory with 16-byte vector loads: a lane group of G
+// lanes owns one key at a time (dot product + shuffle reduction), keeps its
+// own online-softmax state (m, l, acc) and the groups are merged through
+// shared memory at the end of the item -- no per-tile block barriers.
 template <typename T, int HD>
-__global__ void __launch_bounds__(ATT_THREADS) k_attn_split(
+struct AttnCfg {
+  static constexpr int VEC = 16 / sizeof(T);             // elements per 16-byte vector
+  static constexpr int NV = HD / VEC;                     // vectors per K/V row
+  // 8 lanes per key: 3-level shuffle reductions and 4 independent keys per
+  // warp-step; a warp-wide 16-byte load then spans 4 K rows (4 wavefronts,
+  // the minimum for 512 bytes) so the layout costs no extra bank conflicts
+  static constexpr int G = NextPow2<NV>::v < 8 ? NextPow2<NV>::v : 8;   // lanes per key
+  static constexpr int PER = (NV + G - 1) / G;            // vectors per lane
+  static constexpr int KPW = 32 / G;                      // keys per warp-step
+  static constexpr int CW = 4;                            // consumer warps
+  static constexpr int THREADS = (CW + 1) * 32;
+  static constexpr int ROW = HD * sizeof(T);              // bytes per key row
+  static constexpr int TK = (16384 / ROW) / (CW * KPW) * (CW * KPW);   // keys per tile
+  static constexpr int STAGES = 3;
+  static constexpr int STAGE_BYTES = 2 * TK * ROW;        // K tile + V tile
+  static constexpr int SMEM = STAGES * STAGE_BYTES;
+};
+
+FL_DEV uint32_t smem_addr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+FL_DEV void mbar_init_(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+FL_DEV void mbar_expect_tx_(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes) : "memory");
+}
+FL_DEV void mbar_arrive_(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+FL_DEV void mbar_wait_(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred done;\n"
+      "AWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+      "@!done bra AWAIT_%=;\n\t}" ::"r"(smem_addr(bar)), "r"(parity) : "memory");
+}
+FL_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+template <typename T>
+FL_DEV void widen16(const uint4& raw, float* out) {
+  if constexpr (sizeof(T) == 4) {
+    out[0] = __uint_as_float(raw.x); out[1] = __uint_as_float(raw.y);
+    out[2] = __uint_as_float(raw.z); out[3] = __uint_as_float(raw.w);
+  } else {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float2 f = __bfloat1622float2(h[j]);
+      out[2 * j] = f.x; out[2 * j + 1] = f.y;
+    }
+  }
+}
+
+template <typename T, int HD>
+__global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
     const T* __restrict__ q, const fl_row* __restrict__ rows, const int32_t* __restrict__ row_ctx,
-    int Hl, const T* __restrict__ kv_layer, int S, T* __restrict__ out, float* __restrict__ ws_o,
-    float* __restrict__ ws_ml, int max_splits, int keys_per_split) {
-  pdl_trigger();
-  pdl_wait();
-  constexpr int VEC = 16 / sizeof(T);          // elements per 16-byte load
-  constexpr int NV = HD / VEC;                  // 16-byte vectors per key row
-  constexpr int G = NextPow2<NV>::v;            // lanes per key (power of two, <= 32)
-  constexpr int PER = (NV + G - 1) / G;         // vectors per lane
-  constexpr int KPW = 32 / G;                   // keys per warp per step
-  constexpr int NW = ATT_THREADS / 32;
-  constexpr int NG = ATT_THREADS / NV > 0 ? ATT_THREADS / NV : 1;   // key groups in P.V
+    int M, int Hl, const T* __restrict__ kv_layer, int S, T* __restrict__ out,
+    float* __restrict__ ws_o, float* __restrict__ ws_ml, int max_splits, int keys_per_split,
+    int splits) {
+  using Cfg = AttnCfg<T, HD>;
+  constexpr int VEC = Cfg::VEC, NV = Cfg::NV, G = Cfg::G, PER = Cfg::PER, KPW = Cfg::KPW;
+  constexpr int CW = Cfg::CW, TK = Cfg::TK, STAGES = Cfg::STAGES, NP = CW;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full[STAGES];
+  __shared__ __align__(8) uint64_t empty[STAGES];
+  __shared__ float s_m[NP], s_l[NP];
+  __shared__ __align__(16) float s_acc[NP][HD];
 
-  __shared__ float s_p[ATT_CHUNK];
-  __shared__ float s_red[32];
-  __shared__ __align__(16) float s_acc[NG][HD];
-
-  const int split = blockIdx.x, h = blockIdx.y, r = blockIdx.z;
-  const int ctx = row_ctx[r];
-  const int kb0 = split * keys_per_split;
-  if (kb0 >= ctx) return;
-  const int kb1 = min(ctx, kb0 + keys_per_split);
-  const int nsplit = (ctx + keys_per_split - 1) / keys_per_split;
-  const int slot = rows[r].slot;
-  const int D = Hl * HD;
-
-  const T* Kb = kv_layer + ((static_cast<size_t>(slot) * 2 + 0) * Hl + h) * static_cast<size_t>(S) * HD;
-  const T* Vb = kv_layer + ((static_cast<size_t>(slot) * 2 + 1) * Hl + h) * static_cast<size_t>(S) * HD;
-  const T* qr = q + static_cast<size_t>(r) * D + h * HD;
-
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane % G;           // lane within key group
-  const int kw = lane / G;          // key slot within warp
-  const float scale = rsqrtf(static_cast<float>(HD));
-
-  float qv[PER][VEC];
-#pragma unroll
-  for (int p = 0; p < PER; ++p) {
-    const int vi = g + p * G;
-    if (vi < NV) {
-      load16(qr + vi * VEC, qv[p]);
-#pragma unroll
-      for (int j = 0; j < VEC; ++j) qv[p][j] *= scale;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init_(&full[i], 1);
+      mbar_init_(&empty[i], CW);
     }
-  }
-
-  const int vi = threadIdx.x % NV;     // P.V: this thread's 16-byte slice of a V row
-  const int kg = threadIdx.x / NV;     // ... and its key group
-  float acc[VEC];
-#pragma unroll
-  for (int j = 0; j < VEC; ++j) acc[j] = 0.f;
-  float m_run = -INFINITY, l_run = 0.f;
-
-  for (int c0 = kb0; c0 < kb1; c0 += ATT_CHUNK) {
-    const int nk = min(ATT_CHUNK, kb1 - c0);
-    // ---- scores of this chunk (lane group per key, 16-byte K loads)
-    float local_max = -INFINITY;
-    for (int kb = warp * KPW; kb < nk; kb += NW * KPW) {
-      const int k = kb + kw;
-      float dot = 0.f;
-      if (k < nk) {
-        const T* kr = Kb + static_cast<size_t>(c0 + k) * HD;
-#pragma unroll
-        for (int p = 0; p < PER; ++p) {
-          const int v2 = g + p * G;
-          if (v2 < NV) {
-            float kf[VEC];
-            uint4 raw = ld_stream16(kr + v2 * VEC);
-            if constexpr (sizeof(T) == 4) {
-              kf[0] = __uint_as_float(raw.x); kf[1] = __uint_as_float(raw.y);
-              kf[2] = __uint_as_float(raw.z); kf[3] = __uint_as_float(raw.w);
-            } else {
-              const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&raw);
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                float2 f = __bfloat1622float2(hh[j]);
-                kf[2 * j] = f.x; kf[2 * j + 1] = f.y;
-              }
-            }
-#pragma unroll
-            for (int j = 0; j < VEC; ++j) dot = fmaf(qv[p][j], kf[j], dot);
-          }
-        }
-      }
-#pragma unroll
-      for (int o = G / 2; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-      if (k < nk && g == 0) {
-        s_p[k] = dot;
-        local_max = fmaxf(local_max, dot);
-      }
-    }
-    local_max = warp_max(local_max);
-    if (lane == 0) s_red[warp] = local_max;
-    __syncthreads();
-    float m_c = s_red[0];
-#pragma unroll
-    for (int w = 1; w < NW; ++w) m_c = fmaxf(m_c, s_red[w]);
-    const float m_new = fmaxf(m_run, m_c);
-    const float rescale = __expf(m_run - m_new);   // 0 on the first chunk
-    __syncthreads();
-    float psum = 0.f;
-    for (int k = threadIdx.x; k < nk; k += ATT_THREADS) {
-      const float e = __expf(s_p[k] - m_new);
-      s_p[k] = e;
-      psum += e;
-    }
-    const float l_c = block_sum(psum, s_red);   // its __syncthreads publishes s_p
-    l_run = l_run * rescale + l_c;
-    m_run = m_new;
-    // ---- P.V of this chunk (16-byte V loads, NG key groups)
-#pragma unroll
-    for (int j = 0; j < VEC; ++j) acc[j] *= rescale;
-    if (kg < NG) {
-      for (int k = kg; k < nk; k += NG) {
-        const float pk = s_p[k];
-        float vf[VEC];
-        uint4 raw = ld_stream16(Vb + static_cast<size_t>(c0 + k) * HD + vi * VEC);
-        if constexpr (sizeof(T) == 4) {
-          vf[0] = __uint_as_float(raw.x); vf[1] = __uint_as_float(raw.y);
-          vf[2] = __uint_as_float(raw.z); vf[3] = __uint_as_float(raw.w);
-        } else {
-          const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&raw);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            float2 f = __bfloat1622float2(hh[j]);
-            vf[2 * j] = f.x; vf[2 * j + 1] = f.y;
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < VEC; ++j) acc[j] = fmaf(pk, vf[j], acc[j]);
-      }
-    }
-    __syncthreads();   // s_p is rewritten by the next chunk
-  }
-  if (kg < NG) {
-#pragma unroll
-    for (int j = 0; j < VEC; ++j) s_acc[kg][vi * VEC + j] = acc[j];
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < HD; e += ATT_THREADS) {
-    float o = 0.f;
-#pragma unroll 4
-    for (int gi = 0; gi < NG; ++gi) o += s_acc[gi][e];
-    if (nsplit == 1) {
-      out[static_cast<size_t>(r) * D + h * HD + e] = from_f<T>(o / l_run);
-    } else {
-      const size_t w = (static_cast<size_t>(r) * Hl + h) * max_splits + split;
-      ws_o[w * HD + e] = o;
-      if (e == 0) {
-        ws_ml[2 * w] = m_run;
-        ws_ml[2 * w + 1] = l_run;
+  pdl_trigger();
+  pdl_wait();       // q, row_ctx and this step's K/V rows come from predecessors
+
+  const int n_items = M * Hl * splits;
+  const int D = Hl * HD;
+  const size_t head_stride = static_cast<size_t>(S) * HD;
+
+  if (warp == CW) {
+    // ---------------- producer: one lane streams K/V tiles into the ring
+    if (lane == 0) {
+      int st = 0;
+      uint32_t ph = 0;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const int sp = item % splits;
+        const int rh = item / splits;
+        const int h = rh % Hl, r = rh / Hl;
+        const int ctx = row_ctx[r];
+        const int k0 = sp * keys_per_split;
+        if (k0 >= ctx) continue;
+        const int k1 = min(ctx, k0 + keys_per_split);
+        const size_t slot = rows[r].slot;
+        const T* Kb = kv_layer + ((slot * 2 + 0) * Hl + h) * head_stride;
+        const T* Vb = kv_layer + ((slot * 2 + 1) * Hl + h) * head_stride;
+        for (int t0 = k0; t0 < k1; t0 += TK) {
+          const int nk = min(TK, k1 - t0);
+          mbar_wait_(&empty[st], ph ^ 1);
+          uint8_t* buf = smem + st * Cfg::STAGE_BYTES;
+          mbar_expect_tx_(&full[st], 2u * nk * Cfg::ROW);
+          bulk_g2s(buf, Kb + static_cast<size_t>(t0) * HD, nk * Cfg::ROW, &full[st]);
+          bulk_g2s(buf + TK * Cfg::ROW, Vb + static_cast<size_t>(t0) * HD, nk * Cfg::ROW, &full[st]);
+          if (++st == STAGES) { st = 0; ph ^= 1; }
+        }
       }
     }
+    return;
+  }
+
+  // ---------------- consumers
+  const int g = lane % G;           // lane within the key group
+  const int kw = lane / G;          // key group within the warp
+
+  const float scale = rsqrtf(static_cast<float>(HD));
+  int st = 0;
+  uint32_t ph = 0;
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int sp = item % splits;
+    const int rh = item / splits;
+    const int h = rh % Hl, r = rh / Hl;
+    const int ctx = row_ctx[r];
+    const int k0 = sp * keys_per_split;
+    if (k0 >= ctx) continue;
+    const int k1 = min(ctx, k0 + keys_per_split);
+    const int nsplit = (ctx + keys_per_split - 1) / keys_per_split;
+
+    float qv[PER][VEC], acc[PER][VEC];
+    const T* qr = q + static_cast<size_t>(r) * D + h * HD;
+#pragma unroll
+    for (int p = 0; p < PER; ++p) {
+      const int vi = g + p * G;
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) acc[p][j] = 0.f;
+      if (vi < NV) {
+        load16(qr + vi * VEC, qv[p]);
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) qv[p][j] *= scale;
+      }
+    }
+    float m = -INFINITY, l = 0.f;
+
+    for (int t0 = k0; t0 < k1; t0 += TK) {
+      const int nk = min(TK, k1 - t0);
+      mbar_wait_(&full[st], ph);
+      const uint8_t* Ks = smem + st * Cfg::STAGE_BYTES;
+      const uint8_t* Vs = Ks + TK * Cfg::ROW;
+#pragma unroll 2
+      for (int kb = warp * KPW; kb < nk; kb += CW * KPW) {
+        const int k = kb + kw;
+        const bool valid = k < nk;
+        float dot = 0.f;
+        if (valid) {
+#pragma unroll
+          for (int p = 0; p < PER; ++p) {
+            const int vi = g + p * G;
+            if (vi < NV) {
+              float kf[VEC];
+              widen16<T>(*reinterpret_cast<const uint4*>(Ks + k * Cfg::ROW + vi * 16), kf);
+#pragma unroll
+              for (int j = 0; j < VEC; ++j) dot = fmaf(qv[p][j], kf[j], dot);
+            }
+          }
+        }
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+        if (valid) {
+          const float m_new = fmaxf(m, dot);
+          const float c = __expf(m - m_new);
+          const float pk = __expf(dot - m_new);
+          l = l * c + pk;
+          m = m_new;
+#pragma unroll
+          for (int p = 0; p < PER; ++p) {
+            const int vi = g + p * G;
+            if (vi < NV) {
+              float vf[VEC];
+              widen16<T>(*reinterpret_cast<const uint4*>(Vs + k * Cfg::ROW + vi * 16), vf);
+#pragma unroll
+              for (int j = 0; j < VEC; ++j) acc[p][j] = fmaf(pk, vf[j], acc[p][j] * c);
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_(&empty[st]);
+      if (++st == STAGES) { st = 0; ph ^= 1; }
+    }
+
+    // ---- merge the KPW key groups of this warp (same dims per lane g) ...
+#pragma unroll
+    for (int o = G; o < 32; o <<= 1) {
+      const float m_o = __shfl_xor_sync(0xffffffffu, m, o);
+      const float l_o = __shfl_xor_sync(0xffffffffu, l, o);
+      const float mx = fmaxf(m, m_o);
+      const float c1 = mx == -INFINITY ? 0.f : __expf(m - mx);
+      const float c2 = mx == -INFINITY ? 0.f : __expf(m_o - mx);
+      l = l * c1 + l_o * c2;
+#pragma unroll
+      for (int p = 0; p < PER; ++p)
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) {
+          const float a_o = __shfl_xor_sync(0xffffffffu, acc[p][j], o);
+          acc[p][j] = acc[p][j] * c1 + a_o * c2;
+        }
+      m = mx;
+    }
+    // ... then the CW warps through shared memory
+    if (lane == 0) {
+      s_m[warp] = m;
+      s_l[warp] = l;
+    }
+    if (kw == 0) {
+#pragma unroll
+      for (int p = 0; p < PER; ++p) {
+        const int vi = g + p * G;
+        if (vi < NV) {
+#pragma unroll
+          for (int j = 0; j < VEC; ++j) s_acc[warp][vi * VEC + j] = acc[p][j];
+        }
+      }
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(CW * 32) : "memory");
+    float Mx = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < NP; ++i) Mx = fmaxf(Mx, s_m[i]);
+    float L = 0.f;
+#pragma unroll
+    for (int i = 0; i < NP; ++i) L += s_m[i] == -INFINITY ? 0.f : s_l[i] * __expf(s_m[i] - Mx);
+    for (int e = threadIdx.x; e < HD; e += CW * 32) {
+      float o = 0.f;
+#pragma unroll
+      for (int i = 0; i < NP; ++i) o += s_m[i] == -INFINITY ? 0.f : s_acc[i][e] * __expf(s_m[i] - Mx);
+      if (nsplit == 1) {
+        out[static_cast<size_t>(r) * D + h * HD + e] = from_f<T>(o / L);
+      } else {
+        const size_t w = (static_cast<size_t>(r) * Hl + h) * max_splits + sp;
+        ws_o[w * HD + e] = o;
+        if (e == 0) {
+          ws_ml[2 * w] = Mx;
+          ws_ml[2 * w + 1] = L;
+        }
+      }
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(CW * 32) : "memory");   // merge buffers reused
   }
 }
 
@@ -218,10 +332,20 @@ template <typename T, int HD>
 static int attn_launch(const void* q, const fl_row* rows, const int32_t* row_ctx, int M, int Hl,
                        const void* kv_layer, int S, int kps, void* out, float* ws_o, float* ws_ml,
                        cudaStream_t s) {
+  using Cfg = AttnCfg<T, HD>;
+  static int num_sms = 0;
+  if (!num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(k_attn_tma<T, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+  }
   const int ms = attn_max_splits(S);           // workspace stride (CHUNK-sized splits)
   const int splits = (S + kps - 1) / kps;
-  launch_k(k_attn_split<T, HD>, dim3(splits, Hl, M), dim3(ATT_THREADS), 0, s, 1, (const T*)q, rows,
-           row_ctx, Hl, (const T*)kv_layer, S, (T*)out, ws_o, ws_ml, ms, kps);
+  const int items = M * Hl * splits;
+  const int grid = items < 2 * num_sms ? items : 2 * num_sms;
+  launch_k(k_attn_tma<T, HD>, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM, s, 1, (const T*)q, rows,
+           row_ctx, M, Hl, (const T*)kv_layer, S, (T*)out, ws_o, ws_ml, ms, kps, splits);
   if (splits > 1) {
     launch_k(k_attn_combine<T, HD>, dim3(Hl, M), dim3(HD < 128 ? HD : 128), 0, s, 1, row_ctx, Hl,
              ws_o, ws_ml, ms, kps, (T*)out);

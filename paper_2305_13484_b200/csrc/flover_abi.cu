@@ -670,3 +670,25 @@ extern "C" int fl_gemm(const void* x, int ldx, const void* w, const void* bias, 
   FL_CUDA(cudaGetLastError());
   return FL_OK;
 }
+
+extern "C" size_t fl_attention_workspace_bytes(int M, int Hl, int hd, int S) {
+  const size_t ms = fl::attn_max_splits(S);
+  return align256((size_t)M * Hl * ms * hd * 4) + align256((size_t)M * Hl * ms * 2 * 4);
+}
+
+extern "C" int fl_attention(const void* q, const fl_row* rows, const int32_t* row_ctx, int M, int Hl,
+                            int hd, const void* kv_layer, int C, int S, void* out, void* workspace,
+                            int dtype, void* stream) {
+  if (!q || !rows || !row_ctx || !kv_layer || !out || !workspace || M < 1 || Hl < 1)
+    return fail(FL_EINVAL, "bad attention arguments");
+  if (hd != 64 && hd != 96 && hd != 128 && hd != 256) return fail(FL_EINVAL, "head_dim %d", hd);
+  const size_t ms = fl::attn_max_splits(S);
+  float* ws_o = static_cast<float*>(workspace);
+  float* ws_ml = reinterpret_cast<float*>(static_cast<char*>(workspace) +
+                                          align256((size_t)M * Hl * ms * hd * 4));
+  fl::launch_attention(q, rows, row_ctx, M, Hl, hd, kv_layer, C, S,
+                       fl::attn_keys_per_split(M * Hl, S), out, ws_o, ws_ml, dtype,
+                       static_cast<cudaStream_t>(stream));
+  FL_CUDA(cudaGetLastError());
+  return FL_OK;
+}

@@ -184,7 +184,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tma_w, const __grid_constant__ CUtensorMap tma_x,
               const bf16* __restrict__ bias, void* __restrict__ out, int M, int N, int ldo, int epi,
               int kch_total, int kch_per_split, unsigned long long* __restrict__ keys,
-              int index_base) {
+              int index_base, int bn) {
+  // BN is the tile capacity (smem / TMEM sizing); bn <= BN (multiple of 16) is
+  // this launch's token-tile width, chosen to balance M over the m-tiles
   constexpr int B_BYTES = BN * TC_BK * 2;
   constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   constexpr int NCOLS = TmemCols<BN>::v;
@@ -199,7 +201,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tile = blockIdx.x, m_tile = blockIdx.y, split = blockIdx.z, S = gridDim.z;
-  const int n0 = n_tile * TC_BM, m0 = m_tile * BN;
+  const int n0 = n_tile * TC_BM, m0 = m_tile * bn;
+  const uint32_t tx_bytes = A_BYTES + bn * TC_BK * 2;
   const int kc0 = split * kch_per_split;
   const int nch = max(0, min(kch_per_split, kch_total - kc0));
 
@@ -232,7 +235,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int pre = min(nch, STAGES);
       for (int c = 0; c < pre; ++c) {
         uint8_t* a = smem + c * STAGE_BYTES;
-        mbar_expect_tx(&full_bar[c], STAGE_BYTES);
+        mbar_expect_tx(&full_bar[c], tx_bytes);
         tma_load_2d(&tma_w, &full_bar[c], a, (kc0 + c) * TC_BK, n0);
       }
       pdl_wait();                                   // activations are the predecessor's output
@@ -243,7 +246,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const uint32_t ph = (c / STAGES) & 1;
         mbar_wait(&empty_bar[s], ph ^ 1);
         uint8_t* a = smem + s * STAGE_BYTES;
-        mbar_expect_tx(&full_bar[s], STAGE_BYTES);
+        mbar_expect_tx(&full_bar[s], tx_bytes);
         const int k = (kc0 + c) * TC_BK;
         tma_load_2d(&tma_w, &full_bar[s], a, k, n0);
         tma_load_2d(&tma_x, &full_bar[s], a + A_BYTES, k, m0);
@@ -251,7 +254,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc = instr_desc_bf16(TC_BM, BN);
+      const uint32_t idesc = instr_desc_bf16(TC_BM, bn);
       for (int c = 0; c < nch; ++c) {
         const int s = c % STAGES;
         const uint32_t ph = (c / STAGES) & 1;
@@ -277,14 +280,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_wait(&done_bar, 0);
       tc_fence_after();
       const uint32_t taddr = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-      for (int c0 = 0; c0 < BN; c0 += 16) {
+      for (int c0 = 0; c0 < bn; c0 += 16) {
         float v[16];
         tmem_ld16(taddr + c0, v);
 #pragma unroll
         for (int j = 0; j < 16; ++j) red[(c0 + j) * RED_LD + row] = v[j];
       }
     } else {
-      for (int c0 = 0; c0 < BN; ++c0) red[c0 * RED_LD + row] = 0.f;
+      for (int c0 = 0; c0 < bn; ++c0) red[c0 * RED_LD + row] = 0.f;
     }
   }
   // all 192 threads of every CTA in the cluster (S == 1: plain CTA barrier)
@@ -298,7 +301,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int rk = S > 1 ? static_cast<int>(cluster_rank()) : 0;
     const int R = TC_BM / S;
     const int q4 = R / 4;                          // float4 groups of rows (power of two)
-    const int mcount = min(BN, M - m0);
+    const int mcount = min(bn, M - m0);
     const uint32_t red_base = smem_u32(smem);
     const int total = q4 * mcount;
     for (int base = 0; base < total; base += 128) {
@@ -401,7 +404,7 @@ bool make_map(MapCache& cache, const void* ptr, uint64_t rows, uint64_t cols, ui
 
 template <int BN, int STAGES>
 int launch_bn(const GemmArgs& a, const CUtensorMap* mw, const CUtensorMap* mx, int splits, int kpc,
-              cudaStream_t s) {
+              int bn, cudaStream_t s) {
   constexpr int smem = STAGES * (A_BYTES + BN * TC_BK * 2) + 1024;
   static bool configured = false;
   if (!configured) {
@@ -409,10 +412,10 @@ int launch_bn(const GemmArgs& a, const CUtensorMap* mw, const CUtensorMap* mx, i
     cudaFuncSetAttribute(k_gemm_tc<BN, STAGES>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     configured = true;
   }
-  dim3 grid((a.N + TC_BM - 1) / TC_BM, (a.M + BN - 1) / BN, splits);
+  dim3 grid((a.N + TC_BM - 1) / TC_BM, (a.M + bn - 1) / bn, splits);
   cudaError_t e = launch_k(k_gemm_tc<BN, STAGES>, grid, dim3(TC_THREADS), smem, s, splits, *mw, *mx,
                            static_cast<const bf16*>(a.bias), a.out, a.M, a.N, a.ldo, a.epi,
-                           a.K / TC_BK, kpc, a.keys, a.index_base);
+                           a.K / TC_BK, kpc, a.keys, a.index_base, bn);
   if (e != cudaSuccess) {
     g_tc_err = std::string("k_gemm_tc launch: ") + cudaGetErrorString(e);
     return -1;
@@ -458,7 +461,10 @@ int gemm_tc(TcWorkspace* ws, const GemmArgs& a, cudaStream_t s) {
     return -1;
   }
   MapCache& cache = *static_cast<MapCache*>(ws->maps);
-  const int bn = a.M <= 16 ? 16 : a.M <= 32 ? 32 : a.M <= 64 ? 64 : a.M <= 128 ? 128 : 256;
+  // balanced token tiles: ceil(M/256) m-tiles of equal width (multiple of 16)
+  const int mt = (a.M + 255) / 256;
+  const int bn = (((a.M + mt - 1) / mt) + 15) / 16 * 16;
+  const int cap = bn <= 16 ? 16 : bn <= 32 ? 32 : bn <= 64 ? 64 : bn <= 128 ? 128 : 256;
   CUtensorMap *mw, *mx;
   if (!make_map(cache, a.w, a.N, a.K, a.K, TC_BM, &mw)) return -1;
   if (!make_map(cache, a.x, a.mcap > a.M ? a.mcap : a.M, a.K, a.ldx, bn, &mx)) return -1;
@@ -470,12 +476,12 @@ int gemm_tc(TcWorkspace* ws, const GemmArgs& a, cudaStream_t s) {
   while (S < 4 && tiles * S * 2 <= ws->num_sms && kch / (S * 2) >= 1) S *= 2;
   if (force_s > 0) S = force_s;
   const int kpc = (kch + S - 1) / S;
-  switch (bn) {
-    case 16: return launch_bn<16, 12>(a, mw, mx, S, kpc, s);
-    case 32: return launch_bn<32, 10>(a, mw, mx, S, kpc, s);
-    case 64: return launch_bn<64, 8>(a, mw, mx, S, kpc, s);
-    case 128: return launch_bn<128, 6>(a, mw, mx, S, kpc, s);
-    default: return launch_bn<256, 4>(a, mw, mx, S, kpc, s);
+  switch (cap) {
+    case 16: return launch_bn<16, 12>(a, mw, mx, S, kpc, bn, s);
+    case 32: return launch_bn<32, 10>(a, mw, mx, S, kpc, bn, s);
+    case 64: return launch_bn<64, 8>(a, mw, mx, S, kpc, bn, s);
+    case 128: return launch_bn<128, 6>(a, mw, mx, S, kpc, bn, s);
+    default: return launch_bn<256, 4>(a, mw, mx, S, kpc, bn, s);
   }
 }
 
