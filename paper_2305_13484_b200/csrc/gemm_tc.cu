@@ -70,6 +70,17 @@ FL_DEV void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0
       : "memory");
 }
 
+// Multicast variant: the box lands at the same smem offset in every CTA of
+// cta_mask and completes tx bytes on each receiver's mbarrier at that offset.
+FL_DEV void tma_load_2d_mc(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1,
+                           uint16_t cta_mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(cta_mask)
+      : "memory");
+}
+
 FL_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 FL_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -105,6 +116,14 @@ FL_DEV void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
                : "memory");
+}
+
+// commit to the same mbarrier in every CTA of cta_mask
+FL_DEV void mma_commit_mc(uint64_t* bar, uint16_t cta_mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], "
+      "%1;" ::"r"(smem_u32(bar)), "h"(cta_mask)
+      : "memory");
 }
 
 FL_DEV void tmem_ld16(uint32_t taddr, float* v) {
@@ -176,22 +195,36 @@ FL_DEV void store4(void* out, size_t o, int nvalid, const float* v, int epi) {
   }
 }
 
-// grid (N/128, ceil(M/BN), S) with cluster (1,1,S): the S CTAs of a cluster
-// split K for the same output tile and reduce their fp32 partials through
-// distributed shared memory (no global round trip, no atomics).
-template <int BN, int STAGES>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+// grid (N/128, ceil(M/(MT*bn)), S) with cluster (1,1,S).
+//
+// One CTA owns a 128-row weight tile and MT token sub-tiles of bn columns each
+// (MT*bn <= 512 TMEM columns), so every weight byte is read once per GEMM
+// however many rows the fused window holds.  The S CTAs of a cluster split K
+// for the same output tile and reduce their fp32 partials through distributed
+// shared memory (no global round trip, no atomics).  The epilogue walks the
+// accumulator in 64-column chunks: TMEM -> own smem [64][132] -> (cluster
+// barrier) -> each CTA reduces its 128/S weight rows over the S partials ->
+// bias / GELU / residual / argmax -> coalesced global stores.
+template <int BN, int MT, int WT, int STAGES>
+__global__ void __launch_bounds__(TC_THREADS, 2)
     k_gemm_tc(const __grid_constant__ CUtensorMap tma_w, const __grid_constant__ CUtensorMap tma_x,
               const bf16* __restrict__ bias, void* __restrict__ out, int M, int N, int ldo, int epi,
               int kch_total, int kch_per_split, unsigned long long* __restrict__ keys,
-              int index_base, int bn) {
-  // BN is the tile capacity (smem / TMEM sizing); bn <= BN (multiple of 16) is
-  // this launch's token-tile width, chosen to balance M over the m-tiles
-  constexpr int B_BYTES = BN * TC_BK * 2;
-  constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  constexpr int NCOLS = TmemCols<BN>::v;
-  constexpr int RED_LD = TC_BM + 4;          // partial tile [BN][132] fp32 (n fastest)
-  static_assert(BN * RED_LD * 4 <= STAGES * STAGE_BYTES, "partial tile must fit the stage ring");
+              int index_base, int bn, int CM) {
+  // CM: CTAs along N in one cluster that share (multicast) the token tiles;
+  // the cluster is (CM, 1, S) and rank = xi + CM * zi.
+  // BN: sub-tile capacity (smem / TMEM sizing); bn <= BN (multiple of 16): this
+  // launch's sub-tile width, balanced so MT*bn covers the window's rows
+  // WT weight tiles of 128 rows share each token sub-tile (accumulator
+  // (w, j) lives at TMEM column (w * MT + j) * bn)
+  constexpr int XB = BN * TC_BK * 2;
+  constexpr int AB = WT * A_BYTES;
+  constexpr int STAGE_BYTES = AB + MT * XB;
+  constexpr int NCOLS = TmemCols<BN * MT * WT>::v;
+  constexpr int RED_LD = TC_BM + 4;          // partial chunk [CH][132] fp32 (n fastest)
+  constexpr int CH = 64;                     // epilogue chunk (token columns)
+  static_assert(CH * RED_LD * 4 <= STAGES * STAGE_BYTES, "epilogue chunk must fit the stage ring");
+  static_assert(BN * MT * WT <= 512, "TMEM holds 512 fp32 columns");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[STAGES];
   __shared__ __align__(8) uint64_t empty_bar[STAGES];
@@ -200,11 +233,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_tile = blockIdx.x, m_tile = blockIdx.y, split = blockIdx.z, S = gridDim.z;
-  const int n0 = n_tile * TC_BM, m0 = m_tile * bn;
-  const uint32_t tx_bytes = A_BYTES + bn * TC_BK * 2;
+  const int n_tile = blockIdx.x, split = blockIdx.z, S = gridDim.z;
+  const int n0 = n_tile * TC_BM * WT, m0 = blockIdx.y * MT * bn;
   const int kc0 = split * kch_per_split;
   const int nch = max(0, min(kch_per_split, kch_total - kc0));
+  const uint32_t tx_bytes = AB + MT * bn * TC_BK * 2;
+  const int mcount = min(MT * bn, M - m0);   // valid token columns of this tile
+  const int csize = CM * S;
+  const uint32_t crank = csize > 1 ? cluster_rank() : 0;
+  const int xi = static_cast<int>(crank) % CM;          // position in the multicast group
+  const int zi = static_cast<int>(crank) / CM;          // K split index
+  const uint16_t group_mask = static_cast<uint16_t>(((1u << CM) - 1u) << (CM * zi));
+  const int piece = bn / CM;                            // token rows this CTA fetches per sub-tile
 
   // ---- prologue (overlaps the predecessor kernel under PDL)
   if (threadIdx.x == 0) {
@@ -212,7 +252,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_x)) : "memory");
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
+      mbar_init(&empty_bar[s], CM);      // released by every consumer of the group
     }
     mbar_init(&done_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -224,7 +264,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
-  __syncthreads();
+  if (csize > 1) cluster_sync_all();   // peers' barriers exist before any multicast
+  else __syncthreads();
   tc_fence_after();
   pdl_trigger();
   const uint32_t tmem = tmem_base;
@@ -236,11 +277,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int c = 0; c < pre; ++c) {
         uint8_t* a = smem + c * STAGE_BYTES;
         mbar_expect_tx(&full_bar[c], tx_bytes);
-        tma_load_2d(&tma_w, &full_bar[c], a, (kc0 + c) * TC_BK, n0);
+#pragma unroll
+        for (int w = 0; w < WT; ++w)
+          tma_load_2d(&tma_w, &full_bar[c], a + w * A_BYTES, (kc0 + c) * TC_BK, n0 + w * TC_BM);
       }
       pdl_wait();                                   // activations are the predecessor's output
       for (int c = 0; c < pre; ++c)
-        tma_load_2d(&tma_x, &full_bar[c], smem + c * STAGE_BYTES + A_BYTES, (kc0 + c) * TC_BK, m0);
+#pragma unroll
+        for (int j = 0; j < MT; ++j) {
+          uint8_t* dst = smem + c * STAGE_BYTES + AB + j * XB + xi * piece * 128;
+          if (CM > 1)
+            tma_load_2d_mc(&tma_x, &full_bar[c], dst, (kc0 + c) * TC_BK, m0 + j * bn + xi * piece,
+                           group_mask);
+          else
+            tma_load_2d(&tma_x, &full_bar[c], dst, (kc0 + c) * TC_BK, m0 + j * bn);
+        }
       for (int c = pre; c < nch; ++c) {
         const int s = c % STAGES;
         const uint32_t ph = (c / STAGES) & 1;
@@ -248,8 +299,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         uint8_t* a = smem + s * STAGE_BYTES;
         mbar_expect_tx(&full_bar[s], tx_bytes);
         const int k = (kc0 + c) * TC_BK;
-        tma_load_2d(&tma_w, &full_bar[s], a, k, n0);
-        tma_load_2d(&tma_x, &full_bar[s], a + A_BYTES, k, m0);
+#pragma unroll
+        for (int w = 0; w < WT; ++w) tma_load_2d(&tma_w, &full_bar[s], a + w * A_BYTES, k, n0 + w * TC_BM);
+#pragma unroll
+        for (int j = 0; j < MT; ++j) {
+          uint8_t* dst = a + AB + j * XB + xi * piece * 128;
+          if (CM > 1)
+            tma_load_2d_mc(&tma_x, &full_bar[s], dst, k, m0 + j * bn + xi * piece, group_mask);
+          else
+            tma_load_2d(&tma_x, &full_bar[s], dst, k, m0 + j * bn);
+        }
       }
     }
   } else if (warp == 1) {
@@ -261,99 +320,117 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         mbar_wait(&full_bar[s], ph);
         tc_fence_after();
         const uint8_t* a = smem + s * STAGE_BYTES;
-        const uint64_t ad = smem_desc_sw128(a);
-        const uint64_t bd = smem_desc_sw128(a + A_BYTES);
 #pragma unroll
-        for (int k = 0; k < TC_BK / 16; ++k)   // 16 bf16 = 32 bytes = 2 descriptor units
-          mma_bf16(tmem, ad + 2 * k, bd + 2 * k, idesc, (c | k) != 0);
-        mma_commit(&empty_bar[s]);
+        for (int w = 0; w < WT; ++w) {
+          const uint64_t ad = smem_desc_sw128(a + w * A_BYTES);
+#pragma unroll
+          for (int j = 0; j < MT; ++j) {
+            const uint64_t bd = smem_desc_sw128(a + AB + j * XB);
+#pragma unroll
+            for (int k = 0; k < TC_BK / 16; ++k)   // 16 bf16 = 32 bytes = 2 descriptor units
+              mma_bf16(tmem + (w * MT + j) * bn, ad + 2 * k, bd + 2 * k, idesc, (c | k) != 0);
+          }
+        }
+        if (CM > 1) mma_commit_mc(&empty_bar[s], group_mask);
+        else mma_commit(&empty_bar[s]);
       }
       mma_commit(&done_bar);
     }
   } else {
-    // ---- epilogue part 1 (warps 2..5): TMEM -> own smem partial [BN][RED_LD]
     pdl_wait();     // EPI_ACC_F32 reads `out`, written by predecessors
-    const int quarter = warp & 3;
-    const int row = quarter * 32 + lane;
-    float* red = reinterpret_cast<float*>(smem);
     if (nch > 0) {
       mbar_wait(&done_bar, 0);
       tc_fence_after();
-      const uint32_t taddr = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-      for (int c0 = 0; c0 < bn; c0 += 16) {
-        float v[16];
-        tmem_ld16(taddr + c0, v);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) red[(c0 + j) * RED_LD + row] = v[j];
-      }
-    } else {
-      for (int c0 = 0; c0 < bn; ++c0) red[c0 * RED_LD + row] = 0.f;
     }
   }
-  // all 192 threads of every CTA in the cluster (S == 1: plain CTA barrier)
   __syncwarp();
-  tc_fence_before();
-  if (S > 1) cluster_sync_all();
-  else __syncthreads();
 
-  if (warp >= 2) {
-    // ---- epilogue part 2: this CTA reduces rows [rk*R, rk*R+R) over the S partials
-    const int rk = S > 1 ? static_cast<int>(cluster_rank()) : 0;
-    const int R = TC_BM / S;
-    const int q4 = R / 4;                          // float4 groups of rows (power of two)
-    const int mcount = min(bn, M - m0);
-    const uint32_t red_base = smem_u32(smem);
-    const int total = q4 * mcount;
-    for (int base = 0; base < total; base += 128) {
-      const int e = base + threadIdx.x - 64;
-      const bool valid = e < total;
-      const int m = valid ? e / q4 : 0;
-      const int r0 = rk * R + (e % q4) * 4;
-      const uint32_t off = static_cast<uint32_t>((m * RED_LD + r0) * 4);
-      float acc[4] = {0.f, 0.f, 0.f, 0.f};
-      if (valid) {
-        float4 t[8];
+  // ---- epilogue, one 64-column chunk at a time (all 192 threads keep the
+  // cluster barriers in lock step; warps 2..5 move the data)
+  const int rk = zi;
+  const int R = TC_BM / S;
+  const int q4 = R / 4;                          // float4 groups of rows (power of two)
+  float* red = reinterpret_cast<float*>(smem);
+  const uint32_t red_base = smem_u32(smem);
+  const int quarter = warp & 3;
+  const int row = quarter * 32 + lane;
+  const int nchunk = (mcount + CH - 1) / CH;
+  for (int it = 0; it < WT * nchunk; ++it) {
+    const int w = it / nchunk;                   // weight tile
+    const int cb = (it % nchunk) * CH;           // first token column of the chunk
+    const int ncol = min(CH, mcount - cb);
+    const int nw0 = n0 + w * TC_BM;
+    if (warp >= 2) {
+      if (nch > 0) {
+        const uint32_t taddr = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + w * MT * bn + cb;
+        for (int c0 = 0; c0 < ncol; c0 += 16) {
+          float v[16];
+          tmem_ld16(taddr + c0, v);
 #pragma unroll
-        for (int p = 0; p < 8; ++p)      // all peer loads in flight at once
-          if (p < S)
-            t[p] = S > 1 ? ld_dsmem_f4(red_base + off, p)
-                         : *reinterpret_cast<const float4*>(smem + off);
-#pragma unroll
-        for (int p = 0; p < 8; ++p)
-          if (p < S) {
-            acc[0] += t[p].x; acc[1] += t[p].y; acc[2] += t[p].z; acc[3] += t[p].w;
-          }
-      }
-      const int n = n0 + r0;
-      const int nvalid = valid ? max(0, min(4, N - n)) : 0;
-      if (bias) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[j] += j < nvalid ? __bfloat162float(bias[n + j]) : 0.f;
-      }
-      if (epi == EPI_ARGMAX) {
-        // greedy token: max logit, lowest index; reduce over the q4 lanes of this
-        // token, then one 64-bit atomicMax per (token, CTA)
-        unsigned long long key = 0ull;
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (j < nvalid) {
-            const unsigned long long k2 = argmax_key(acc[j], index_base + n + j);
-            key = k2 > key ? k2 : key;
-          }
-        for (int o = 1; o < q4 && o < 32; o <<= 1) {
-          const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
-          key = other > key ? other : key;
+          for (int j = 0; j < 16; ++j) red[(c0 + j) * RED_LD + row] = v[j];
         }
-        if (valid && (e % q4) == 0 && key) atomicMax(&keys[m0 + m], key);
-      } else if (nvalid > 0) {
-        store4(out, static_cast<size_t>(m0 + m) * ldo + n, nvalid, acc, epi);
+      } else {
+        for (int c0 = 0; c0 < ncol; ++c0) red[c0 * RED_LD + row] = 0.f;
       }
     }
+    tc_fence_before();
+    if (csize > 1) cluster_sync_all();
+    else __syncthreads();
+    if (warp >= 2) {
+      const int total = q4 * ncol;
+      for (int base = 0; base < total; base += 128) {
+        const int e = base + threadIdx.x - 64;
+        const bool valid = e < total;
+        const int m = valid ? e / q4 : 0;
+        const int r0 = rk * R + (e % q4) * 4;
+        const uint32_t off = static_cast<uint32_t>((m * RED_LD + r0) * 4);
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        if (valid) {
+          float4 t[8];
+#pragma unroll
+          for (int p = 0; p < 8; ++p)      // all peer loads in flight at once
+            if (p < S)
+              t[p] = S > 1 ? ld_dsmem_f4(red_base + off, static_cast<uint32_t>(xi + CM * p))
+                           : *reinterpret_cast<const float4*>(smem + off);
+#pragma unroll
+          for (int p = 0; p < 8; ++p)
+            if (p < S) {
+              acc[0] += t[p].x; acc[1] += t[p].y; acc[2] += t[p].z; acc[3] += t[p].w;
+            }
+        }
+        const int n = nw0 + r0;
+        const int nvalid = valid ? max(0, min(4, N - n)) : 0;
+        if (bias) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[j] += j < nvalid ? __bfloat162float(bias[n + j]) : 0.f;
+        }
+        const int mg = m0 + cb + m;
+        if (epi == EPI_ARGMAX) {
+          // greedy token: max logit, lowest index; reduce over the q4 lanes of
+          // this token, then one 64-bit atomicMax per (token, CTA)
+          unsigned long long key = 0ull;
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (j < nvalid) {
+              const unsigned long long k2 = argmax_key(acc[j], index_base + n + j);
+              key = k2 > key ? k2 : key;
+            }
+          for (int o = 1; o < q4 && o < 32; o <<= 1) {
+            const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
+            key = other > key ? other : key;
+          }
+          if (valid && (e % q4) == 0 && key) atomicMax(&keys[mg], key);
+        } else if (nvalid > 0) {
+          store4(out, static_cast<size_t>(mg) * ldo + n, nvalid, acc, epi);
+        }
+      }
+    }
+    // the chunk buffer is rewritten next round; peers may still read it
+    __syncwarp();
+    if (csize > 1) cluster_sync_all();
+    else __syncthreads();
   }
-  // peers may still be reading this CTA's partial
-  __syncwarp();
-  if (S > 1) cluster_sync_all();
-  else __syncthreads();
+  if (csize > 1 && mcount <= 0) cluster_sync_all();
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(NCOLS));
@@ -402,20 +479,21 @@ bool make_map(MapCache& cache, const void* ptr, uint64_t rows, uint64_t cols, ui
   return true;
 }
 
-template <int BN, int STAGES>
+template <int BN, int MT, int WT, int STAGES>
 int launch_bn(const GemmArgs& a, const CUtensorMap* mw, const CUtensorMap* mx, int splits, int kpc,
-              int bn, cudaStream_t s) {
-  constexpr int smem = STAGES * (A_BYTES + BN * TC_BK * 2) + 1024;
+              int bn, int cm, cudaStream_t s) {
+  constexpr int smem = STAGES * (WT * A_BYTES + MT * BN * TC_BK * 2) + 1024;
+  static_assert(smem <= 232448, "dynamic shared memory budget");
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(k_gemm_tc<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(k_gemm_tc<BN, STAGES>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(k_gemm_tc<BN, MT, WT, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_gemm_tc<BN, MT, WT, STAGES>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     configured = true;
   }
-  dim3 grid((a.N + TC_BM - 1) / TC_BM, (a.M + bn - 1) / bn, splits);
-  cudaError_t e = launch_k(k_gemm_tc<BN, STAGES>, grid, dim3(TC_THREADS), smem, s, splits, *mw, *mx,
-                           static_cast<const bf16*>(a.bias), a.out, a.M, a.N, a.ldo, a.epi,
-                           a.K / TC_BK, kpc, a.keys, a.index_base, bn);
+  dim3 grid((a.N + WT * TC_BM - 1) / (WT * TC_BM), (a.M + MT * bn - 1) / (MT * bn), splits);
+  cudaError_t e = launch_k(k_gemm_tc<BN, MT, WT, STAGES>, grid, dim3(TC_THREADS), smem, s,
+                           dim3(cm, 1, splits), *mw, *mx, static_cast<const bf16*>(a.bias), a.out,
+                           a.M, a.N, a.ldo, a.epi, a.K / TC_BK, kpc, a.keys, a.index_base, bn, cm);
   if (e != cudaSuccess) {
     g_tc_err = std::string("k_gemm_tc launch: ") + cudaGetErrorString(e);
     return -1;
@@ -461,27 +539,38 @@ int gemm_tc(TcWorkspace* ws, const GemmArgs& a, cudaStream_t s) {
     return -1;
   }
   MapCache& cache = *static_cast<MapCache*>(ws->maps);
-  // balanced token tiles: ceil(M/256) m-tiles of equal width (multiple of 16)
-  const int mt = (a.M + 255) / 256;
-  const int bn = (((a.M + mt - 1) / mt) + 15) / 16 * 16;
+  // token tiling: balanced sub-tiles of <= 256 columns, one per CTA along M.
+  // Wide token tiles (> 64 columns) pair two 128-row weight tiles per CTA
+  // (WT=2, 2*bn TMEM columns) so each token byte loaded feeds twice the MMA
+  // work; those configurations run 2 CTAs per SM (<= 113 KB smem each).
+  const int ntiles_m = (a.M + 255) / 256;
+  const int bn = (((a.M + ntiles_m - 1) / ntiles_m) + 15) / 16 * 16;
   const int cap = bn <= 16 ? 16 : bn <= 32 ? 32 : bn <= 64 ? 64 : bn <= 128 ? 128 : 256;
-  CUtensorMap *mw, *mx;
-  if (!make_map(cache, a.w, a.N, a.K, a.K, TC_BM, &mw)) return -1;
-  if (!make_map(cache, a.x, a.mcap > a.M ? a.mcap : a.M, a.K, a.ldx, bn, &mx)) return -1;
-  const int tiles = ((a.N + TC_BM - 1) / TC_BM) * ((a.M + bn - 1) / bn);
+  static const int force_wt = getenv("FL_TC_WT") ? atoi(getenv("FL_TC_WT")) : 0;
+  const int wt = force_wt ? force_wt : (cap >= 128 ? 2 : 1);
+  const int ntn = (a.N + wt * TC_BM - 1) / (wt * TC_BM);
+  const int tiles = ntn * ntiles_m;
   const int kch = a.K / TC_BK;
-  // split K across a cluster of S CTAs until the tiles cover the SMs
+  const int per_sm = (cap == 128 || (cap == 256 && wt == 1)) ? 2 : 1;
   static const int force_s = getenv("FL_TC_SPLIT") ? atoi(getenv("FL_TC_SPLIT")) : 0;
   int S = 1;
-  while (S < 4 && tiles * S * 2 <= ws->num_sms && kch / (S * 2) >= 1) S *= 2;
+  while (S < 4 && tiles * S * 2 <= per_sm * ws->num_sms && kch / (S * 2) >= 1) S *= 2;
   if (force_s > 0) S = force_s;
   const int kpc = (kch + S - 1) / S;
+  const int cm = 1;
+  CUtensorMap *mw, *mx;
+  if (!make_map(cache, a.w, a.N, a.K, a.K, TC_BM, &mw)) return -1;
+  if (!make_map(cache, a.x, a.mcap > a.M ? a.mcap : a.M, a.K, a.ldx, bn / cm, &mx)) return -1;
+  if (wt == 2) {
+    if (cap == 128) return launch_bn<128, 1, 2, 2>(a, mw, mx, S, kpc, bn, cm, s);   // 96 KB
+    if (cap == 256) return launch_bn<256, 1, 2, 3>(a, mw, mx, S, kpc, bn, cm, s);   // 192 KB
+  }
   switch (cap) {
-    case 16: return launch_bn<16, 12>(a, mw, mx, S, kpc, bn, s);
-    case 32: return launch_bn<32, 10>(a, mw, mx, S, kpc, bn, s);
-    case 64: return launch_bn<64, 8>(a, mw, mx, S, kpc, bn, s);
-    case 128: return launch_bn<128, 6>(a, mw, mx, S, kpc, bn, s);
-    default: return launch_bn<256, 4>(a, mw, mx, S, kpc, bn, s);
+    case 16: return launch_bn<16, 1, 1, 12>(a, mw, mx, S, kpc, bn, cm, s);
+    case 32: return launch_bn<32, 1, 1, 10>(a, mw, mx, S, kpc, bn, cm, s);
+    case 64: return launch_bn<64, 1, 1, 8>(a, mw, mx, S, kpc, bn, cm, s);
+    case 128: return launch_bn<128, 1, 1, 3>(a, mw, mx, S, kpc, bn, cm, s);
+    default: return launch_bn<256, 1, 1, 2>(a, mw, mx, S, kpc, bn, cm, s);
   }
 }
 

@@ -36,7 +36,8 @@ def _gemm(x, w, bias, out, epi, use_tc, dtype):
 
 
 SHAPES = [(1, 768, 768), (7, 2304, 768), (16, 512, 1024), (55, 3072, 768), (64, 768, 3072),
-          (100, 50257, 768), (129, 1536, 4096), (256, 4096, 512), (300, 1000, 256), (17, 128, 64)]
+          (100, 50257, 768), (129, 1536, 4096), (256, 4096, 512), (300, 1000, 256), (17, 128, 64),
+          (350, 1536, 4096), (512, 768, 768), (700, 1024, 512), (1000, 384, 256)]
 
 
 @pytest.mark.parametrize("M,N,K", SHAPES)
