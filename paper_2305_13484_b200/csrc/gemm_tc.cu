@@ -547,7 +547,7 @@ int gemm_tc(TcWorkspace* ws, const GemmArgs& a, cudaStream_t s) {
   const int bn = (((a.M + ntiles_m - 1) / ntiles_m) + 15) / 16 * 16;
   const int cap = bn <= 16 ? 16 : bn <= 32 ? 32 : bn <= 64 ? 64 : bn <= 128 ? 128 : 256;
   static const int force_wt = getenv("FL_TC_WT") ? atoi(getenv("FL_TC_WT")) : 0;
-  const int wt = force_wt ? force_wt : (cap >= 128 ? 2 : 1);
+  const int wt = force_wt ? force_wt : 1;
   const int ntn = (a.N + wt * TC_BM - 1) / (wt * TC_BM);
   const int tiles = ntn * ntiles_m;
   const int kch = a.K / TC_BK;
