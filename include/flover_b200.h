@@ -181,6 +181,9 @@ int fl_profile_read(fl_handle* h, int cls, double* total_ms, int64_t* records, d
  * uses (use_tc: 1 tcgen05, 0 SIMT).  epi: 0 store(dtype) 1 gelu(dtype)
  * 2 accumulate(f32) 3 store(f32).  workspace: >= fl_gemm_workspace_bytes(). */
 size_t fl_gemm_workspace_bytes(void);
+/* Diagnostics: when non-NULL, every tensor-core GEMM CTA b writes 4 clocks to
+ * dev_counters[4b..4b+3]: producer wait, producer total, MMA wait, MMA total. */
+void fl_gemm_debug(unsigned long long* dev_counters);
 /* Diagnostic entry: K4 alone.  q [M, Hl*hd]; rows (device) give the slot of each
  * row, row_ctx (device) its context length; kv_layer is one layer of the pool
  * [C][2][Hl][S][hd]; out [M, Hl*hd].  workspace >= fl_attention_workspace_bytes. */

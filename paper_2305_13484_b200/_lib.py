@@ -21,7 +21,8 @@ W_LAYER_COUNT = 12
 EXPORTS = ("fl_abi_version", "fl_last_error", "fl_workspace_bytes", "fl_create", "fl_destroy",
            "fl_comm_unique_id", "fl_comm_init", "fl_step", "fl_shuffle", "fl_kernel_launches",
            "fl_gemm_workspace_bytes", "fl_gemm", "fl_profile", "fl_profile_read", "fl_configure",
-           "fl_last_duration_ms", "fl_attention_workspace_bytes", "fl_attention")
+           "fl_last_duration_ms", "fl_attention_workspace_bytes", "fl_attention",
+           "fl_gemm_debug")
 PROF_ATTENTION, PROF_GEMM, PROF_SHUFFLE, PROF_STEP = 0, 1, 2, 3
 
 
@@ -85,6 +86,8 @@ def load() -> C.CDLL:
     lib.fl_last_duration_ms.argtypes = [C.c_void_p, C.POINTER(C.c_float)]
     lib.fl_profile_read.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_double),
                                     C.POINTER(C.c_int64), C.POINTER(C.c_double)]
+    lib.fl_gemm_debug.argtypes = [C.c_void_p]
+    lib.fl_gemm_debug.restype = None
     lib.fl_attention_workspace_bytes.restype = C.c_size_t
     lib.fl_attention_workspace_bytes.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int]
     lib.fl_attention.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int,

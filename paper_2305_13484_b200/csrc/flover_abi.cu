@@ -649,6 +649,7 @@ void* g_dbg_base = nullptr;
 }
 
 extern "C" size_t fl_gemm_workspace_bytes(void) { return fl::tc_workspace_bytes(0, 0); }
+extern "C" void fl_gemm_debug(unsigned long long* dev_counters) { fl::tc_set_debug(dev_counters); }
 
 extern "C" int fl_gemm(const void* x, int ldx, const void* w, const void* bias, void* out, int ldo,
                        int M, int N, int K, int epi, int dtype, int use_tc, void* workspace,

@@ -22,6 +22,8 @@ size_t tc_workspace_bytes(int max_rows, int max_n);
 int tc_init(TcWorkspace* ws, void* base, size_t bytes);
 void tc_destroy(TcWorkspace* ws);
 const char* tc_last_error();
+// diagnostics: per-CTA [producer wait, producer total, mma wait, mma total] clocks
+void tc_set_debug(unsigned long long* p);
 
 // out[M,N] = X[M,K] . W[N,K]^T (+bias, epilogue), bf16 operands, fp32 accumulate in TMEM.
 // Returns 0, or -1 with tc_last_error() set (shape the kernel does not cover).

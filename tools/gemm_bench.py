@@ -16,6 +16,7 @@ shapes = [(48, 2304, 768), (48, 768, 768), (48, 3072, 768), (48, 768, 3072), (48
 if len(sys.argv) > 1:
     shapes = [tuple(map(int, a.split("x"))) for a in sys.argv[1:]]
 s = torch.cuda.Stream()
+dbg = torch.zeros(4 * 4096, dtype=torch.int64, device="cuda")
 for M, N, K in shapes:
     x = torch.randn(M, K, device="cuda").bfloat16()
     w = (torch.randn(N, K, device="cuda") * 0.02).bfloat16()
@@ -43,3 +44,9 @@ for M, N, K in shapes:
         gbs = (N * K * 2 + M * K * 2 + M * N * 2) / us / 1e3
         res.append(f"{name} {us:7.2f} us {gbs:7.0f} GB/s")
     print(f"M={M:4d} N={N:6d} K={K:6d}  " + "   ".join(res), flush=True)
+    if os.environ.get("GEMM_DBG"):
+        dbg.zero_(); lib.fl_gemm_debug(C.c_void_p(dbg.data_ptr())); ours(); torch.cuda.synchronize()
+        lib.fl_gemm_debug(None)
+        d = dbg.view(-1, 4).cpu().double(); d = d[d[:, 3] > 0]
+        print(f"   CTAs {len(d)}: producer waits {100*d[:,0].sum()/d[:,1].sum():.0f}% of {d[:,1].mean():.0f} clk, "
+              f"mma waits {100*d[:,2].sum()/d[:,3].sum():.0f}% of {d[:,3].mean():.0f} clk")
