@@ -282,6 +282,7 @@ def run_ours(args, cfg):
     ex.profile(True)
     l0 = ex.launches()
     rows0, it0, mv0 = ex.rows_total, ex.iterations, ex.moved_kv_bytes
+    sl0 = len(ex.shuffle_log)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     streams = []
     with ClockSampler(local) as clk:
@@ -345,6 +346,12 @@ def run_ours(args, cfg):
         kern["shuffle"] = {"bound": "hbm", "records": sh["records"], "ms": sh["ms"],
                            "bytes_per_launch": mv / sh["records"],
                            "achieved": mv / (sh["ms"] / 1e3) / 1e9, "peak": hbm, "unit": "GB/s"}
+    if "shuffle" in kern:
+        log = ex.shuffle_log[sl0:]
+        if log:
+            kern["shuffle"]["device_clock_check"] = {
+                "shuffles": len(log), "moves": sum(x[0] for x in log),
+                "gbs": sum(x[1] for x in log) / (sum(x[2] for x in log) / 1e3) / 1e9}
     for k in kern.values():
         k["frac"] = k["achieved"] / k["peak"]
         k["share_of_step"] = k["ms"] / max(prof["step"]["ms"] + sh["ms"], 1e-9)

@@ -172,6 +172,7 @@ class CudaExecutor:
         self.orphan_rows_total = 0
         self.shuffles = 0
         self.moved_kv_bytes = 0
+        self.shuffle_log = []             # (moves, algorithmic bytes, device ms) per shuffle
         self.seen = []
         self.h2d_bytes = 0
         self.d2h_bytes = 0
@@ -381,12 +382,14 @@ class CudaExecutor:
 
     def on_shuffle(self, plan) -> float | None:
         moves = []
+        nbytes = 0
         for m in plan.moves:
             info = self._live[m.request_id]
             ctx = info["P"] + info["gen"] - 1      # KV positions written so far
             moves.append((m.src_slot % self.C, m.dst_slot % self.C, ctx))
-            self.moved_kv_bytes += 2 * ctx * self.spec.kv_bytes_per_token(
+            nbytes += 2 * ctx * self.spec.kv_bytes_per_token(
                 2 if self.dtype == "bf16" else 4, self.tp_size)
+        self.moved_kv_bytes += nbytes
         flat = (C.c_int32 * (3 * len(moves)))(*[v for mv in moves for v in mv])
         self.h2d_bytes += 12 * len(moves)
         cs = self.stream
@@ -396,6 +399,7 @@ class CudaExecutor:
             self._orphans.pop(s, None)
         if self._lib_timing:
             ms = self._last_ms()
+            self.shuffle_log.append((len(moves), nbytes, ms))
             return self.clock_reduce(ms) if self.clock_reduce else ms
         return None
 
