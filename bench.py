@@ -297,6 +297,7 @@ def run_ours(args, cfg):
     launches = ex.launches() - l0
     prof = ex.profile_read()
     att_bytes = ex.attn_bytes_profiled     # K4 bytes of exactly the profiled steps
+    mv1, sl1 = ex.moved_kv_bytes, len(ex.shuffle_log)
     ex.profile(False)
     if world > 1:
         t = torch.tensor([ms], device="cuda")
@@ -342,12 +343,12 @@ def run_ours(args, cfg):
                         "achieved": g["bytes"] / (g["ms"] / 1e3) / 1e9, "peak": hbm, "unit": "GB/s"}
     sh = prof["shuffle"]
     if sh["records"]:
-        mv = ex.moved_kv_bytes - mv0
+        mv = mv1 - mv0
         kern["shuffle"] = {"bound": "hbm", "records": sh["records"], "ms": sh["ms"],
                            "bytes_per_launch": mv / sh["records"],
                            "achieved": mv / (sh["ms"] / 1e3) / 1e9, "peak": hbm, "unit": "GB/s"}
     if "shuffle" in kern:
-        log = ex.shuffle_log[sl0:]
+        log = ex.shuffle_log[sl0:sl1]
         if log:
             kern["shuffle"]["device_clock_check"] = {
                 "shuffles": len(log), "moves": sum(x[0] for x in log),
