@@ -172,9 +172,10 @@ int fl_configure(fl_handle* h, int use_graphs, int profile_every, int time_steps
 int fl_last_duration_ms(fl_handle* h, float* ms);
 int fl_profile(fl_handle* h, int enable);
 /* Drains pending records (synchronises on them) and returns the totals since the
- * last fl_profile(h, 1): summed milliseconds, launch records and algorithmic
- * bytes (GEMM: weights + activations in + out; other classes report 0). */
-int fl_profile_read(fl_handle* h, int cls, double* total_ms, int64_t* records, double* bytes);
+ * last fl_profile(h, 1): summed milliseconds, launch records, algorithmic bytes
+ * and flops (GEMM: weights + activations in + out, 2*M*N*K; other classes 0). */
+int fl_profile_read(fl_handle* h, int cls, double* total_ms, int64_t* records, double* bytes,
+                    double* flops);
 
 /* Diagnostic entry for kernel-level parity tests: one projection GEMM
  * out[M,N] (=|+=) X[M,K] . W[N,K]^T + bias through the same kernels fl_step

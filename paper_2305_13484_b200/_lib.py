@@ -85,7 +85,8 @@ def load() -> C.CDLL:
     lib.fl_configure.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int]
     lib.fl_last_duration_ms.argtypes = [C.c_void_p, C.POINTER(C.c_float)]
     lib.fl_profile_read.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_double),
-                                    C.POINTER(C.c_int64), C.POINTER(C.c_double)]
+                                    C.POINTER(C.c_int64), C.POINTER(C.c_double),
+                                    C.POINTER(C.c_double)]
     lib.fl_gemm_debug.argtypes = [C.c_void_p]
     lib.fl_gemm_debug.restype = None
     lib.fl_attention_workspace_bytes.restype = C.c_size_t

@@ -98,12 +98,13 @@ struct fl_handle {
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;
   // live profiling
-  struct Rec { int cls; cudaEvent_t a, b; double bytes; };
+  struct Rec { int cls; cudaEvent_t a, b; double bytes, flops; };
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
   std::vector<Rec> pending;
   double tot_ms[FL_PROF_CLASSES] = {};
   double tot_bytes[FL_PROF_CLASSES] = {};
+  double tot_flops[FL_PROF_CLASSES] = {};
   int64_t tot_n[FL_PROF_CLASSES] = {};
   // CUDA graphs of the step, keyed by (n_rows, n_dec, logits, profiled)
   struct GraphEntry {
@@ -145,7 +146,7 @@ struct ProfScope {
   int cls;
   cudaStream_t s;
   cudaEvent_t a = nullptr;
-  double bytes = 0;
+  double bytes = 0, flops = 0;
   ProfScope(fl_handle* h_, int c, cudaStream_t st) : h(h_), cls(c), s(st) {
     if (h->prof) {
       a = h->ev();
@@ -158,7 +159,7 @@ struct ProfScope {
     if (a) {
       cudaEvent_t b = h->ev();
       cudaEventRecordWithFlags(b, s, h->capturing ? cudaEventRecordExternal : 0);
-      (h->sink ? *h->sink : h->pending).push_back({cls, a, b, bytes});
+      (h->sink ? *h->sink : h->pending).push_back({cls, a, b, bytes, flops});
     }
   }
 };
@@ -373,13 +374,14 @@ int fl_profile(fl_handle* h, int enable) {
   }
   h->pending.clear();
   for (auto& kv : h->graphs) kv.second.pending = false;
-  for (int c = 0; c < FL_PROF_CLASSES; ++c) h->tot_ms[c] = h->tot_bytes[c] = 0, h->tot_n[c] = 0;
+  for (int c = 0; c < FL_PROF_CLASSES; ++c) h->tot_ms[c] = h->tot_bytes[c] = h->tot_flops[c] = 0, h->tot_n[c] = 0;
   h->prof = enable != 0;
   h->step_counter = 0;
   return FL_OK;
 }
 
-int fl_profile_read(fl_handle* h, int cls, double* total_ms, int64_t* records, double* bytes) {
+int fl_profile_read(fl_handle* h, int cls, double* total_ms, int64_t* records, double* bytes,
+                    double* flops) {
   if (!h || cls < 0 || cls >= FL_PROF_CLASSES) return fail(FL_EINVAL, "bad profile query");
   for (auto& kv : h->graphs) {
     if (kv.second.pending) {
@@ -393,6 +395,7 @@ int fl_profile_read(fl_handle* h, int cls, double* total_ms, int64_t* records, d
     FL_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
     h->tot_ms[r.cls] += ms;
     h->tot_bytes[r.cls] += r.bytes;
+    h->tot_flops[r.cls] += r.flops;
     h->tot_n[r.cls] += 1;
     h->ev_pool.push_back(r.a);
     h->ev_pool.push_back(r.b);
@@ -401,6 +404,7 @@ int fl_profile_read(fl_handle* h, int cls, double* total_ms, int64_t* records, d
   if (total_ms) *total_ms = h->tot_ms[cls];
   if (records) *records = h->tot_n[cls];
   if (bytes) *bytes = h->tot_bytes[cls];
+  if (flops) *flops = h->tot_flops[cls];
   return FL_OK;
 }
 
@@ -421,6 +425,7 @@ int gemm(fl_handle* h, const void* x, int ldx, const void* w, const void* bias, 
   ProfScope ps(h, FL_PROF_GEMM, s);
   const double oes = (epi == fl::EPI_STORE || epi == fl::EPI_GELU) ? h->es
                      : epi == fl::EPI_ARGMAX ? 0.0 : 4.0;
+  ps.flops = 2.0 * M * N * K;
   ps.bytes = (double)N * K * h->es + (double)M * K * h->es + (double)M * N * oes *
              (epi == fl::EPI_ACC_F32 ? 2.0 : 1.0);
   if (h->p.use_tensor_cores) return fl::gemm_tc(&h->tcws, a, s) ? FL_ECUDA : FL_OK;
@@ -444,7 +449,9 @@ int enqueue_step(fl_handle* h, int n_rows, int n_dec, bool want_logits, cudaStre
   const fl_pool_desc& p = h->p;
   const int d = m.d_model, hd = m.head_dim, L = m.n_layer, dt = m.dtype, es = h->es;
   const int Hl = h->Hl, Dl = h->Dl, Fl = h->Fl;
-  const bool tp = m.tp_size > 1;
+  // the collective path runs whenever a communicator exists (also at world 1,
+  // which exercises it on a single GPU)
+  const bool tp = h->comm != nullptr;
   const size_t kv_layer_elems = (size_t)p.pool_slots * 2 * Hl * p.max_seq * hd;
   char* kv = static_cast<char*>(p.kv);
   // greedy argmax fused into the LM-head GEMM epilogue (tensor-core path)
@@ -535,6 +542,8 @@ void harvest(fl_handle* h, std::vector<fl_handle::Rec>& recs) {
     if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) {
       h->tot_ms[r.cls] += ms;
       h->tot_bytes[r.cls] += r.bytes;
+      h->tot_flops[r.cls] += r.flops;
+    h->tot_flops[r.cls] += r.flops;
       h->tot_n[r.cls] += 1;
     }
   }

@@ -139,9 +139,9 @@ class CudaExecutor:
         self.use_graphs = use_graphs
         self._lib_timing = False
         _lib.check(self.lib.fl_configure(self.handle, int(use_graphs), 8, 0))
-        if tp_size > 1:
-            if comm_id is None:
-                raise InvalidParam("tp_size > 1 needs comm_id (see tp.make_comm_id)")
+        if tp_size > 1 and comm_id is None:
+            raise InvalidParam("tp_size > 1 needs comm_id (see tp.make_comm_id)")
+        if comm_id is not None:      # NCCL path (at tp_size 1 it still runs the collectives)
             buf = C.create_string_buffer(bytes(comm_id), 128)
             _lib.check(self.lib.fl_comm_init(self.handle, buf, tp_rank, tp_size))
 
@@ -436,7 +436,8 @@ class CudaExecutor:
         out = {}
         for name, cls in (("attention", _lib.PROF_ATTENTION), ("gemm", _lib.PROF_GEMM),
                           ("shuffle", _lib.PROF_SHUFFLE), ("step", _lib.PROF_STEP)):
-            ms, n, b = C.c_double(), C.c_int64(), C.c_double()
-            _lib.check(self.lib.fl_profile_read(self.handle, cls, C.byref(ms), C.byref(n), C.byref(b)))
-            out[name] = {"ms": ms.value, "records": n.value, "bytes": b.value}
+            ms, n, b, f = C.c_double(), C.c_int64(), C.c_double(), C.c_double()
+            _lib.check(self.lib.fl_profile_read(self.handle, cls, C.byref(ms), C.byref(n), C.byref(b),
+                                                C.byref(f)))
+            out[name] = {"ms": ms.value, "records": n.value, "bytes": b.value, "flops": f.value}
         return out
