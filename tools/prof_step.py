@@ -36,12 +36,14 @@ torch.cuda.synchronize()
 if a.profile:
     ex.profile(True)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+torch.cuda.profiler.start()          # ncu --profile-from-start off: steady-state decode only
 e0.record()
 t0 = time.perf_counter()
 for _ in range(a.iters):
     st.step_iteration()
 t1 = time.perf_counter()
 e1.record(); torch.cuda.synchronize()
+torch.cuda.profiler.stop()
 t2 = time.perf_counter()
 print(f"rows={a.rows} host launch {1e6*(t1-t0)/a.iters:.1f} us/iter, wall {1e6*(t2-t0)/a.iters:.1f} us/iter, "
       f"device {1e3*e0.elapsed_time(e1)/a.iters:.1f} us/iter")
