@@ -12,7 +12,7 @@ agg = collections.defaultdict(list)
 for d in data:
     if d['Metric Name'] == 'gpu__time_duration.sum':
         name = d['Kernel Name'].split('(')[0][:48]
-        agg[(name, d.get('Grid Size', ''))].append(float(d['Metric Value']) / (1e3 if d['Metric Unit'] == 'nsecond' else 1.0))
+        agg[(name, d.get('Grid Size', ''))].append(float(d['Metric Value'].replace(',', '')) / (1e3 if d['Metric Unit'] in ('ns', 'nsecond') else 1.0))
 tot = sum(sum(v) for v in agg.values())
 print(f"total {tot:.1f} us over {sum(len(v) for v in agg.values())} launches")
 for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):

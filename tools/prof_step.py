@@ -19,6 +19,7 @@ ap.add_argument("--config", default="c2")
 ap.add_argument("--rows", type=int, default=48)
 ap.add_argument("--iters", type=int, default=200)
 ap.add_argument("--profile", action="store_true")
+ap.add_argument("--pre", type=int, default=5, help="decode iterations before the measured loop (context growth)")
 a = ap.parse_args()
 cfg = bench.CONFIGS[a.config]
 spec = get_spec(cfg["spec"])
@@ -30,7 +31,7 @@ st = fl.FusionStream(reqs, fl.CostParams(preprocess_ms=0.0), fl.TPConfig(), exec
 torch.cuda.set_stream(ex.cs)
 st.try_fuse_pending()
 st.step_iteration()            # admission step (prefill rows)
-for _ in range(5):
+for _ in range(a.pre):
     st.step_iteration()
 torch.cuda.synchronize()
 if a.profile:
