@@ -1,0 +1,133 @@
+"""Dynamic batching -- the comparison discipline of config C5.
+
+Drop-in for the reference's ``run_dynamic_batching`` (baselines.py:51-127):
+arrivals are grouped into fixed windows anchored at the first arrival
+(``max_batch`` chunks dispatch when they fill), one instance runs the
+batches FIFO, a batch dispatches when its window closes, its members are
+preprocessed and the previous batch is done, and it runs as long as its
+longest member with every member riding along (nothing joins or leaves
+mid-batch).  With ``executor=None`` and the cost clock the trace is
+identical to the reference's (tests/test_baselines_golden.py).
+
+With a ``CudaExecutor`` each batch really runs on the B200: its members
+take slots 0..B-1 of a fresh window and every iteration is one ``fl_step``
+over the whole batch; members past their end marker stay in the window as
+ORPHAN rows (computed and discarded -- the rigid batch keeps paying for
+them, which is exactly what temporal fusion avoids).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+from .buffer import BufferLayout
+from .core import Request
+from .cost import CostParams, TPConfig, iteration_time
+from .errors import InvalidParam
+from .trace import EventKind, Trace, TraceEvent
+
+
+@dataclass(frozen=True)
+class BatchWindowConfig:
+    window_ms: float
+    max_batch: int | None = None
+
+    def __post_init__(self):
+        if self.window_ms < 0:
+            raise InvalidParam("window_ms must be >= 0")
+        if self.max_batch is not None and self.max_batch < 1:
+            raise InvalidParam("max_batch must be >= 1 when set")
+
+
+def _partition(ordered, cfg: BatchWindowConfig) -> list:
+    """[(members, nominal dispatch time)] in dispatch order."""
+    if cfg.window_ms == 0:
+        return [([r], r.arrival_time) for r in ordered]
+    t0 = ordered[0].arrival_time
+    windows: dict = {}
+    for r in ordered:
+        windows.setdefault(math.floor((r.arrival_time - t0) / cfg.window_ms), []).append(r)
+    out = []
+    for idx in sorted(windows):
+        close = t0 + (idx + 1) * cfg.window_ms
+        chunk = []
+        for r in windows[idx]:
+            chunk.append(r)
+            if cfg.max_batch is not None and len(chunk) == cfg.max_batch:
+                out.append((chunk, r.arrival_time))
+                chunk = []
+        if chunk:
+            out.append((chunk, close))
+    return out
+
+
+class _BatchStream:
+    """The slice of the FusionStream surface an executor reads."""
+
+    def __init__(self, clock: str):
+        self.layout = BufferLayout()
+        self.clock = clock
+        self.iteration_index = 0
+
+
+def run_dynamic_batching(requests, cfg: BatchWindowConfig, params: CostParams,
+                         tp: TPConfig | None = None, record_tokens: bool = True, *,
+                         executor=None, clock: str = "cost") -> Trace:
+    if clock not in ("cost", "device"):
+        raise InvalidParam(f"clock must be 'cost' or 'device', got {clock!r}")
+    if clock == "device" and executor is None:
+        raise InvalidParam("clock='device' needs an executor")
+    tp = tp or TPConfig()
+    ordered = sorted(requests, key=lambda r: (r.arrival_time, r.request_id))
+    ev = []
+    for r in ordered:
+        ev.append(TraceEvent(r.arrival_time, EventKind.ARRIVED, r.request_id, None))
+        ev.append(TraceEvent(r.arrival_time, EventKind.PREPROCESS_START, r.request_id, None))
+        ev.append(TraceEvent(r.arrival_time + params.preprocess_ms, EventKind.PREPROCESS_DONE,
+                             r.request_id, None))
+    trace = Trace("dynamic_batching", ev)
+    if not ordered:
+        return trace
+
+    done_at = None
+    for members, nominal in _partition(ordered, cfg):
+        start = max(nominal, max(r.arrival_time + params.preprocess_ms for r in members))
+        if done_at is not None:
+            start = max(start, done_at)
+        model_dur = iteration_time(len(members),
+                                   sum(m.batch_size * params.request_bytes for m in members),
+                                   params, tp)
+        n_iters = max(m.actual_output_length for m in members)
+        for m in members:
+            ev.append(TraceEvent(start, EventKind.FUSED, m.request_id, None))
+        bs = None
+        if executor is not None:
+            bs = _BatchStream(clock)
+            for m in members:
+                executor.on_fuse(m.request_id, bs.layout.fuse_request(m.request_id, 1), m)
+        t = start
+        for k in range(1, n_iters + 1):
+            dur = model_dur
+            if bs is not None:
+                dev = executor.run_iteration(bs)
+                bs.iteration_index += 1
+                if clock == "device":
+                    dur = dev
+            t = start + k * dur if clock == "cost" else t + dur
+            for m in members:
+                if k <= m.actual_output_length:
+                    if record_tokens:
+                        ev.append(TraceEvent(t, EventKind.TOKEN_GENERATED, m.request_id, k))
+                    if k == m.actual_output_length:
+                        ev.append(TraceEvent(t, EventKind.EVICTED, m.request_id, None))
+                        if bs is not None:       # rides along as an ORPHAN row
+                            slot = bs.layout.per_request_offset[m.request_id]
+                            bs.layout.evict_request(m.request_id)
+                            executor.on_evict(m.request_id, slot)
+            ev.append(TraceEvent(t, EventKind.ITERATION_COMPLETED, None, dur))
+        done_at = start + n_iters * model_dur if clock == "cost" else t
+    if executor is not None:
+        executor.on_drain(None)
+    trace.sort()
+    return trace

@@ -299,7 +299,42 @@ def gen_schedules():
     _dump("schedules.json.gz", {"cases": cases}, gz=True)
 
 
+def gen_dynbatch():
+    """run_dynamic_batching traces (baselines.py:51-127)."""
+    from fusionsim.baselines import BatchWindowConfig, run_dynamic_batching
+    cases = []
+
+    def add(name, reqs, window, max_batch, cost, tp=1, record_tokens=True):
+        tr = run_dynamic_batching(reqs, BatchWindowConfig(window, max_batch), CostParams(**cost),
+                                  TPConfig(tp_size=tp), record_tokens=record_tokens).format_lines()
+        cases.append({"name": name, "requests": req_json(reqs), "window": window,
+                      "max_batch": max_batch,
+                      "cost": {k: (v.hex() if isinstance(v, float) else v) for k, v in cost.items()},
+                      "tp": tp, "record_tokens": record_tokens, "trace_sha": sha(tr),
+                      "n_events": len(tr), "trace_head": tr[:80]})
+
+    # reference tests/test_baselines.py worked examples
+    add("worked", [_req(0, 0.0, 3), _req(1, 100.0, 2), _req(2, 510.0, 4)], 500.0, None, {})
+    add("maxbatch", [_req(i, 1.0 * i, 2 + i) for i in range(5)], 100.0, 2, TIGHT)
+    add("zero_window", [_req(i, 7.0 * i, 3) for i in range(4)], 0.0, None, TIGHT)
+    add("tp2", [_req(i, 13.0 * i, 4 + i % 3) for i in range(6)], 25.0, 3, TIGHT, tp=2)
+    for lam in (1, 4, 16, 64):
+        n, mean, lo, hi, mx, il = SCEN["c3"]
+        sc = Scenario(scenario_id="c5", discipline=Discipline.DYNAMIC_BATCHING, n_requests=48,
+                      arrival=PoissonArrival(1000.0 / lam), lengths=UniformLength(lo, hi),
+                      max_output_length=mx, input_len=il, window_ms=50.0)
+        add(f"c5/lam{lam}", build_requests(sc, 1), 50.0, None, {}, record_tokens=lam != 64)
+    g = Xorshift64Star(777)
+    for i in range(40):
+        cost = random_cost(g)
+        reqs = random_requests(g)
+        add(f"rand{i}", reqs, 60.0 * g.next_float(), g.uniform_int(1, 4) if i % 2 else None, cost,
+            tp=2 if i % 3 == 0 else 1)
+    _dump("dynbatch.json.gz", {"cases": cases}, gz=True)
+
+
 if __name__ == "__main__":
+    gen_dynbatch()
     gen_rng()
     gen_alg1()
     gen_plans()
