@@ -415,7 +415,8 @@ namespace {
 using fl::GemmArgs;
 
 int gemm(fl_handle* h, const void* x, int ldx, const void* w, const void* bias, void* out,
-          int ldo, int M, int N, int K, int epi, cudaStream_t s) {
+          int ldo, int M, int N, int K, int epi, cudaStream_t s,
+          const fl::RopeArgs* rope = nullptr, bool* fused = nullptr) {
   GemmArgs a{x, w, bias, out, M, N, K, ldx, ldo, epi, h->m.dtype, h->p.max_rows};
   if (epi == fl::EPI_ARGMAX) {
     a.keys = h->keys;
@@ -428,7 +429,21 @@ int gemm(fl_handle* h, const void* x, int ldx, const void* w, const void* bias, 
   ps.flops = 2.0 * M * N * K;
   ps.bytes = (double)N * K * h->es + (double)M * K * h->es + (double)M * N * oes *
              (epi == fl::EPI_ACC_F32 ? 2.0 : 1.0);
-  if (h->p.use_tensor_cores) return fl::gemm_tc(&h->tcws, a, s) ? FL_ECUDA : FL_OK;
+  if (fused) *fused = false;
+  // the fused rotary/KV-append epilogue is opt-in: measured slower than the
+  // separate k_rope_append at C3 (per-element sincos + scattered KV stores)
+  static const bool fuse = getenv("FL_QKV_FUSE") != nullptr;
+  if (!fuse) rope = nullptr;
+  if (rope) {
+    a.epi = h->p.use_tensor_cores ? fl::EPI_QKV : fl::EPI_STORE;
+    a.rope = *rope;
+  }
+  if (h->p.use_tensor_cores) {
+    const int r = fl::gemm_tc(&h->tcws, a, s);
+    if (r < 0) return FL_ECUDA;
+    if (fused) *fused = rope && r == 0;
+    return FL_OK;
+  }
   fl::gemm_simt(a, s);
   return FL_OK;
 }
@@ -469,9 +484,26 @@ int enqueue_step(fl_handle* h, int n_rows, int n_dec, bool want_logits, cudaStre
     void* kvl = kv + kv_layer_elems * es * l;
     // K2 + K3
     fl::launch_layernorm(h->x, W[FL_W_LN1_G], W[FL_W_LN1_B], h->h, n_rows, d, m.ln_eps, dt, s);
-    FL_GEMM(h->h, d, W[FL_W_QKV], W[FL_W_QKV_B], h->qkv, 3 * Dl, n_rows, 3 * Dl, d, fl::EPI_STORE, s);
-    fl::launch_rope_append(h->qkv, h->rows, h->row_pos, n_rows, Hl, hd, m.rotary_dim, m.family, kvl,
-                           p.pool_slots, p.max_seq, h->q, dt, s);
+    // QKV projection; on the tcgen05 path its epilogue applies the rotary and
+    // appends K/V at each row's (slot, pos) itself (EPI_QKV)
+    fl::RopeArgs ra;
+    ra.rows = h->rows;
+    ra.row_pos = h->row_pos;
+    ra.kv_layer = kvl;
+    ra.q_out = h->q;
+    ra.Hl = Hl;
+    ra.hd = hd;
+    ra.rot = m.family == FL_FAMILY_GPT2 ? 0 : m.rotary_dim;
+    ra.family = m.family;
+    ra.S = p.max_seq;
+    bool qkv_fused = false;
+    FL_GEMM(h->h, d, W[FL_W_QKV], W[FL_W_QKV_B], h->qkv, 3 * Dl, n_rows, 3 * Dl, d, fl::EPI_STORE, s,
+            &ra, &qkv_fused);
+    if (!qkv_fused) {
+      fl::launch_rope_append(h->qkv, h->rows, h->row_pos, n_rows, Hl, hd, m.rotary_dim, m.family,
+                             kvl, p.pool_slots, p.max_seq, h->q, dt, s);
+      fl::g_launches += 1;
+    }
     // K4
     {
       ProfScope ps(h, FL_PROF_ATTENTION, s);
@@ -479,7 +511,7 @@ int enqueue_step(fl_handle* h, int n_rows, int n_dec, bool want_logits, cudaStre
                                              p.pool_slots, p.max_seq, att_keys, h->a, h->att_o,
                                              h->att_ml, dt, s);
     }
-    fl::g_launches += 2;
+    fl::g_launches += 1;
     // MLP input: GPT-2 = LN2 of the updated residual; GPT-J = LN1 output;
     // NeoX = LN2 of the residual *before* the attention update.
     if (m.family == FL_FAMILY_NEOX) {

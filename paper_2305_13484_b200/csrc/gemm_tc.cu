@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               const bf16* __restrict__ bias, void* __restrict__ out, int M, int N, int ldo, int epi,
               int kch_total, int kch_per_split, unsigned long long* __restrict__ keys,
               int index_base, int bn, int CM, int MT, int WT, int stages, int ncols,
-              int cl_split, unsigned long long* __restrict__ dbg) {
+              int cl_split, const RopeArgs rope, unsigned long long* __restrict__ dbg) {
   // cl_split: the S K-splits form a cluster and reduce through DSMEM; otherwise
   // every split is independent and (EPI_ACC_F32) red.adds its partial.
   constexpr int RED_LD = TC_BM + 4;          // partial chunk [CH][132] fp32 (n fastest)
@@ -441,7 +441,48 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             for (int j = 0; j < 32; ++j) r[j] = 0u;
           }
           const int ncol = min(32, mcount - cb);
-          if (epi == EPI_ARGMAX) {
+          if (epi == EPI_QKV) {
+            // q/k/v section, head and dim of this weight row; rotary partner is a
+            // lane of this warp (GPT-J: n^1; NeoX: n +- rot/2 inside the head's
+            // first rot dims -- a head starts on a 32-row boundary for hd % 32 == 0)
+            const int D = rope.Hl * rope.hd;
+            const int sec = n / D, rem = n - sec * D;
+            const int hh = rem / rope.hd, ii = rem - hh * rope.hd;
+            const bool rot_row = sec < 2 && ii < rope.rot;
+            int src = lane, jf = 0;
+            float sgn = 0.f;
+            if (rope.family == FL_FAMILY_GPTJ) {
+              src = lane ^ 1; jf = ii >> 1; sgn = (ii & 1) ? 1.f : -1.f;
+            } else if (rope.family == FL_FAMILY_NEOX) {
+              const int half = rope.rot >> 1;
+              src = ii < half ? lane + half : lane - half;
+              jf = ii < half ? ii : ii - half;
+              sgn = ii < half ? -1.f : 1.f;
+            }
+            src = rot_row ? src : lane;
+            const float inv_freq = exp2f(-(2.f * jf / max(rope.rot, 1)) * 13.287712379549449f);
+#pragma unroll 4
+            for (int j = 0; j < 32; ++j) {
+              if (j >= ncol) break;
+              float x = __uint_as_float(r[j]) + bv;
+              const float xp = __shfl_sync(0xffffffffu, x, src);
+              const int mg = m0 + cb + j;
+              const int pos = rope.row_pos[mg];
+              if (rot_row) {
+                float sn, cs;
+                sincosf(static_cast<float>(pos) * inv_freq, &sn, &cs);
+                x = x * cs + sgn * xp * sn;
+              }
+              if (!nok) continue;
+              if (sec == 0) {
+                static_cast<bf16*>(rope.q_out)[static_cast<size_t>(mg) * D + rem] = __float2bfloat16_rn(x);
+              } else if (rope.rows[mg].kind != FL_ROW_ORPHAN) {
+                const size_t slot = rope.rows[mg].slot;
+                const size_t o = (((slot * 2 + (sec - 1)) * rope.Hl + hh) * rope.S + pos) * rope.hd + ii;
+                static_cast<bf16*>(rope.kv_layer)[o] = __float2bfloat16_rn(x);
+              }
+            }
+          } else if (epi == EPI_ARGMAX) {
 #pragma unroll 4
             for (int j = 0; j < 32; ++j) {
               if (j >= ncol) break;
@@ -655,7 +696,7 @@ int launch_tc(const GemmArgs& a, const CUtensorMap* mw, const CUtensorMap* mx, i
   cudaError_t e = launch_k(cm == 2 ? k_gemm_tc<true> : k_gemm_tc<false>, grid, dim3(TC_THREADS), smem, s, dim3(cm, 1, cl_split ? splits : 1), *mw, *mx,
                            static_cast<const bf16*>(a.bias), a.out, a.M, a.N, a.ldo, a.epi,
                            a.K / TC_BK, kpc, a.keys, a.index_base, bn, cm, mt, wt, stages, ncols,
-                           cl_split, g_dbg);
+                           cl_split, a.rope, g_dbg);
   if (e != cudaSuccess) {
     char buf[256];
     snprintf(buf, sizeof buf, "k_gemm_tc launch (grid %u,%u,%u cluster %d,1,%d smem %d stages %d bn %d): %s",
@@ -725,6 +766,7 @@ int gemm_tc(TcWorkspace* ws, const GemmArgs& a, cudaStream_t s) {
   int S = 1;
   if (a.epi != EPI_ARGMAX) {
     const int smax = (bn >= 128 || a.epi == EPI_ACC_F32) ? 8 : 4;
+    // (EPI_QKV is only ever requested when the caller accepts S == 1)
     while (S < smax && tiles * (S + 1) <= ws->num_sms && kch / (S + 1) >= 2) ++S;
   }
   if (force_s > 0 && a.epi != EPI_ARGMAX) S = force_s;
@@ -739,6 +781,13 @@ int gemm_tc(TcWorkspace* ws, const GemmArgs& a, cudaStream_t s) {
   CUtensorMap *mw, *mx;
   if (!make_map(cache, a.w, a.N, a.K, a.K, TC_BM, &mw)) return -1;
   if (!make_map(cache, a.x, a.mcap > a.M ? a.mcap : a.M, a.K, a.ldx, bn / cm, &mx)) return -1;
+  // the fused QKV epilogue needs whole sums in registers: with a clustered
+  // K split it falls back to a plain store (return 2: caller runs k_rope_append)
+  if (a.epi == EPI_QKV && S > 1) {
+    GemmArgs b = a;
+    b.epi = EPI_STORE;
+    return launch_tc(b, mw, mx, S, kpc2, bn, cm, mt, wt, s) ? -1 : 2;
+  }
   return launch_tc(a, mw, mx, S, kpc2, bn, cm, mt, wt, s);
 }
 

@@ -26,7 +26,8 @@ const char* tc_last_error();
 void tc_set_debug(unsigned long long* p);
 
 // out[M,N] = X[M,K] . W[N,K]^T (+bias, epilogue), bf16 operands, fp32 accumulate in TMEM.
-// Returns 0, or -1 with tc_last_error() set (shape the kernel does not cover).
+// Returns 0, or -1 with tc_last_error() set (shape the kernel does not cover);
+// EPI_QKV returns 2 when it fell back to a plain store into a.out.
 int gemm_tc(TcWorkspace* ws, const GemmArgs& a, cudaStream_t s);
 
 }  // namespace fl
