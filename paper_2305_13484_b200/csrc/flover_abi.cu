@@ -575,7 +575,6 @@ void harvest(fl_handle* h, std::vector<fl_handle::Rec>& recs) {
       h->tot_ms[r.cls] += ms;
       h->tot_bytes[r.cls] += r.bytes;
       h->tot_flops[r.cls] += r.flops;
-    h->tot_flops[r.cls] += r.flops;
       h->tot_n[r.cls] += 1;
     }
   }
@@ -699,12 +698,16 @@ extern "C" int fl_gemm(const void* x, int ldx, const void* w, const void* bias, 
   fl::GemmArgs a{x, w, bias, out, M, N, K, ldx, ldo, epi, dtype, M};
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (use_tc) {
+    if (g_dbg_base != workspace) {
+      if (g_dbg_base) fl::tc_destroy(&g_dbg_ws);
+      if (fl::tc_init(&g_dbg_ws, workspace, fl::tc_workspace_bytes(0, 0)))
+        return fail(FL_ECUDA, "%s", fl::tc_last_error());
+      g_dbg_base = workspace;
+    }
     // the caller's scratch may have been reused by the allocator: re-arm the
-    // split-K counters every call (diagnostic path only)
-    if (g_dbg_base) fl::tc_destroy(&g_dbg_ws);
-    if (fl::tc_init(&g_dbg_ws, workspace, fl::tc_workspace_bytes(0, 0)))
-      return fail(FL_ECUDA, "%s", fl::tc_last_error());
-    g_dbg_base = workspace;
+    // stream-K flags on the stream every call (diagnostic path only)
+    static const bool no_rearm = getenv("FL_GEMM_NO_REARM") != nullptr;   // timing loops
+    if (!no_rearm) FL_CUDA(fl::sk_rearm(workspace, s));
     if (fl::gemm_tc(&g_dbg_ws, a, s)) return fail(FL_EINVAL, "%s", fl::tc_last_error());
   } else {
     fl::gemm_simt(a, s);

@@ -1,0 +1,911 @@
+// K3/K5/K6/K7/K8 projections: persistent stream-K GEMM on 2-SM tcgen05 pairs.
+//
+// out[M,N] = X[M,K] . W[N,K]^T, swap-AB: a CTA pair (cluster of 2, one
+// tcgen05.mma.cta_group::2 per K-step) owns a 256-row weight tile on the UMMA
+// M side -- each CTA stages its own 128 weight rows and half of the window's
+// token columns -- and the whole fused window (<= 512 tokens, MT sub-tiles of
+// BN <= 256 columns) on the UMMA N side, accumulated in TMEM.
+//
+// Work decomposition (stream-K): the (token tile, weight tile, 64-wide K
+// chunk) units of the GEMM are dealt out as equal contiguous ranges to one
+// pair per two SMs, so every SM streams the same number of weight bytes no
+// matter how N/256 divides 74 (QKV: 48 tiles, FFN-up: 64, attn-out: 16 ...).
+// A range crosses weight tiles; the piece of a tile a pair owns is a
+// "segment".  A tile split between pairs is finished by
+//   - residual GEMMs (EPI_ACC_F32): every segment red.add.v4's its partial
+//     into the fp32 residual (bias from the segment holding k = 0);
+//   - all other epilogues: the segment holding k = 0 (always the LAST segment
+//     of its pair's range, while the other pieces are the FIRST segments of
+//     the following pairs' ranges) waits for the others' fp32 partials
+//     (workspace slot per pair + release/acquire flag, self-resetting) and
+//     runs the epilogue on the full sum.  Waits only point to higher pairs,
+//     so they cannot cycle.
+//
+// Roles (256 threads per CTA):
+//   warp 0   : TMA producer of the weight tiles (ahead of griddepcontrol.wait)
+//   warps 6,7: TMA producers of the token sub-tiles
+//   warp 1   : TMEM allocator; in the leader CTA lane 0 issues the MMAs
+//   warps 2-5: epilogue (TMEM lanes 32*(warp%4)..+32), double-buffered TMEM
+//              accumulators when the window fits 256 columns
+// Reference: the modelled step is cost.py:89-109 (iteration_time); the GEMMs
+// are the FC layers the paper shards across TP ranks.
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <map>
+#include <string>
+#include <tuple>
+
+#include "common.cuh"
+#include "gemm_tc.cuh"
+
+namespace fl {
+
+namespace {
+
+constexpr int SK_BM = 128;                 // weight rows per CTA (256 per pair)
+constexpr int SK_BK = 64;                  // K per stage (one 128-byte swizzle row)
+constexpr int SK_THREADS = 256;
+constexpr int SK_A_BYTES = SK_BM * SK_BK * 2;
+constexpr int SK_MAXST = 16;
+constexpr int SK_RING_BUDGET = 200 * 1024;
+constexpr int SK_STG_LD = 36;              // transpose row stride (floats): conflict-free
+
+thread_local std::string g_sk_err;
+unsigned long long* g_sk_dbg = nullptr;
+
+FL_DEV uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+FL_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+FL_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+FL_DEV bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// one waiting thread with back-off (keeps the MIO queue free for the others)
+FL_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try(bar, parity)) __nanosleep(40);
+}
+FL_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred done;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+      "@!done bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// arrive on the barrier at the same smem offset in cluster CTA `rank`
+FL_DEV void mbar_arrive_cluster(uint64_t* bar, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+// 2-SM load: lands in this CTA's smem, completes tx on the leader's barrier
+FL_DEV void tma_load_pair(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1) {
+  const uint32_t leader_bar = smem_u32(bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, "
+      "{%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+FL_DEV void mma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+// arrive on `bar` in both CTAs of the pair (mask = 3 << even rank of the pair)
+FL_DEV void commit_pair(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], "
+      "%1;" ::"r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+FL_DEV uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+FL_DEV float4 ld_dsmem_f4(const void* local, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local)), "r"(rank));
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(remote));
+  return v;
+}
+FL_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+FL_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+FL_DEV void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+FL_DEV uint64_t desc_sw128(const void* tile) {
+  const uint64_t addr = smem_u32(tile);
+  uint64_t d = (addr >> 4) & 0x3FFFull;
+  d |= 1ull << 16;
+  d |= (1024ull >> 4) << 32;
+  d |= 1ull << 46;
+  d |= 2ull << 61;
+  return d;
+}
+__host__ __device__ constexpr uint32_t idesc_bf16(int m, int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(m >> 4) << 24);
+}
+FL_DEV void tmem_ld32(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+        "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+        "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+FL_DEV void red_add_v4(float* p, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+FL_DEV unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+FL_DEV void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+FL_DEV void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }   // the 4 epilogue warps
+
+struct SkParams {
+  int M, N, ldo, epi;
+  int kch;          // K / 64
+  int ntn;          // 256-row weight tiles
+  int mt, bn;       // token sub-tiles per tile and their width (UMMA N)
+  int span;         // tokens per token tile (mt * bn)
+  int stages, ncols, nbuf;
+  int units, npairs;
+  const bf16* bias;
+  void* out;
+  unsigned long long* keys;
+  int index_base;
+  float* part;      // [npairs][2][span_max][128] fp32 partial slots
+  unsigned* flags;  // [npairs][2]
+  int slot_elems;   // floats per (pair, half) slot
+  int vec;          // out rows 16-byte aligned: vector stores
+  int red;          // EPI_ACC_F32 split tiles: red.add pieces (else owner fix-up)
+  int csplit;       // >1: the S pairs of a cluster split one tile's K, DSMEM reduction
+  RopeArgs rope;
+  unsigned long long* dbg;   // diagnostics: per CTA [prod wait, prod total, mma wait, mma total]
+};
+
+// unit range of pair p: [p*U/P, (p+1)*U/P)
+FL_DEV int range_lo(int p, const SkParams& P) {
+  return static_cast<int>((static_cast<long long>(p) * P.units) / P.npairs);
+}
+// the pair whose range holds unit x
+FL_DEV int owner_of(int x, const SkParams& P) {
+  return static_cast<int>(((static_cast<long long>(x) + 1) * P.npairs + P.units - 1) / P.units) - 1;
+}
+
+// EPI_QKV epilogue of 32 token columns [mbase, mbase+ncol) of this thread's
+// weight row n (full sums, bias included): rotary on q/k, q -> q_out, k/v ->
+// the KV pool at each row's (slot, pos) -- what k_rope_append does.
+FL_DEV void epi_qkv(const SkParams& P, const float* v, int n, bool nok, int mbase, int ncol, int lane) {
+  const RopeArgs& rope = P.rope;
+  const int D = rope.Hl * rope.hd;
+  const int sec = n / D, rem = n - sec * D;
+  const int hh = rem / rope.hd, ii = rem - hh * rope.hd;
+  const bool rot_row = sec < 2 && ii < rope.rot;
+  int src = lane, jf = 0;
+  float sgn = 0.f;
+  if (rope.family == FL_FAMILY_GPTJ) {
+    src = lane ^ 1; jf = ii >> 1; sgn = (ii & 1) ? 1.f : -1.f;
+  } else if (rope.family == FL_FAMILY_NEOX) {
+    const int half = rope.rot >> 1;
+    src = ii < half ? lane + half : lane - half;
+    jf = ii < half ? ii : ii - half;
+    sgn = ii < half ? -1.f : 1.f;
+  }
+  src = rot_row ? src : lane;
+  const float inv_freq = exp2f(-(2.f * jf / max(rope.rot, 1)) * 13.287712379549449f);
+#pragma unroll 4
+  for (int j = 0; j < 32; ++j) {
+    if (j >= ncol) break;
+    float x = v[j];
+    const float xp = __shfl_sync(0xffffffffu, x, src);
+    const int mg = mbase + j;
+    const int pos = rope.row_pos[mg];
+    if (rot_row) {
+      float sn, cs;
+      sincosf(static_cast<float>(pos) * inv_freq, &sn, &cs);
+      x = x * cs + sgn * xp * sn;
+    }
+    if (!nok) continue;
+    if (sec == 0) {
+      static_cast<bf16*>(rope.q_out)[static_cast<size_t>(mg) * D + rem] = __float2bfloat16_rn(x);
+    } else if (rope.rows[mg].kind != FL_ROW_ORPHAN) {
+      const size_t slot = rope.rows[mg].slot;
+      const size_t o = (((slot * 2 + (sec - 1)) * rope.Hl + hh) * rope.S + pos) * rope.hd + ii;
+      static_cast<bf16*>(rope.kv_layer)[o] = __float2bfloat16_rn(x);
+    }
+  }
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(SK_THREADS, 1)
+    k_gemm_sk(const __grid_constant__ CUtensorMap tma_w, const __grid_constant__ CUtensorMap tma_x,
+              const __grid_constant__ SkParams P) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[SK_MAXST];
+  __shared__ __align__(8) uint64_t empty_bar[SK_MAXST];
+  __shared__ __align__(8) uint64_t tfull_bar[2];
+  __shared__ __align__(8) uint64_t tempty_bar[2];
+  __shared__ uint32_t tmem_base;
+  __shared__ __align__(16) float stg[4 * 32 * SK_STG_LD];   // epilogue transpose, 32x36 per warp
+
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned long long g_start = 0;
+  if (P.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
+  const int xi = blockIdx.x & 1;                 // position in the pair (cluster rank)
+  const int pair = blockIdx.x >> 1;
+  const bool leader = xi == 0;
+  const uint32_t crank = cluster_ctarank();
+  const uint32_t prank = crank & ~1u;            // the pair's leader in the cluster
+  const uint16_t pmask = static_cast<uint16_t>(3u << prank);
+  const int XB = (P.bn / 2) * SK_BK * 2;         // this CTA's half of a token sub-tile
+  const int STAGE = SK_A_BYTES + P.mt * XB;
+  const int stages = P.stages, kch = P.kch;
+  const int u0 = range_lo(pair, P), u1 = range_lo(pair + 1, P);
+
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_w)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_x)) : "memory");
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full_bar[s], 1 + P.mt);   // weight producer + one per token sub-tile
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull_bar[b], 1);
+      mbar_init(&tempty_bar[b], 8);   // 4 epilogue warps x 2 CTAs
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
+                 "r"(P.ncols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  pdl_trigger();
+  const uint32_t tmem = tmem_base;
+  const int acc_cols = P.mt * P.bn;
+
+  if (warp == 0 || warp >= 6) {
+    // producers: warp 0 streams the weight tiles, warp 6 + j the token
+    // sub-tile j -- one TMA request per thread per K chunk (a request costs
+    // its issuing thread ~250 cycles, tools/probes/tma_rate.cu)
+    const int role = warp == 0 ? -1 : warp - 6;   // -1: weights, j >= 0: token sub-tile j
+    if (lane == 0 && role < P.mt) {
+      auto coords = [&](int u, int& m0, int& n0, int& k) {
+        const int t = u / kch;
+        k = (u - t * kch) * SK_BK;
+        const int tm = t / P.ntn, tn = t - tm * P.ntn;
+        m0 = tm * P.span;
+        n0 = tn * 2 * SK_BM + xi * SK_BM;
+      };
+      const uint32_t my_tx = 2u * (role < 0 ? SK_A_BYTES : XB);   // both CTAs' bytes
+      auto issue = [&](int u, int st) {
+        int m0, n0, k;
+        coords(u, m0, n0, k);
+        if (leader) mbar_expect_tx(&full_bar[st], my_tx);
+        if (role < 0)
+          tma_load_pair(&tma_w, &full_bar[st], smem + st * STAGE, k, n0);
+        else
+          tma_load_pair(&tma_x, &full_bar[st], smem + st * STAGE + SK_A_BYTES + role * XB, k,
+                        m0 + role * P.bn + xi * (P.bn / 2));
+      };
+      const int pre = min(u1 - u0, stages);
+      if (role >= 0) pdl_wait();            // activations are the predecessor's output
+      for (int i = 0; i < pre; ++i) issue(u0 + i, i);   // weights stream ahead of the wait
+      int s = pre % stages;
+      uint32_t ph = pre == stages ? 1u : 0u;
+      unsigned long long waited = 0, t_start = clock64();
+      for (int u = u0 + pre; u < u1; ++u) {
+        const unsigned long long tw = P.dbg ? clock64() : 0;
+        mbar_wait(&empty_bar[s], ph ^ 1);
+        if (P.dbg) waited += clock64() - tw;
+        issue(u, s);
+        if (++s == stages) { s = 0; ph ^= 1; }
+      }
+      if (P.dbg && role < 0) {
+        P.dbg[4 * blockIdx.x + 0] = waited;
+        P.dbg[4 * blockIdx.x + 1] = clock64() - t_start;
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      const uint32_t idesc = idesc_bf16(2 * SK_BM, P.bn);
+      int s = 0, seg = 0;
+      uint32_t ph = 0;
+      unsigned long long waited = 0, twait = 0, t_start = clock64();
+      for (int u = u0; u < u1;) {
+        const int t = u / kch;
+        const int klo = u - t * kch;
+        const int khi = min(kch, klo + (u1 - u));
+        const int b = P.nbuf == 2 ? (seg & 1) : 0;
+        const uint32_t use = P.nbuf == 2 ? (seg >> 1) : seg;
+        unsigned long long tw = P.dbg ? clock64() : 0;
+        mbar_wait(&tempty_bar[b], (use & 1) ^ 1);   // epilogue drained this buffer
+        if (P.dbg) twait += clock64() - tw;
+        tc_fence_after();
+        const uint32_t acc = tmem + b * acc_cols;
+        for (int c = klo; c < khi; ++c) {
+          tw = P.dbg ? clock64() : 0;
+          mbar_wait(&full_bar[s], ph);
+          if (P.dbg) waited += clock64() - tw;
+          tc_fence_after();
+          const uint8_t* st = smem + s * STAGE;
+          const uint64_t ad = desc_sw128(st);
+          for (int j = 0; j < P.mt; ++j) {
+            const uint64_t bd = desc_sw128(st + SK_A_BYTES + j * XB);
+#pragma unroll
+            for (int kk = 0; kk < SK_BK / 16; ++kk)
+              mma_pair(acc + j * P.bn, ad + 2 * kk, bd + 2 * kk, idesc, (c > klo) | kk);
+          }
+          commit_pair(&empty_bar[s], pmask);
+          if (++s == stages) { s = 0; ph ^= 1; }
+        }
+        commit_pair(&tfull_bar[b], pmask);
+        u += khi - klo;
+        ++seg;
+      }
+      if (P.dbg) {
+        P.dbg[4 * blockIdx.x + 2] = waited;
+        P.dbg[4 * blockIdx.x + 3] = clock64() - t_start;
+        P.dbg[4 * (2048 + blockIdx.x) + 0] = twait;
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- epilogue
+    pdl_wait();   // EPI_ACC_F32 reads `out`, written by predecessors
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    int seg = 0;
+    unsigned long long e_wait = 0, e_flag = 0, e_blk = 0, e_post = 0, e_ld = 0, e_sts = 0, e_t0 = clock64();
+    if (P.csplit > 1) {
+      // ---- even split-K: the S pairs t*S .. t*S+S-1 each hold the fp32 partial
+      // of one K piece of tile t.  All publish, then piece s reduces tokens
+      // [s, s+1) * mcount / S over the S slots and runs the epilogue -- the
+      // fix-up is spread over the S pairs instead of serialised in one owner.
+      const int S = P.csplit;
+      const int t = u0 / kch, piece = pair - t * S;
+      const int tm = t / P.ntn, tn = t - tm * P.ntn;
+      const int m0 = tm * P.span;
+      const int mcount = min(P.span, P.M - m0);
+      const int nbase = tn * 2 * SK_BM + xi * SK_BM;
+      const uint32_t tacc = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+      if (warp == 2 && lane == 0) mbar_wait_sleep(&tfull_bar[0], 0);
+      epi_bar();
+      tc_fence_after();
+      float* pub = P.part + static_cast<size_t>(pair * 2 + xi) * P.slot_elems;
+      float* ws_ = stg + quarter * (32 * SK_STG_LD);
+      const int c4 = (lane & 7) * 4, jb = lane >> 3;
+      for (int cb = 0; cb < mcount; cb += 32) {
+        uint32_t r[32];
+        tmem_ld32(tacc + cb, r);
+        const int ncol = min(32, mcount - cb);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) ws_[j * SK_STG_LD + lane] = __uint_as_float(r[j]);
+        __syncwarp();
+        float* dst = pub + static_cast<size_t>(cb) * SK_BM + quarter * 32 + c4;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int j = i * 4 + jb;
+          if (j < ncol)
+            *reinterpret_cast<float4*>(dst + j * SK_BM) = *reinterpret_cast<const float4*>(ws_ + j * SK_STG_LD + c4);
+        }
+        __syncwarp();
+      }
+      __threadfence();
+      epi_bar();
+      unsigned* arrive = P.flags + 2 * SK_MAX_PAIRS + (t * 2 + xi);
+      unsigned* done = arrive + 2 * SK_MAX_PAIRS;
+      if (warp == 2 && lane == 0) {
+        atomicAdd(arrive, 1u);
+        long long spins = 0;
+        while (ld_acquire(arrive) < static_cast<unsigned>(S)) {
+          __nanosleep(64);
+          if (++spins > (1ll << 26)) __trap();
+        }
+      }
+      epi_bar();
+      // reduce my token slice: warp (quarter) takes tokens, lane = 4 weight rows
+      const int lo = piece * mcount / S, hi = (piece + 1) * mcount / S;
+      const int rrow = lane * 4;                      // row within this CTA's 128
+      const int nn = nbase + rrow;
+      float b4[4] = {0.f, 0.f, 0.f, 0.f};
+      if (P.bias)
+        for (int q = 0; q < 4; ++q) b4[q] = nn + q < P.N ? __bfloat162float(P.bias[nn + q]) : 0.f;
+      for (int tok = lo + quarter; tok < hi; tok += 4) {
+        float4 acc = make_float4(b4[0], b4[1], b4[2], b4[3]);
+        float4 q[4];
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+          if (p < S)
+            q[p] = *reinterpret_cast<const float4*>(P.part + static_cast<size_t>((t * S + p) * 2 + xi) * P.slot_elems +
+                                                    static_cast<size_t>(tok) * SK_BM + rrow);
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+          if (p < S) { acc.x += q[p].x; acc.y += q[p].y; acc.z += q[p].z; acc.w += q[p].w; }
+        const size_t o = static_cast<size_t>(m0 + tok) * P.ldo + nn;
+        if (nn + 3 < P.N && P.vec) {
+          if (EPI == EPI_ACC_F32) {
+            float4* d = reinterpret_cast<float4*>(static_cast<float*>(P.out) + o);
+            const float4 y = *d;
+            *d = make_float4(y.x + acc.x, y.y + acc.y, y.z + acc.z, y.w + acc.w);
+          } else if (EPI == EPI_STORE_F32) {
+            *reinterpret_cast<float4*>(static_cast<float*>(P.out) + o) = acc;
+          } else {
+            if (EPI == EPI_GELU) {
+              acc.x = gelu_tanh(acc.x); acc.y = gelu_tanh(acc.y); acc.z = gelu_tanh(acc.z); acc.w = gelu_tanh(acc.w);
+            }
+            __nv_bfloat162 l2 = __floats2bfloat162_rn(acc.x, acc.y), h2 = __floats2bfloat162_rn(acc.z, acc.w);
+            *reinterpret_cast<uint2*>(static_cast<bf16*>(P.out) + o) =
+                make_uint2(*reinterpret_cast<uint32_t*>(&l2), *reinterpret_cast<uint32_t*>(&h2));
+          }
+        } else {
+          const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+          for (int qq = 0; qq < 4 && nn + qq < P.N; ++qq) {
+            if (EPI == EPI_ACC_F32) static_cast<float*>(P.out)[o + qq] += a4[qq];
+            else if (EPI == EPI_STORE_F32) static_cast<float*>(P.out)[o + qq] = a4[qq];
+            else static_cast<bf16*>(P.out)[o + qq] = __float2bfloat16_rn(EPI == EPI_GELU ? gelu_tanh(a4[qq]) : a4[qq]);
+          }
+        }
+      }
+      epi_bar();
+      if (warp == 2 && lane == 0) {
+        // the last reader re-arms both counters for the next launch
+        if (atomicAdd(done, 1u) == static_cast<unsigned>(S - 1)) {
+          *arrive = 0u;
+          *done = 0u;
+          __threadfence();
+        }
+      }
+      tc_fence_before();
+    }
+    for (int u = u0; u < u1 && P.csplit == 1;) {
+      const int t = u / kch;
+      const int klo = u - t * kch;
+      const int khi = min(kch, klo + (u1 - u));
+      const int b = P.nbuf == 2 ? (seg & 1) : 0;
+      const uint32_t use = P.nbuf == 2 ? (seg >> 1) : seg;
+      const int tm = t / P.ntn, tn = t - tm * P.ntn;
+      const int m0 = tm * P.span;
+      const int mcount = min(P.span, P.M - m0);
+      const int nbase = tn * 2 * SK_BM + xi * SK_BM;
+      const int n = nbase + row;
+      const bool nok = n < P.N;
+      const bool whole = klo == 0 && khi == kch;
+      const float bv = (P.bias && nok && klo == 0) ? __bfloat162float(P.bias[n]) : 0.f;
+      const uint32_t tacc = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + b * acc_cols;
+      unsigned long long tw0 = P.dbg ? clock64() : 0;
+      if (warp == 2 && lane == 0) mbar_wait_sleep(&tfull_bar[b], use & 1);
+      epi_bar();
+      if (P.dbg) e_wait += clock64() - tw0;
+      tc_fence_after();
+
+      // segment mode: final epilogue (whole tile, or the k = 0 owner of a split
+      // tile after folding in the later pieces), red.add (split residual tile),
+      // or publish (a later piece of a split tile)
+      enum { FINAL = 0, RED = 1, PUB = 2 };
+      int mode = FINAL, plast = pair;
+      if (!whole) {
+        if (EPI == EPI_ACC_F32 && P.red) {
+          mode = RED;
+        } else if (klo > 0) {
+          mode = PUB;
+        } else {
+          plast = owner_of((t + 1) * kch - 1, P);
+          const unsigned long long tf0 = P.dbg ? clock64() : 0;
+          if (warp == 2 && lane == 0) {
+            for (int p = pair + 1; p <= plast; ++p) {
+              const unsigned* f = &P.flags[p * 2 + xi];
+              long long spins = 0;
+              while (ld_acquire(f) == 0u) {
+                __nanosleep(64);
+                if (++spins > (1ll << 26)) __trap();   // a lost partial: fail loudly, never hang
+              }
+            }
+          }
+          epi_bar();
+          if (P.dbg) e_flag += clock64() - tf0;
+        }
+      }
+      float* pub = P.part + static_cast<size_t>(pair * 2 + xi) * P.slot_elems;
+      const unsigned long long tb0 = P.dbg ? clock64() : 0;
+      // Each mode has its own loops (mixing them lets the compiler predicate the
+      // loads / atomics of other modes into the hot loop: 6x slower).  Stores
+      // go through a per-warp smem transpose so every lane moves 16 bytes
+      // (4 weight rows of one token): a 32x32 block is 8 vector accesses per
+      // lane instead of 32 scalar ones (tools/probes/store_probe.cu: 2.8x).
+      const bool vec = P.vec && nbase + SK_BM <= P.N;
+      for (int cb = 0; cb < mcount; cb += 32) {
+        uint32_t r[32];
+        const unsigned long long tl0 = P.dbg ? clock64() : 0;
+        tmem_ld32(tacc + cb, r);
+        const int ncol = min(32, mcount - cb);
+        if (P.dbg) e_ld += clock64() - tl0;
+        if ((EPI == EPI_QKV || EPI == EPI_ARGMAX || !vec) && mode == FINAL) {
+          // lane-per-weight-row epilogues (rotary partner / argmax reduce are lanes)
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) + bv;
+          for (int p = pair + 1; p <= plast; ++p) {
+            const float* slot = P.part + static_cast<size_t>(p * 2 + xi) * P.slot_elems + cb * SK_BM + row;
+            float q[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) q[j] = j < ncol ? slot[j * SK_BM] : 0.f;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += q[j];
+          }
+          if (EPI == EPI_QKV) {
+            epi_qkv(P, v, n, nok, m0 + cb, ncol, lane);
+          } else if (EPI == EPI_ARGMAX) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              unsigned long long key = (nok && j < ncol) ? argmax_key(v[j], P.index_base + n) : 0ull;
+#pragma unroll
+              for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
+                key = other > key ? other : key;
+              }
+              if (lane == 0 && key) atomicMax(&P.keys[m0 + cb + j], key);
+            }
+          } else if (nok) {
+            const size_t o0 = static_cast<size_t>(m0 + cb) * P.ldo + n;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              if (j >= ncol) continue;
+              const size_t o = o0 + static_cast<size_t>(j) * P.ldo;
+              if (EPI == EPI_STORE || EPI == EPI_GELU)
+                static_cast<bf16*>(P.out)[o] = __float2bfloat16_rn(EPI == EPI_GELU ? gelu_tanh(v[j]) : v[j]);
+              else if (EPI == EPI_ACC_F32)
+                static_cast<float*>(P.out)[o] += v[j];
+              else
+                static_cast<float*>(P.out)[o] = v[j];
+            }
+          }
+          continue;
+        }
+        if (!vec && mode == RED) {
+          if (nok) {
+            float* dst = static_cast<float*>(P.out) + static_cast<size_t>(m0 + cb) * P.ldo + n;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j < ncol) atomicAdd(dst + static_cast<size_t>(j) * P.ldo, __uint_as_float(r[j]) + bv);
+          }
+          continue;
+        }
+        // ---- staged: lane -> token j = (i*32+lane)/8, weight rows c4..c4+3
+        float* ws_ = stg + quarter * (32 * SK_STG_LD);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) ws_[j * SK_STG_LD + lane] = __uint_as_float(r[j]) + bv;
+        __syncwarp();
+        const int c4 = (lane & 7) * 4;
+        const int jb = lane >> 3;
+        const int nn = nbase + quarter * 32 + c4;
+        if (mode == PUB) {
+          float* dst = pub + static_cast<size_t>(cb) * SK_BM + quarter * 32 + c4;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int j = i * 4 + jb;
+            if (j < ncol)
+              *reinterpret_cast<float4*>(dst + j * SK_BM) = *reinterpret_cast<const float4*>(ws_ + j * SK_STG_LD + c4);
+          }
+        } else if (mode == RED) {
+          float* dst = static_cast<float*>(P.out) + static_cast<size_t>(m0 + cb) * P.ldo + nn;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int j = i * 4 + jb;
+            if (j < ncol) {
+              const float4 w = *reinterpret_cast<const float4*>(ws_ + j * SK_STG_LD + c4);
+              red_add_v4(dst + static_cast<size_t>(j) * P.ldo, w.x, w.y, w.z, w.w);
+            }
+          }
+        } else {
+          float4 w[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) w[i] = *reinterpret_cast<const float4*>(ws_ + (i * 4 + jb) * SK_STG_LD + c4);
+          for (int p = pair + 1; p <= plast; ++p) {
+            const float* slot = P.part + static_cast<size_t>(p * 2 + xi) * P.slot_elems +
+                                static_cast<size_t>(cb) * SK_BM + quarter * 32 + c4;
+            float4 q[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int j = i * 4 + jb;
+              q[i] = j < ncol ? *reinterpret_cast<const float4*>(slot + j * SK_BM) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              w[i].x += q[i].x; w[i].y += q[i].y; w[i].z += q[i].z; w[i].w += q[i].w;
+            }
+          }
+          if (EPI == EPI_STORE || EPI == EPI_GELU) {
+            bf16* dst = static_cast<bf16*>(P.out) + static_cast<size_t>(m0 + cb) * P.ldo + nn;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int j = i * 4 + jb;
+              if (j >= ncol) continue;
+              float4 x = w[i];
+              if (EPI == EPI_GELU) { x.x = gelu_tanh(x.x); x.y = gelu_tanh(x.y); x.z = gelu_tanh(x.z); x.w = gelu_tanh(x.w); }
+              __nv_bfloat162 lo = __floats2bfloat162_rn(x.x, x.y), hi = __floats2bfloat162_rn(x.z, x.w);
+              *reinterpret_cast<uint2*>(dst + static_cast<size_t>(j) * P.ldo) =
+                  make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+            }
+          } else if (EPI == EPI_ACC_F32) {
+            float* dst = static_cast<float*>(P.out) + static_cast<size_t>(m0 + cb) * P.ldo + nn;
+            float4 y[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int j = i * 4 + jb;
+              y[i] = j < ncol ? *reinterpret_cast<const float4*>(dst + static_cast<size_t>(j) * P.ldo) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int j = i * 4 + jb;
+              if (j < ncol)
+                *reinterpret_cast<float4*>(dst + static_cast<size_t>(j) * P.ldo) =
+                    make_float4(y[i].x + w[i].x, y[i].y + w[i].y, y[i].z + w[i].z, y[i].w + w[i].w);
+            }
+          } else {
+            float* dst = static_cast<float*>(P.out) + static_cast<size_t>(m0 + cb) * P.ldo + nn;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int j = i * 4 + jb;
+              if (j < ncol) *reinterpret_cast<float4*>(dst + static_cast<size_t>(j) * P.ldo) = w[i];
+            }
+          }
+        }
+        __syncwarp();
+      }
+      const unsigned long long tb1 = P.dbg ? clock64() : 0;
+      if (P.dbg) e_blk += tb1 - tb0;
+      if (mode == PUB) {
+        __threadfence();
+        epi_bar();
+        if (warp == 2 && lane == 0) st_release(&P.flags[pair * 2 + xi], 1u);
+      } else if (plast > pair) {
+        epi_bar();
+        if (warp == 2 && lane == 0)
+          for (int p = pair + 1; p <= plast; ++p) P.flags[p * 2 + xi] = 0u;   // re-arm
+      }
+      // this buffer may be overwritten by the next-but-one segment
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(&tempty_bar[b], prank);
+      if (P.dbg) e_post += clock64() - tb1;
+      u += khi - klo;
+      ++seg;
+    }
+    if (P.dbg && warp == 2 && lane == 0) {
+      unsigned long long g_end;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
+      P.dbg[4 * (4096 + blockIdx.x) + 0] = g_start;
+      P.dbg[4 * (4096 + blockIdx.x) + 1] = g_end;
+      P.dbg[4 * (4096 + blockIdx.x) + 2] = e_wait;
+      P.dbg[4 * (4096 + blockIdx.x) + 3] = clock64() - e_t0;
+      P.dbg[4 * (6144 + blockIdx.x) + 0] = e_flag;
+      P.dbg[4 * (6144 + blockIdx.x) + 1] = e_blk;
+      P.dbg[4 * (6144 + blockIdx.x) + 2] = e_post;
+      P.dbg[4 * (6144 + blockIdx.x) + 3] = e_ld;
+      P.dbg[4 * (4096 + blockIdx.x) + 3] = e_sts;
+    }
+  }
+
+  __syncwarp();
+  tc_fence_before();
+  __syncwarp();
+  cluster_sync_all();            // the pair's TMEM is freed jointly
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(P.ncols));
+  }
+}
+
+// ------------------------------------------------------------------ host side
+PFN_cuTensorMapEncodeTiled_v12000 g_encode_sk = nullptr;
+
+struct MapKey {
+  const void* ptr;
+  int dtype;               // 0 bf16, 1 f32
+  uint64_t rows, cols, ld_bytes;
+  uint32_t box_c, box_r;
+  int swz;
+  bool operator<(const MapKey& o) const {
+    return std::tie(ptr, dtype, rows, cols, ld_bytes, box_c, box_r, swz) <
+           std::tie(o.ptr, o.dtype, o.rows, o.cols, o.ld_bytes, o.box_c, o.box_r, o.swz);
+  }
+};
+std::map<MapKey, CUtensorMap> g_sk_maps;
+
+// 2-D row-major tensor [rows][cols] (row stride ld_bytes), box [box_r][box_c]
+bool sk_map(const MapKey& key, CUtensorMap** out) {
+  auto it = g_sk_maps.find(key);
+  if (it != g_sk_maps.end()) {
+    *out = &it->second;
+    return true;
+  }
+  if (!g_encode_sk) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
+      g_sk_err = "cuTensorMapEncodeTiled entry point unavailable";
+      return false;
+    }
+    g_encode_sk = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  CUtensorMap map;
+  cuuint64_t dims[2] = {key.cols, key.rows};
+  cuuint64_t strides[1] = {key.ld_bytes};
+  cuuint32_t box[2] = {key.box_c, key.box_r};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode_sk(&map, key.dtype ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                           const_cast<void*>(key.ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           key.swz ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char buf[160];
+    snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled failed (%d) rows=%llu cols=%llu", (int)r,
+             (unsigned long long)key.rows, (unsigned long long)key.cols);
+    g_sk_err = buf;
+    return false;
+  }
+  *out = &(g_sk_maps[key] = map);
+  return true;
+}
+
+}  // namespace
+
+size_t sk_workspace_bytes() {
+  return (size_t)SK_MAX_PAIRS * 2 * SK_MAX_SPAN * SK_BM * 4 + SK_MAX_PAIRS * 6 * 4 + 256;
+}
+
+const char* sk_last_error() { return g_sk_err.c_str(); }
+void sk_set_debug(unsigned long long* p) { g_sk_dbg = p; }
+
+int sk_init(void* base, size_t bytes) {
+  if (bytes < sk_workspace_bytes()) {
+    g_sk_err = "stream-K workspace too small";
+    return -1;
+  }
+  // flags live after the partial slots and must start at zero (self-resetting after)
+  char* f = static_cast<char*>(base) + (size_t)SK_MAX_PAIRS * 2 * SK_MAX_SPAN * SK_BM * 4;
+  if (cudaMemset(f, 0, SK_MAX_PAIRS * 6 * 4) != cudaSuccess) {
+    g_sk_err = "stream-K flag reset failed";
+    return -1;
+  }
+  return 0;
+}
+
+cudaError_t sk_rearm(void* base, cudaStream_t s) {
+  char* f = static_cast<char*>(base) + (size_t)SK_MAX_PAIRS * 2 * SK_MAX_SPAN * SK_BM * 4;
+  return cudaMemsetAsync(f, 0, SK_MAX_PAIRS * 6 * 4, s);
+}
+
+int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
+  if (a.M <= 0 || a.N <= 0) return 0;
+  if (a.dtype != FL_DTYPE_BF16 || a.K % SK_BK || a.ldx % 8) {
+    g_sk_err = "tensor-core GEMM needs bf16, K % 64 == 0 and 16-byte aligned rows";
+    return -1;
+  }
+  static bool configured = false;
+  if (!configured) {
+    for (auto k : {k_gemm_sk<EPI_STORE>, k_gemm_sk<EPI_GELU>, k_gemm_sk<EPI_ACC_F32>, k_gemm_sk<EPI_STORE_F32>,
+                   k_gemm_sk<EPI_ARGMAX>, k_gemm_sk<EPI_QKV>})
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SK_RING_BUDGET + 1024);
+    configured = true;
+  }
+  SkParams P{};
+  P.M = a.M;
+  P.N = a.N;
+  P.ldo = a.ldo;
+  P.epi = a.epi;
+  P.kch = a.K / SK_BK;
+  P.ntn = (a.N + 2 * SK_BM - 1) / (2 * SK_BM);
+  // token tiling: the whole window per tile when it fits (<= 512 columns)
+  const int mt = a.M <= 256 ? 1 : 2;
+  const int ntm = (a.M + SK_MAX_SPAN - 1) / SK_MAX_SPAN;
+  const int per = (a.M + ntm - 1) / ntm;
+  P.mt = mt;
+  P.bn = (((per + mt - 1) / mt) + 15) / 16 * 16;
+  if (ntm > 1) P.bn = (P.bn + 31) / 32 * 32;   // 32-token store boxes never cross token tiles
+  P.span = P.mt * P.bn;
+  const int stage = SK_A_BYTES + P.mt * (P.bn / 2) * SK_BK * 2;
+  P.stages = SK_RING_BUDGET / stage;
+  if (P.stages > SK_MAXST) P.stages = SK_MAXST;
+  static const int force_st = getenv("FL_SK_STAGES") ? atoi(getenv("FL_SK_STAGES")) : 0;
+  if (force_st > 1 && force_st < P.stages) P.stages = force_st;
+  P.nbuf = P.span <= 256 ? 2 : 1;
+  const int cols = P.nbuf * P.span;
+  P.ncols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
+  P.units = ntm * P.ntn * P.kch;
+  // every pair streams >= 4 chunks (amortise the split-tile fix-up)
+  int npairs = num_sms / 2;
+  if (npairs > SK_MAX_PAIRS) npairs = SK_MAX_PAIRS;
+  // wide windows (tensor-bound): whole or evenly split tiles, so no pair
+  // stalls its MMA on a mid-range epilogue (the 320-column accumulator cannot
+  // be double-buffered); narrow windows (HBM-bound): every SM streams
+  const int tiles = ntm * P.ntn;
+  if (a.M >= 96 && tiles <= npairs) npairs = tiles * (npairs / tiles);
+  static const int force_pairs = getenv("FL_SK_PAIRS") ? atoi(getenv("FL_SK_PAIRS")) : 0;
+  if (force_pairs > 0 && force_pairs < npairs) npairs = force_pairs;
+  // cluster split-K (DSMEM reduction) for evenly split tiles of the direct epilogues
+  P.csplit = 1;
+  static const int no_csplit = getenv("FL_SK_NO_CSPLIT") != nullptr;
+  if (!no_csplit && a.M >= 96 && tiles <= npairs && npairs / tiles >= 2 &&
+      (a.epi == EPI_ACC_F32 || a.epi == EPI_STORE_F32 || a.epi == EPI_STORE || a.epi == EPI_GELU)) {
+    P.csplit = npairs / tiles > 4 ? 4 : npairs / tiles;
+    npairs = tiles * P.csplit;
+  }
+  const int cap = (P.units + 3) / 4;
+  if (npairs > cap && P.csplit == 1) npairs = cap;
+  if (npairs < 1) npairs = 1;
+  P.npairs = npairs;
+  P.bias = static_cast<const bf16*>(a.bias);
+  P.out = a.out;
+  P.keys = a.keys;
+  P.index_base = a.index_base;
+  P.part = static_cast<float*>(ws);
+  P.slot_elems = SK_MAX_SPAN * SK_BM;
+  P.flags = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + (size_t)SK_MAX_PAIRS * 2 * SK_MAX_SPAN * SK_BM * 4);
+  P.rope = a.rope;
+  P.dbg = g_sk_dbg;
+  static const int use_red = getenv("FL_SK_RED") ? atoi(getenv("FL_SK_RED")) : 0;
+  P.red = use_red;
+  P.vec = (a.ldo % 4 == 0 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0) ? 1 : 0;
+  CUtensorMap *mw, *mx;
+  if (!sk_map({a.w, 0, (uint64_t)a.N, (uint64_t)a.K, (uint64_t)a.K * 2, SK_BK, SK_BM, 1}, &mw)) return -1;
+  if (!sk_map({a.x, 0, (uint64_t)(a.mcap > a.M ? a.mcap : a.M), (uint64_t)a.K, (uint64_t)a.ldx * 2, SK_BK,
+               (uint32_t)(P.bn / 2), 1}, &mx))
+    return -1;
+  const int smem = P.stages * stage + 1024;
+  void (*kern)(const CUtensorMap, const CUtensorMap, const SkParams) = nullptr;
+  switch (a.epi) {
+    case EPI_STORE: kern = k_gemm_sk<EPI_STORE>; break;
+    case EPI_GELU: kern = k_gemm_sk<EPI_GELU>; break;
+    case EPI_ACC_F32: kern = k_gemm_sk<EPI_ACC_F32>; break;
+    case EPI_STORE_F32: kern = k_gemm_sk<EPI_STORE_F32>; break;
+    case EPI_ARGMAX: kern = k_gemm_sk<EPI_ARGMAX>; break;
+    case EPI_QKV: kern = k_gemm_sk<EPI_QKV>; break;
+    default: g_sk_err = "unknown epilogue"; return -1;
+  }
+  cudaError_t e = launch_k(kern, dim3(2 * npairs), dim3(SK_THREADS), smem, s, dim3(2, 1, 1), *mw, *mx, P);
+  if (e != cudaSuccess) {
+    char buf[256];
+    snprintf(buf, sizeof buf, "k_gemm_sk launch (pairs %d smem %d stages %d bn %d mt %d): %s", npairs, smem,
+             P.stages, P.bn, P.mt, cudaGetErrorString(e));
+    g_sk_err = buf;
+    return -1;
+  }
+  return 0;
+}
+
+}  // namespace fl

@@ -709,10 +709,10 @@ int launch_tc(const GemmArgs& a, const CUtensorMap* mw, const CUtensorMap* mx, i
 
 }  // namespace
 
-size_t tc_workspace_bytes(int, int) { return 256; }
+size_t tc_workspace_bytes(int, int) { return sk_workspace_bytes(); }
 
-const char* tc_last_error() { return g_tc_err.c_str(); }
-void tc_set_debug(unsigned long long* p) { g_dbg = p; }
+const char* tc_last_error() { return g_tc_err.empty() ? sk_last_error() : g_tc_err.c_str(); }
+void tc_set_debug(unsigned long long* p) { g_dbg = p; sk_set_debug(p); }
 
 int tc_init(TcWorkspace* ws, void* base, size_t bytes) {
   if (!g_encode) {
@@ -727,6 +727,10 @@ int tc_init(TcWorkspace* ws, void* base, size_t bytes) {
   }
   ws->base = base;
   ws->bytes = bytes;
+  if (sk_init(base, bytes)) {
+    g_tc_err = sk_last_error();
+    return -1;
+  }
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&ws->num_sms, cudaDevAttrMultiProcessorCount, dev);
@@ -745,6 +749,10 @@ int gemm_tc(TcWorkspace* ws, const GemmArgs& a, cudaStream_t s) {
     g_tc_err = "tensor-core GEMM needs bf16, K % 64 == 0 and 16-byte aligned rows";
     return -1;
   }
+  // default: the persistent stream-K pair kernel (gemm_sk.cu); FL_GEMM_LEGACY=1
+  // selects the per-tile cluster-split kernel below (kept for comparison)
+  static const bool legacy = getenv("FL_GEMM_LEGACY") != nullptr;
+  if (!legacy) return gemm_sk(ws->base, ws->num_sms, a, s);
   MapCache& cache = *static_cast<MapCache*>(ws->maps);
   // Token tiling: the whole window in one CTA when it fits TMEM (MT sub-tiles
   // of <= 256 columns, MT*bn <= 512), so each weight byte is read once.

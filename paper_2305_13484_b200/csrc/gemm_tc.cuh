@@ -30,4 +30,15 @@ void tc_set_debug(unsigned long long* p);
 // EPI_QKV returns 2 when it fell back to a plain store into a.out.
 int gemm_tc(TcWorkspace* ws, const GemmArgs& a, cudaStream_t s);
 
+// Persistent stream-K 2-SM GEMM (gemm_sk.cu), the default tensor-core path;
+// workspace = fp32 partial slots + self-resetting flags (zeroed by sk_init).
+constexpr int SK_MAX_PAIRS = 80;
+constexpr int SK_MAX_SPAN = 512;   // tokens per token tile
+size_t sk_workspace_bytes();
+int sk_init(void* base, size_t bytes);
+cudaError_t sk_rearm(void* base, cudaStream_t s);
+int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s);
+const char* sk_last_error();
+void sk_set_debug(unsigned long long* p);
+
 }  // namespace fl

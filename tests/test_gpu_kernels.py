@@ -37,7 +37,9 @@ def _gemm(x, w, bias, out, epi, use_tc, dtype):
 
 SHAPES = [(1, 768, 768), (7, 2304, 768), (16, 512, 1024), (55, 3072, 768), (64, 768, 3072),
           (100, 50257, 768), (129, 1536, 4096), (256, 4096, 512), (300, 1000, 256), (17, 128, 64),
-          (350, 1536, 4096), (512, 768, 768), (700, 1024, 512), (1000, 384, 256)]
+          (350, 1536, 4096), (512, 768, 768), (700, 1024, 512), (1000, 384, 256),
+          # GPT-J 6B projection shapes at a saturated window (stream-K splits tiles)
+          (320, 12288, 4096), (262, 4096, 16384), (96, 16384, 4096), (5, 4096, 4096)]
 
 
 @pytest.mark.parametrize("M,N,K", SHAPES)

@@ -5,6 +5,7 @@
 import ctypes as C
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ.setdefault("FL_GEMM_NO_REARM", "1")   # same workspace every call: flags self-reset
 import torch
 from paper_2305_13484_b200 import _lib
 
@@ -16,7 +17,7 @@ shapes = [(48, 2304, 768), (48, 768, 768), (48, 3072, 768), (48, 768, 3072), (48
 if len(sys.argv) > 1:
     shapes = [tuple(map(int, a.split("x"))) for a in sys.argv[1:]]
 s = torch.cuda.Stream()
-dbg = torch.zeros(4 * 4096, dtype=torch.int64, device="cuda")
+dbg = torch.zeros(4 * 8192, dtype=torch.int64, device="cuda")
 for M, N, K in shapes:
     x = torch.randn(M, K, device="cuda").bfloat16()
     w = (torch.randn(N, K, device="cuda") * 0.02).bfloat16()
@@ -47,6 +48,22 @@ for M, N, K in shapes:
     if os.environ.get("GEMM_DBG"):
         dbg.zero_(); lib.fl_gemm_debug(C.c_void_p(dbg.data_ptr())); ours(); torch.cuda.synchronize()
         lib.fl_gemm_debug(None)
-        d = dbg.view(-1, 4).cpu().double(); d = d[d[:, 3] > 0]
-        print(f"   CTAs {len(d)}: producer waits {100*d[:,0].sum()/d[:,1].sum():.0f}% of {d[:,1].mean():.0f} clk, "
-              f"mma waits {100*d[:,2].sum()/d[:,3].sum():.0f}% of {d[:,3].mean():.0f} clk")
+        d = dbg.view(-1, 4).cpu().double()
+        g = int((d[:2048, 1] > 0).sum().item() + (d[:2048, 3] > 0).sum().item() // 1)
+        p = d[:2048][d[:2048, 1] > 0]
+        lead = d[:2048, 3] > 0
+        m = d[:2048][lead]
+        te = d[2048:4096, 0][lead]
+        e = d[4096:6144]
+        ok = e[:, 1] > 0
+        e = e[ok]
+        ef = d[6144:8192, 0][ok]
+        eb = d[6144:8192, 1][ok]
+        ep = d[6144:8192, 2][ok]
+        el = d[6144:8192, 3][ok]
+        t0 = e[:, 0].min()
+        print(f"   producer: {len(p)} CTAs, waits {100*p[:,0].sum()/max(p[:,1].sum(),1):.0f}% of {p[:,1].mean():.0f} clk;"
+              f" mma: {len(m)} CTAs, full-waits {100*m[:,2].sum()/max(m[:,3].sum(),1):.0f}%, tmem-waits "
+              f"{100*te.sum()/max(m[:,3].sum(),1):.0f}% of {m[:,3].mean():.0f} clk", flush=True)
+        print(f"   epilogue: start spread {(e[:,0].max()-t0)/1e3:.1f} us, end {(e[:,1].min()-t0)/1e3:.1f}..{(e[:,1].max()-t0)/1e3:.1f} us;"
+              f" tfull-wait {e[:,2].mean():.0f} clk, flag-wait {ef.mean():.0f} (max {ef.max():.0f}) clk, blocks {eb.mean():.0f} (ldtm {el.mean():.0f}, ldtm+sts {e[:,3].mean():.0f}) post {ep.mean():.0f}", flush=True)
