@@ -103,6 +103,22 @@ FL_DEV void tma_load_pair(const CUtensorMap* map, uint64_t* bar, void* dst, int 
       "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1)
       : "memory");
 }
+// 2-SM load multicast to the CTAs of `mask` (same smem offset in each);
+// complete_tx lands on each destination pair's leader barrier
+FL_DEV void tma_load_pair_mc(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1, uint16_t mask) {
+  const uint32_t leader_bar = smem_u32(bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+FL_DEV void l2_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
 FL_DEV void mma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -188,18 +204,22 @@ struct SkParams {
   int slot_elems;   // floats per (pair, half) slot
   int vec;          // out rows 16-byte aligned: vector stores
   int red;          // EPI_ACC_F32 split tiles: red.add pieces (else owner fix-up)
-  int csplit;       // >1: the S pairs of a cluster split one tile's K, DSMEM reduction
+  int csplit;       // >1: tile K split evenly over S pairs, spread reduction
+  int l2_ahead;     // weight chunks prefetched into L2 beyond the ring
+  int cn;           // pairs per cluster: token slices sharing multicast weight tiles
+  int nclus;        // clusters (work ranges)
+  int slice;        // tokens per pair (mt * bn)
   RopeArgs rope;
   unsigned long long* dbg;   // diagnostics: per CTA [prod wait, prod total, mma wait, mma total]
 };
 
-// unit range of pair p: [p*U/P, (p+1)*U/P)
-FL_DEV int range_lo(int p, const SkParams& P) {
-  return static_cast<int>((static_cast<long long>(p) * P.units) / P.npairs);
+// unit range of cluster q: [q*U/Q, (q+1)*U/Q)
+FL_DEV int range_lo(int q, const SkParams& P) {
+  return static_cast<int>((static_cast<long long>(q) * P.units) / P.nclus);
 }
-// the pair whose range holds unit x
+// the cluster whose range holds unit x
 FL_DEV int owner_of(int x, const SkParams& P) {
-  return static_cast<int>(((static_cast<long long>(x) + 1) * P.npairs + P.units - 1) / P.units) - 1;
+  return static_cast<int>(((static_cast<long long>(x) + 1) * P.nclus + P.units - 1) / P.units) - 1;
 }
 
 // EPI_QKV epilogue of 32 token columns [mbase, mbase+ncol) of this thread's
@@ -263,22 +283,30 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
   unsigned long long g_start = 0;
   if (P.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
   const int xi = blockIdx.x & 1;                 // position in the pair (cluster rank)
-  const int pair = blockIdx.x >> 1;
+  const int pair = blockIdx.x >> 1;              // global pair id = clu * CN + c
   const bool leader = xi == 0;
   const uint32_t crank = cluster_ctarank();
   const uint32_t prank = crank & ~1u;            // the pair's leader in the cluster
   const uint16_t pmask = static_cast<uint16_t>(3u << prank);
+  const int CN = P.cn;
+  const int c = static_cast<int>(crank >> 1);    // token slice of this pair in the cluster
+  const int clu = pair / CN;
+  // weight rows are multicast to the same-half CTA of every pair of the cluster
+  uint16_t wmask = 0;
+  for (int q = 0; q < CN; ++q) wmask |= static_cast<uint16_t>(1u << (2 * q + xi));
+  const uint16_t allmask = static_cast<uint16_t>((1u << (2 * CN)) - 1u);
+  const int wrows = SK_BM / CN;                  // weight rows this CTA loads per chunk
   const int XB = (P.bn / 2) * SK_BK * 2;         // this CTA's half of a token sub-tile
   const int STAGE = SK_A_BYTES + P.mt * XB;
   const int stages = P.stages, kch = P.kch;
-  const int u0 = range_lo(pair, P), u1 = range_lo(pair + 1, P);
+  const int u0 = range_lo(clu, P), u1 = range_lo(clu + 1, P);
 
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_w)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_x)) : "memory");
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full_bar[s], 1 + P.mt);   // weight producer + one per token sub-tile
-      mbar_init(&empty_bar[s], 1);
+      mbar_init(&empty_bar[s], CN);          // every pair's MMAs consumed the stage
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull_bar[b], 1);
@@ -308,7 +336,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         const int t = u / kch;
         k = (u - t * kch) * SK_BK;
         const int tm = t / P.ntn, tn = t - tm * P.ntn;
-        m0 = tm * P.span;
+        m0 = tm * P.span + c * P.slice;          // this pair's token slice
         n0 = tn * 2 * SK_BM + xi * SK_BM;
       };
       const uint32_t my_tx = 2u * (role < 0 ? SK_A_BYTES : XB);   // both CTAs' bytes
@@ -316,15 +344,26 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         int m0, n0, k;
         coords(u, m0, n0, k);
         if (leader) mbar_expect_tx(&full_bar[st], my_tx);
-        if (role < 0)
+        if (role < 0 && CN == 1)
           tma_load_pair(&tma_w, &full_bar[st], smem + st * STAGE, k, n0);
+        else if (role < 0)
+          tma_load_pair_mc(&tma_w, &full_bar[st], smem + st * STAGE + c * wrows * 128, k, n0 + c * wrows, wmask);
         else
           tma_load_pair(&tma_x, &full_bar[st], smem + st * STAGE + SK_A_BYTES + role * XB, k,
                         m0 + role * P.bn + xi * (P.bn / 2));
       };
+      // weights are also prefetched into L2 `D` chunks beyond the ring: the
+      // ring alone (~180 KB at wide windows) cannot cover HBM latency
+      const int D = role < 0 ? P.l2_ahead : 0;
+      auto prefetch = [&](int u) {
+        int m0, n0, k;
+        coords(u, m0, n0, k);
+        l2_prefetch_2d(&tma_w, k, n0 + c * wrows);
+      };
       const int pre = min(u1 - u0, stages);
       if (role >= 0) pdl_wait();            // activations are the predecessor's output
       for (int i = 0; i < pre; ++i) issue(u0 + i, i);   // weights stream ahead of the wait
+      for (int u = u0 + pre; u < min(u1, u0 + pre + D); ++u) prefetch(u);
       int s = pre % stages;
       uint32_t ph = pre == stages ? 1u : 0u;
       unsigned long long waited = 0, t_start = clock64();
@@ -333,6 +372,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         mbar_wait(&empty_bar[s], ph ^ 1);
         if (P.dbg) waited += clock64() - tw;
         issue(u, s);
+        if (D && u + D < u1) prefetch(u + D);
         if (++s == stages) { s = 0; ph ^= 1; }
       }
       if (P.dbg && role < 0) {
@@ -370,7 +410,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
             for (int kk = 0; kk < SK_BK / 16; ++kk)
               mma_pair(acc + j * P.bn, ad + 2 * kk, bd + 2 * kk, idesc, (c > klo) | kk);
           }
-          commit_pair(&empty_bar[s], pmask);
+          commit_pair(&empty_bar[s], CN == 1 ? pmask : allmask);
           if (++s == stages) { s = 0; ph ^= 1; }
         }
         commit_pair(&tfull_bar[b], pmask);
@@ -396,10 +436,10 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       // [s, s+1) * mcount / S over the S slots and runs the epilogue -- the
       // fix-up is spread over the S pairs instead of serialised in one owner.
       const int S = P.csplit;
-      const int t = u0 / kch, piece = pair - t * S;
+      const int t = u0 / kch, piece = clu - t * S;
       const int tm = t / P.ntn, tn = t - tm * P.ntn;
-      const int m0 = tm * P.span;
-      const int mcount = min(P.span, P.M - m0);
+      const int m0 = tm * P.span + c * P.slice;   // this pair's token slice
+      const int mcount = min(P.slice, P.M - m0);
       const int nbase = tn * 2 * SK_BM + xi * SK_BM;
       const uint32_t tacc = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
       if (warp == 2 && lane == 0) mbar_wait_sleep(&tfull_bar[0], 0);
@@ -426,7 +466,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       }
       __threadfence();
       epi_bar();
-      unsigned* arrive = P.flags + 2 * SK_MAX_PAIRS + (t * 2 + xi);
+      unsigned* arrive = P.flags + 2 * SK_MAX_PAIRS + ((t * CN + c) * 2 + xi);
       unsigned* done = arrive + 2 * SK_MAX_PAIRS;
       if (warp == 2 && lane == 0) {
         atomicAdd(arrive, 1u);
@@ -450,7 +490,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
 #pragma unroll
         for (int p = 0; p < 4; ++p)
           if (p < S)
-            q[p] = *reinterpret_cast<const float4*>(P.part + static_cast<size_t>((t * S + p) * 2 + xi) * P.slot_elems +
+            q[p] = *reinterpret_cast<const float4*>(P.part + static_cast<size_t>(((t * S + p) * CN + c) * 2 + xi) * P.slot_elems +
                                                     static_cast<size_t>(tok) * SK_BM + rrow);
 #pragma unroll
         for (int p = 0; p < 4; ++p)
@@ -498,8 +538,8 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       const int b = P.nbuf == 2 ? (seg & 1) : 0;
       const uint32_t use = P.nbuf == 2 ? (seg >> 1) : seg;
       const int tm = t / P.ntn, tn = t - tm * P.ntn;
-      const int m0 = tm * P.span;
-      const int mcount = min(P.span, P.M - m0);
+      const int m0 = tm * P.span + c * P.slice;   // this pair's token slice
+      const int mcount = min(P.slice, P.M - m0);
       const int nbase = tn * 2 * SK_BM + xi * SK_BM;
       const int n = nbase + row;
       const bool nok = n < P.N;
@@ -516,7 +556,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       // tile after folding in the later pieces), red.add (split residual tile),
       // or publish (a later piece of a split tile)
       enum { FINAL = 0, RED = 1, PUB = 2 };
-      int mode = FINAL, plast = pair;
+      int mode = FINAL, plast = clu;      // plast: last cluster holding a piece
       if (!whole) {
         if (EPI == EPI_ACC_F32 && P.red) {
           mode = RED;
@@ -526,8 +566,8 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
           plast = owner_of((t + 1) * kch - 1, P);
           const unsigned long long tf0 = P.dbg ? clock64() : 0;
           if (warp == 2 && lane == 0) {
-            for (int p = pair + 1; p <= plast; ++p) {
-              const unsigned* f = &P.flags[p * 2 + xi];
+            for (int q = clu + 1; q <= plast; ++q) {
+              const unsigned* f = &P.flags[(q * CN + c) * 2 + xi];
               long long spins = 0;
               while (ld_acquire(f) == 0u) {
                 __nanosleep(64);
@@ -558,7 +598,8 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
           float v[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) + bv;
-          for (int p = pair + 1; p <= plast; ++p) {
+          for (int qc = clu + 1; qc <= plast; ++qc) {
+            const int p = qc * CN + c;
             const float* slot = P.part + static_cast<size_t>(p * 2 + xi) * P.slot_elems + cb * SK_BM + row;
             float q[32];
 #pragma unroll
@@ -634,7 +675,8 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
           float4 w[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) w[i] = *reinterpret_cast<const float4*>(ws_ + (i * 4 + jb) * SK_STG_LD + c4);
-          for (int p = pair + 1; p <= plast; ++p) {
+          for (int qc = clu + 1; qc <= plast; ++qc) {
+            const int p = qc * CN + c;
             const float* slot = P.part + static_cast<size_t>(p * 2 + xi) * P.slot_elems +
                                 static_cast<size_t>(cb) * SK_BM + quarter * 32 + c4;
             float4 q[8];
@@ -692,10 +734,10 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         __threadfence();
         epi_bar();
         if (warp == 2 && lane == 0) st_release(&P.flags[pair * 2 + xi], 1u);
-      } else if (plast > pair) {
+      } else if (plast > clu) {
         epi_bar();
         if (warp == 2 && lane == 0)
-          for (int p = pair + 1; p <= plast; ++p) P.flags[p * 2 + xi] = 0u;   // re-arm
+          for (int q = clu + 1; q <= plast; ++q) P.flags[(q * CN + c) * 2 + xi] = 0u;   // re-arm
       }
       // this buffer may be overwritten by the next-but-one segment
       tc_fence_before();
@@ -830,45 +872,53 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   P.epi = a.epi;
   P.kch = a.K / SK_BK;
   P.ntn = (a.N + 2 * SK_BM - 1) / (2 * SK_BM);
-  // token tiling: the whole window per tile when it fits (<= 512 columns)
-  const int mt = a.M <= 256 ? 1 : 2;
-  const int ntm = (a.M + SK_MAX_SPAN - 1) / SK_MAX_SPAN;
-  const int per = (a.M + ntm - 1) / ntm;
+  // CN pairs per cluster split the token tile into slices and share (multicast)
+  // every weight chunk; CN = 1: the whole window (<= 512 tokens) in one pair
+  static const int force_cn = getenv("FL_SK_CN") ? atoi(getenv("FL_SK_CN")) : 0;
+  int CN = 1;
+  if (force_cn == 1 || force_cn == 2 || force_cn == 4) CN = force_cn;
+  const int smax = CN == 1 ? SK_MAX_SPAN : 256;           // tokens per pair
+  const int ntm = (a.M + CN * smax - 1) / (CN * smax);
+  const int per = (a.M + ntm - 1) / ntm;                   // tokens per token tile
+  const int slice0 = (per + CN - 1) / CN;
+  const int mt = slice0 <= 256 ? 1 : 2;
   P.mt = mt;
-  P.bn = (((per + mt - 1) / mt) + 15) / 16 * 16;
-  if (ntm > 1) P.bn = (P.bn + 31) / 32 * 32;   // 32-token store boxes never cross token tiles
-  P.span = P.mt * P.bn;
+  P.bn = (((slice0 + mt - 1) / mt) + 15) / 16 * 16;
+  if (ntm > 1 || CN > 1) P.bn = (P.bn + 31) / 32 * 32;     // 32-token epilogue blocks never cross slices
+  P.slice = P.mt * P.bn;
+  P.span = CN * P.slice;
+  P.cn = CN;
   const int stage = SK_A_BYTES + P.mt * (P.bn / 2) * SK_BK * 2;
   P.stages = SK_RING_BUDGET / stage;
   if (P.stages > SK_MAXST) P.stages = SK_MAXST;
   static const int force_st = getenv("FL_SK_STAGES") ? atoi(getenv("FL_SK_STAGES")) : 0;
   if (force_st > 1 && force_st < P.stages) P.stages = force_st;
-  P.nbuf = P.span <= 256 ? 2 : 1;
-  const int cols = P.nbuf * P.span;
+  P.nbuf = P.slice <= 256 ? 2 : 1;
+  const int cols = P.nbuf * P.slice;
   P.ncols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
   P.units = ntm * P.ntn * P.kch;
-  // every pair streams >= 4 chunks (amortise the split-tile fix-up)
-  int npairs = num_sms / 2;
-  if (npairs > SK_MAX_PAIRS) npairs = SK_MAX_PAIRS;
+  int nclus = num_sms / (2 * CN);
+  if (nclus * CN > SK_MAX_PAIRS) nclus = SK_MAX_PAIRS / CN;
   // wide windows (tensor-bound): whole or evenly split tiles, so no pair
-  // stalls its MMA on a mid-range epilogue (the 320-column accumulator cannot
-  // be double-buffered); narrow windows (HBM-bound): every SM streams
+  // stalls its MMA on a mid-range epilogue; narrow windows (HBM-bound): every
+  // SM streams an equal share (stream-K)
   const int tiles = ntm * P.ntn;
-  if (a.M >= 96 && tiles <= npairs) npairs = tiles * (npairs / tiles);
+  if (a.M >= 96 && tiles <= nclus) nclus = tiles * (nclus / tiles);
   static const int force_pairs = getenv("FL_SK_PAIRS") ? atoi(getenv("FL_SK_PAIRS")) : 0;
-  if (force_pairs > 0 && force_pairs < npairs) npairs = force_pairs;
-  // cluster split-K (DSMEM reduction) for evenly split tiles of the direct epilogues
+  if (force_pairs > 0 && force_pairs / CN < nclus) nclus = force_pairs / CN;
+  // evenly split tiles of the direct epilogues: spread reduction (no owner)
   P.csplit = 1;
   static const int no_csplit = getenv("FL_SK_NO_CSPLIT") != nullptr;
-  if (!no_csplit && a.M >= 96 && tiles <= npairs && npairs / tiles >= 2 &&
+  if (!no_csplit && a.M >= 96 && tiles <= nclus && nclus / tiles >= 2 &&
       (a.epi == EPI_ACC_F32 || a.epi == EPI_STORE_F32 || a.epi == EPI_STORE || a.epi == EPI_GELU)) {
-    P.csplit = npairs / tiles > 4 ? 4 : npairs / tiles;
-    npairs = tiles * P.csplit;
+    P.csplit = nclus / tiles > 4 ? 4 : nclus / tiles;
+    nclus = tiles * P.csplit;
   }
-  const int cap = (P.units + 3) / 4;
-  if (npairs > cap && P.csplit == 1) npairs = cap;
-  if (npairs < 1) npairs = 1;
-  P.npairs = npairs;
+  const int cap = (P.units + 3) / 4;                       // >= 4 chunks per range
+  if (nclus > cap && P.csplit == 1) nclus = cap;
+  if (nclus < 1) nclus = 1;
+  P.nclus = nclus;
+  P.npairs = nclus * CN;
   P.bias = static_cast<const bf16*>(a.bias);
   P.out = a.out;
   P.keys = a.keys;
@@ -880,9 +930,12 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   P.dbg = g_sk_dbg;
   static const int use_red = getenv("FL_SK_RED") ? atoi(getenv("FL_SK_RED")) : 0;
   P.red = use_red;
+  static const int l2a = getenv("FL_SK_L2AHEAD") ? atoi(getenv("FL_SK_L2AHEAD")) : 8;
+  P.l2_ahead = l2a;
   P.vec = (a.ldo % 4 == 0 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0) ? 1 : 0;
   CUtensorMap *mw, *mx;
-  if (!sk_map({a.w, 0, (uint64_t)a.N, (uint64_t)a.K, (uint64_t)a.K * 2, SK_BK, SK_BM, 1}, &mw)) return -1;
+  if (!sk_map({a.w, 0, (uint64_t)a.N, (uint64_t)a.K, (uint64_t)a.K * 2, SK_BK, (uint32_t)(SK_BM / CN), 1}, &mw))
+    return -1;
   if (!sk_map({a.x, 0, (uint64_t)(a.mcap > a.M ? a.mcap : a.M), (uint64_t)a.K, (uint64_t)a.ldx * 2, SK_BK,
                (uint32_t)(P.bn / 2), 1}, &mx))
     return -1;
@@ -897,10 +950,10 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
     case EPI_QKV: kern = k_gemm_sk<EPI_QKV>; break;
     default: g_sk_err = "unknown epilogue"; return -1;
   }
-  cudaError_t e = launch_k(kern, dim3(2 * npairs), dim3(SK_THREADS), smem, s, dim3(2, 1, 1), *mw, *mx, P);
+  cudaError_t e = launch_k(kern, dim3(2 * P.npairs), dim3(SK_THREADS), smem, s, dim3(2 * CN, 1, 1), *mw, *mx, P);
   if (e != cudaSuccess) {
     char buf[256];
-    snprintf(buf, sizeof buf, "k_gemm_sk launch (pairs %d smem %d stages %d bn %d mt %d): %s", npairs, smem,
+    snprintf(buf, sizeof buf, "k_gemm_sk launch (pairs %d smem %d stages %d bn %d mt %d): %s", P.npairs, smem,
              P.stages, P.bn, P.mt, cudaGetErrorString(e));
     g_sk_err = buf;
     return -1;

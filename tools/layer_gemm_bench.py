@@ -1,0 +1,87 @@
+"""GEMM-only replay of one fused GPT-J decode step with cold weights.
+
+    python tools/layer_gemm_bench.py [M ...]
+
+28 layers x (QKV store, attn-out residual-add, FFN-up GELU, FFN-down
+residual-add) + the LM head with the fused greedy argmax, each layer with its
+own weights (11.3 GB: every weight byte comes from HBM, as in the real step),
+captured in one CUDA graph; ours (C-ABI fl_gemm) vs torch.matmul (cuBLAS,
+plain GEMMs without the epilogues).
+"""
+import ctypes as C
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ.setdefault("FL_GEMM_NO_REARM", "1")
+import torch
+from paper_2305_13484_b200 import _lib
+
+lib = _lib.load()
+ws = torch.empty(lib.fl_gemm_workspace_bytes(), dtype=torch.uint8, device="cuda")
+L, d, F, V = 28, 4096, 16384, 50400
+g = torch.Generator(device="cuda").manual_seed(0)
+W = [[(torch.randn(n, k, device="cuda", generator=g) * 0.02).bfloat16() for n, k in
+      ((3 * d, d), (d, d), (F, d), (d, F))] for _ in range(L)]
+Wlm = (torch.randn(V, d, device="cuda", generator=g) * 0.02).bfloat16()
+s = torch.cuda.Stream()
+Ms = [int(a) for a in sys.argv[1:]] or [8, 64, 128, 192, 256, 320]
+ONLY = os.environ.get("ONLY")      # e.g. "qkv" or "qkv,o": only these projections (28 cold layers)
+SEL = ONLY.split(",") if ONLY else ["qkv", "o", "fc", "proj"]
+for M in Ms:
+    h = torch.randn(M, d, device="cuda").bfloat16()
+    qkv = torch.empty(M, 3 * d, device="cuda", dtype=torch.bfloat16)
+    f = torch.empty(M, F, device="cuda", dtype=torch.bfloat16)
+    a = torch.randn(M, d, device="cuda").bfloat16()
+    x = torch.zeros(M, d, device="cuda")
+    keys = torch.zeros(M, device="cuda", dtype=torch.int64)
+    st = C.c_void_p(0)
+    def gemm(xx, ww, out, epi, ldo):
+        Mx, K = xx.shape
+        N = ww.shape[0]
+        _lib.check(lib.fl_gemm(xx.data_ptr(), K, ww.data_ptr(), None, out.data_ptr(), ldo, Mx, N, K, epi, 1, 1,
+                               ws.data_ptr(), C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    def ours():
+        for l in range(L):
+            if "qkv" in SEL: gemm(h, W[l][0], qkv, 0, 3 * d)
+            if "o" in SEL: gemm(a, W[l][1], x, 2, d)
+            if "fc" in SEL: gemm(h, W[l][2], f, 1, F)
+            if "proj" in SEL: gemm(f, W[l][3], x, 2, d)
+    def ref():
+        for l in range(L):
+            if "qkv" in SEL: torch.matmul(h, W[l][0].T, out=qkv)
+            if "o" in SEL: torch.matmul(a, W[l][1].T)
+            if "fc" in SEL: torch.matmul(h, W[l][2].T, out=f)
+            if "proj" in SEL: torch.matmul(f, W[l][3].T)
+    res = []
+    for name, fn in (("ours", ours), ("cublas", ref)):
+        with torch.cuda.stream(s):
+            fn(); torch.cuda.synchronize()
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr, stream=s):
+                fn()
+            gr.replay(); torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            for _ in range(5):
+                gr.replay()
+            e1.record(s); torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 5
+        wel = sum({"qkv": 3 * d * d, "o": d * d, "fc": d * F, "proj": d * F}[k] for k in SEL)
+        tf = 2 * M * L * wel / (ms * 1e-3) / 1e12
+        gb = L * wel * 2 / (ms * 1e-3) / 1e9
+        res.append(f"{name} {1e3 * ms / L:7.1f} us/layer ({tf:5.0f} TF/s, {gb:5.0f} GB/s weights)")
+    print(f"{ONLY or 'all'} M={M:4d}  " + "   ".join(res), flush=True)
+    if os.environ.get("GEMM_DBG"):
+        dbg = torch.zeros(4 * 8192, dtype=torch.int64, device="cuda")
+        lib.fl_gemm_debug(C.c_void_p(dbg.data_ptr())); ours(); torch.cuda.synchronize(); lib.fl_gemm_debug(None)
+        dd = dbg.view(-1, 4).cpu().double()
+        p = dd[:2048][dd[:2048, 1] > 0]
+        lead = dd[:2048, 3] > 0
+        m = dd[:2048][lead]
+        e = dd[4096:6144]
+        ok = e[:, 1] > 0
+        e = e[ok]
+        t0 = e[:, 0].min()
+        print(f"   last GEMM: {len(p)} CTAs; producer waits {100*p[:,0].sum()/max(p[:,1].sum(),1):.0f}% of {p[:,1].mean():.0f} clk;"
+              f" mma full-waits {100*m[:,2].sum()/max(m[:,3].sum(),1):.0f}% of {m[:,3].mean():.0f} clk;"
+              f" CTA start spread {(e[:,0].max()-t0)/1e3:.1f} us, end {(e[:,1].min()-t0)/1e3:.1f}..{(e[:,1].max()-t0)/1e3:.1f} us;"
+              f" tfull-wait {e[:,2].mean():.0f} clk, epi total {e[:,3].mean():.0f} clk", flush=True)

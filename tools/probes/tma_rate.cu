@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <cstdio>
 #include <cstdint>
+#include <cstdlib>
 
 __device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void wait(uint64_t* b, uint32_t ph) {
@@ -31,7 +32,7 @@ __global__ void stream(const __grid_constant__ CUtensorMap map, const uint8_t* b
       const int st = it % stages;
       if (it >= stages) wait(&full[st], ((it / stages) - 1) & 1);
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&full[st])), "r"(bytes));
-      const int box = (blockIdx.x * 7 + it) % nbox;
+      const int box = (blockIdx.x * 1021 + it * 148 + issuer * 37) % nbox;
       if (MODE == 0) {
         asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
                      ::"r"(sa(s + st * bytes)), "l"((uint64_t)&map), "r"(sa(&full[st])), "r"((box % 16) * 64), "r"((box / 16) * rows) : "memory");
@@ -48,8 +49,8 @@ __global__ void stream(const __grid_constant__ CUtensorMap map, const uint8_t* b
   }
 }
 int main() {
-  // 4 MB source (L2 resident): [2048 rows][1024 bf16]
-  const int R = 2048, K = 1024;
+  // source: [R rows][1024 bf16]; R = 2048 (4 MB, L2 resident) or 262144 (512 MB, HBM stream)
+  const int R = getenv("HBM") ? 262144 : 2048, K = 1024;
   uint8_t* w;
   cudaMalloc(&w, (size_t)R * K * 2);
   cudaMemset(w, 1, (size_t)R * K * 2);
@@ -58,7 +59,7 @@ int main() {
   cudaDriverEntryPointQueryResult q;
   cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q);
   for (int warps : {1, 2, 4})
-  for (int rows : {64, 128}) {
+  for (int rows : {128}) {
     CUtensorMap map;
     cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)R}, str[1] = {(cuuint64_t)K * 2};
     cuuint32_t box[2] = {64, (cuuint32_t)rows}, es[2] = {1, 1};
@@ -67,13 +68,13 @@ int main() {
     const int nbox = 16 * (R / rows);
     for (int mode = 0; mode < 1; ++mode)
       for (int grid : {16, 148})
-        for (int stages : {4}) {
+        for (int stages : {4, 8}) {
           const int bytes = rows * 128;
           const int smem = warps * stages * bytes + 1024;
           if (smem > 220 * 1024) continue;
           auto k = mode ? stream<1> : stream<0>;
           cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-          const int iters = 400;
+          const int iters = getenv("HBM") ? 1500 : 400;
           k<<<grid, 32 * warps, smem>>>(map, w, iters, stages, rows, nbox, cyc);
           cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
           cudaEventRecord(a);
