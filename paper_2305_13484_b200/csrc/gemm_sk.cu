@@ -46,7 +46,7 @@ namespace {
 
 constexpr int SK_BM = 128;                 // weight rows per CTA (256 per pair)
 constexpr int SK_BK = 64;                  // K per stage (one 128-byte swizzle row)
-constexpr int SK_THREADS = 256;
+constexpr int SK_THREADS = 288;
 constexpr int SK_A_BYTES = SK_BM * SK_BK * 2;
 constexpr int SK_MAXST = 16;
 constexpr int SK_RING_BUDGET = 200 * 1024;
@@ -209,6 +209,8 @@ struct SkParams {
   int cn;           // pairs per cluster: token slices sharing multicast weight tiles
   int nclus;        // clusters (work ranges)
   int slice;        // tokens per pair (mt * bn)
+  int krot;         // rotate the K walk of whole tiles per cluster
+  int wsplit;       // weight producers per CTA (each loads 128 / wsplit rows per chunk)
   RopeArgs rope;
   unsigned long long* dbg;   // diagnostics: per CTA [prod wait, prod total, mma wait, mma total]
 };
@@ -276,6 +278,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
   __shared__ __align__(8) uint64_t tfull_bar[2];
   __shared__ __align__(8) uint64_t tempty_bar[2];
   __shared__ uint32_t tmem_base;
+  __shared__ unsigned long long issue_clk[SK_MAXST];   // diagnostics: W issue time per stage
   __shared__ __align__(16) float stg[4 * 32 * SK_STG_LD];   // epilogue transpose, 32x36 per warp
 
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -305,7 +308,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_w)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_x)) : "memory");
     for (int s = 0; s < stages; ++s) {
-      mbar_init(&full_bar[s], 1 + P.mt);   // weight producer + one per token sub-tile
+      mbar_init(&full_bar[s], P.wsplit + P.mt);   // weight producers + one per token sub-tile
       mbar_init(&empty_bar[s], CN);          // every pair's MMAs consumed the stage
     }
     for (int b = 0; b < 2; ++b) {
@@ -327,25 +330,34 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
   const int acc_cols = P.mt * P.bn;
 
   if (warp == 0 || warp >= 6) {
+    // (warp 8: second weight producer when the weight tile is split in two)
     // producers: warp 0 streams the weight tiles, warp 6 + j the token
     // sub-tile j -- one TMA request per thread per K chunk (a request costs
     // its issuing thread ~250 cycles, tools/probes/tma_rate.cu)
-    const int role = warp == 0 ? -1 : warp - 6;   // -1: weights, j >= 0: token sub-tile j
-    if (lane == 0 && role < P.mt) {
+    const int role = warp == 0 ? -1 : warp == 8 ? -2 : warp - 6;   // -1/-2: weight parts, j >= 0: token sub-tile j
+    if (lane == 0 && role < P.mt && role >= -P.wsplit) {
+      // pairs walking a whole tile start at a pair-dependent K chunk, so the
+      // pairs do not all request the same activation chunk from L2 at once
+      const int rot = P.krot ? (clu * 7) % kch : 0;
       auto coords = [&](int u, int& m0, int& n0, int& k) {
         const int t = u / kch;
-        k = (u - t * kch) * SK_BK;
+        int kk = u - t * kch;
+        if (rot && t * kch >= u0 && (t + 1) * kch <= u1) kk = kk + rot < kch ? kk + rot : kk + rot - kch;
+        k = kk * SK_BK;
         const int tm = t / P.ntn, tn = t - tm * P.ntn;
         m0 = tm * P.span + c * P.slice;          // this pair's token slice
         n0 = tn * 2 * SK_BM + xi * SK_BM;
       };
-      const uint32_t my_tx = 2u * (role < 0 ? SK_A_BYTES : XB);   // both CTAs' bytes
+      const int wpart = -1 - role;                        // weight part of this producer
+      const int wprows = SK_BM / P.wsplit;
+      const uint32_t my_tx = 2u * (role < 0 ? SK_A_BYTES / P.wsplit : XB);   // both CTAs' bytes
       auto issue = [&](int u, int st) {
         int m0, n0, k;
         coords(u, m0, n0, k);
         if (leader) mbar_expect_tx(&full_bar[st], my_tx);
+        if (P.dbg && role < 0) issue_clk[st] = clock64();
         if (role < 0 && CN == 1)
-          tma_load_pair(&tma_w, &full_bar[st], smem + st * STAGE, k, n0);
+          tma_load_pair(&tma_w, &full_bar[st], smem + st * STAGE + wpart * wprows * 128, k, n0 + wpart * wprows);
         else if (role < 0)
           tma_load_pair_mc(&tma_w, &full_bar[st], smem + st * STAGE + c * wrows * 128, k, n0 + c * wrows, wmask);
         else
@@ -358,7 +370,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       auto prefetch = [&](int u) {
         int m0, n0, k;
         coords(u, m0, n0, k);
-        l2_prefetch_2d(&tma_w, k, n0 + c * wrows);
+        l2_prefetch_2d(&tma_w, k, CN == 1 ? n0 + wpart * wprows : n0 + c * wrows);
       };
       const int pre = min(u1 - u0, stages);
       if (role >= 0) pdl_wait();            // activations are the predecessor's output
@@ -375,7 +387,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         if (D && u + D < u1) prefetch(u + D);
         if (++s == stages) { s = 0; ph ^= 1; }
       }
-      if (P.dbg && role < 0) {
+      if (P.dbg && role == -1) {
         P.dbg[4 * blockIdx.x + 0] = waited;
         P.dbg[4 * blockIdx.x + 1] = clock64() - t_start;
       }
@@ -385,7 +397,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       const uint32_t idesc = idesc_bf16(2 * SK_BM, P.bn);
       int s = 0, seg = 0;
       uint32_t ph = 0;
-      unsigned long long waited = 0, twait = 0, t_start = clock64();
+      unsigned long long waited = 0, twait = 0, lat = 0, nlat = 0, t_start = clock64();
       for (int u = u0; u < u1;) {
         const int t = u / kch;
         const int klo = u - t * kch;
@@ -400,7 +412,12 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         for (int c = klo; c < khi; ++c) {
           tw = P.dbg ? clock64() : 0;
           mbar_wait(&full_bar[s], ph);
-          if (P.dbg) waited += clock64() - tw;
+          if (P.dbg) {
+            const unsigned long long now = clock64();
+            waited += now - tw;
+            lat += now - *reinterpret_cast<volatile unsigned long long*>(&issue_clk[s]);
+            ++nlat;
+          }
           tc_fence_after();
           const uint8_t* st = smem + s * STAGE;
           const uint64_t ad = desc_sw128(st);
@@ -421,6 +438,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         P.dbg[4 * blockIdx.x + 2] = waited;
         P.dbg[4 * blockIdx.x + 3] = clock64() - t_start;
         P.dbg[4 * (2048 + blockIdx.x) + 0] = twait;
+        P.dbg[4 * (2048 + blockIdx.x) + 1] = nlat ? lat / nlat : 0;
       }
     }
   } else {
@@ -930,11 +948,15 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   P.dbg = g_sk_dbg;
   static const int use_red = getenv("FL_SK_RED") ? atoi(getenv("FL_SK_RED")) : 0;
   P.red = use_red;
-  static const int l2a = getenv("FL_SK_L2AHEAD") ? atoi(getenv("FL_SK_L2AHEAD")) : 8;
+  static const int l2a = getenv("FL_SK_L2AHEAD") ? atoi(getenv("FL_SK_L2AHEAD")) : 0;
   P.l2_ahead = l2a;
+  static const int krot = getenv("FL_SK_KROT") ? atoi(getenv("FL_SK_KROT")) : 0;
+  P.krot = krot;
+  static const int wsplit = getenv("FL_SK_WSPLIT") ? atoi(getenv("FL_SK_WSPLIT")) : 1;
+  P.wsplit = (CN == 1 && wsplit == 2) ? 2 : 1;
   P.vec = (a.ldo % 4 == 0 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0) ? 1 : 0;
   CUtensorMap *mw, *mx;
-  if (!sk_map({a.w, 0, (uint64_t)a.N, (uint64_t)a.K, (uint64_t)a.K * 2, SK_BK, (uint32_t)(SK_BM / CN), 1}, &mw))
+  if (!sk_map({a.w, 0, (uint64_t)a.N, (uint64_t)a.K, (uint64_t)a.K * 2, SK_BK, (uint32_t)(SK_BM / CN / P.wsplit), 1}, &mw))
     return -1;
   if (!sk_map({a.x, 0, (uint64_t)(a.mcap > a.M ? a.mcap : a.M), (uint64_t)a.K, (uint64_t)a.ldx * 2, SK_BK,
                (uint32_t)(P.bn / 2), 1}, &mx))

@@ -77,11 +77,12 @@ for M in Ms:
         p = dd[:2048][dd[:2048, 1] > 0]
         lead = dd[:2048, 3] > 0
         m = dd[:2048][lead]
+        lat = dd[2048:4096, 1][lead]
         e = dd[4096:6144]
         ok = e[:, 1] > 0
         e = e[ok]
         t0 = e[:, 0].min()
         print(f"   last GEMM: {len(p)} CTAs; producer waits {100*p[:,0].sum()/max(p[:,1].sum(),1):.0f}% of {p[:,1].mean():.0f} clk;"
-              f" mma full-waits {100*m[:,2].sum()/max(m[:,3].sum(),1):.0f}% of {m[:,3].mean():.0f} clk;"
+              f" mma full-waits {100*m[:,2].sum()/max(m[:,3].sum(),1):.0f}% of {m[:,3].mean():.0f} clk; issue->full {lat.mean():.0f} clk;"
               f" CTA start spread {(e[:,0].max()-t0)/1e3:.1f} us, end {(e[:,1].min()-t0)/1e3:.1f}..{(e[:,1].max()-t0)/1e3:.1f} us;"
               f" tfull-wait {e[:,2].mean():.0f} clk, epi total {e[:,3].mean():.0f} clk", flush=True)
