@@ -195,6 +195,18 @@ int fl_attention(const void* q, const fl_row* rows, const int32_t* row_ctx, int 
 int fl_gemm(const void* x, int ldx, const void* w, const void* bias, void* out, int ldo, int M,
             int N, int K, int epi, int dtype, int use_tc, void* workspace, void* cuda_stream);
 
+/* Device-resident shuffle planner: Algorithm 1
+ * (find_shuffled_memory_region, reference buffer.py:59-88) and plan_shuffle
+ * (buffer.py:226-258) over one window of n <= 8192 slots starting at slot lo.
+ * occ[n] (int32, nonzero = occupied) and size[n] (int64 bytes) are device
+ * arrays.  Writes, stream-ordered, into device memory:
+ *   out[0] = window offset (absolute slot), out[1] = window length (occupants),
+ *   out[2] = n_moves, out[3 + 2r], out[4 + 2r] = (src, dst) slot of move r
+ *   (ascending, as plan_shuffle pairs them);  *bytes = total_bytes_moved.
+ * out must hold 3 + 2n ints.  Returns FL_EINVAL for n outside [0, 8192]. */
+int fl_plan_shuffle(const int32_t* occ, const int64_t* size, int n, int lo, int32_t* out,
+                    long long* bytes, void* cuda_stream);
+
 #ifdef __cplusplus
 }
 #endif

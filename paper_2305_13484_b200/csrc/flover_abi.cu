@@ -737,3 +737,18 @@ extern "C" int fl_attention(const void* q, const fl_row* rows, const int32_t* ro
   FL_CUDA(cudaGetLastError());
   return FL_OK;
 }
+
+namespace fl {
+int launch_plan_shuffle(const int32_t* occ, const int64_t* size, int n, int lo, int32_t* out,
+                        long long* bytes, cudaStream_t s);
+}
+
+extern "C" int fl_plan_shuffle(const int32_t* occ, const int64_t* size, int n, int lo, int32_t* out,
+                               long long* bytes, void* stream) {
+  if (n < 0 || n > 8192) return fail(FL_EINVAL, "plan window of %d slots outside [0, 8192]", n);
+  if (!out || !bytes || (n > 0 && (!occ || !size))) return fail(FL_EINVAL, "null planner argument");
+  if (fl::launch_plan_shuffle(occ, size, n, lo, out, bytes, static_cast<cudaStream_t>(stream)))
+    return fail(FL_ECUDA, "planner launch: %s", cudaGetErrorString(cudaGetLastError()));
+  fl::g_launches += 1;
+  return FL_OK;
+}

@@ -915,8 +915,49 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   const int cols = P.nbuf * P.slice;
   P.ncols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
   P.units = ntm * P.ntn * P.kch;
+  void (*kern)(const CUtensorMap, const CUtensorMap, const SkParams) = nullptr;
+  switch (a.epi) {
+    case EPI_STORE: kern = k_gemm_sk<EPI_STORE>; break;
+    case EPI_GELU: kern = k_gemm_sk<EPI_GELU>; break;
+    case EPI_ACC_F32: kern = k_gemm_sk<EPI_ACC_F32>; break;
+    case EPI_STORE_F32: kern = k_gemm_sk<EPI_STORE_F32>; break;
+    case EPI_ARGMAX: kern = k_gemm_sk<EPI_ARGMAX>; break;
+    case EPI_QKV: kern = k_gemm_sk<EPI_QKV>; break;
+    default: g_sk_err = "unknown epilogue"; return -1;
+  }
+  const int smem = P.stages * stage + 1024;
   int nclus = num_sms / (2 * CN);
   if (nclus * CN > SK_MAX_PAIRS) nclus = SK_MAX_PAIRS / CN;
+  // a persistent grid must be co-resident: clusters of 2*CN CTAs at ~200 KB
+  // each only fit where a GPC still has 2*CN free SMs, so ask the occupancy
+  // calculator (SM count is not a multiple of the cluster size per GPC)
+  {
+    static std::map<std::tuple<const void*, int, int>, int> occ_cache;
+    const auto key = std::make_tuple(reinterpret_cast<const void*>(kern), 2 * CN, smem);
+    auto it = occ_cache.find(key);
+    if (it == occ_cache.end()) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(2 * CN * 128);
+      cfg.blockDim = dim3(SK_THREADS);
+      cfg.dynamicSmemBytes = smem;
+      cudaLaunchAttribute at;
+      at.id = cudaLaunchAttributeClusterDimension;
+      at.val.clusterDim.x = 2 * CN;
+      at.val.clusterDim.y = 1;
+      at.val.clusterDim.z = 1;
+      cfg.attrs = &at;
+      cfg.numAttrs = 1;
+      int nc = 0;
+      if (cudaOccupancyMaxActiveClusters(&nc, kern, &cfg) != cudaSuccess || nc < 1) {
+        cudaGetLastError();
+        nc = nclus;
+      }
+      if (getenv("FL_SK_VERBOSE"))
+        fprintf(stderr, "k_gemm_sk: cluster %d x %d B smem -> %d co-resident clusters\n", 2 * CN, smem, nc);
+      it = occ_cache.emplace(key, nc).first;
+    }
+    if (nclus > it->second) nclus = it->second;
+  }
   // wide windows (tensor-bound): whole or evenly split tiles, so no pair
   // stalls its MMA on a mid-range epilogue; narrow windows (HBM-bound): every
   // SM streams an equal share (stream-K)
@@ -961,17 +1002,6 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   if (!sk_map({a.x, 0, (uint64_t)(a.mcap > a.M ? a.mcap : a.M), (uint64_t)a.K, (uint64_t)a.ldx * 2, SK_BK,
                (uint32_t)(P.bn / 2), 1}, &mx))
     return -1;
-  const int smem = P.stages * stage + 1024;
-  void (*kern)(const CUtensorMap, const CUtensorMap, const SkParams) = nullptr;
-  switch (a.epi) {
-    case EPI_STORE: kern = k_gemm_sk<EPI_STORE>; break;
-    case EPI_GELU: kern = k_gemm_sk<EPI_GELU>; break;
-    case EPI_ACC_F32: kern = k_gemm_sk<EPI_ACC_F32>; break;
-    case EPI_STORE_F32: kern = k_gemm_sk<EPI_STORE_F32>; break;
-    case EPI_ARGMAX: kern = k_gemm_sk<EPI_ARGMAX>; break;
-    case EPI_QKV: kern = k_gemm_sk<EPI_QKV>; break;
-    default: g_sk_err = "unknown epilogue"; return -1;
-  }
   cudaError_t e = launch_k(kern, dim3(2 * P.npairs), dim3(SK_THREADS), smem, s, dim3(2 * CN, 1, 1), *mw, *mx, P);
   if (e != cudaSuccess) {
     char buf[256];

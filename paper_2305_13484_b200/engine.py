@@ -235,6 +235,8 @@ class FusionStream:
             lay.trim_boundaries()
             if done and lay.has_interior_holes():
                 plan = plan_shuffle(lay)
+                if self.executor is not None and getattr(self.executor, "device_plan", False):
+                    self.executor.check_device_plan(lay, plan)   # csrc/planner.cu, bit-exact
                 if plan.moves:
                     apply_shuffle(lay, plan)
                     dev_sh = None

@@ -56,10 +56,12 @@ class CudaExecutor:
                  state_slots: int = 4096, tp_rank: int = 0, tp_size: int = 1, seed: int = 0,
                  weights: dict | None = None, use_tensor_cores: bool | None = None,
                  capture_logits: bool = False, device: str = "cuda", comm_id: bytes | None = None,
-                 time_steps: bool = False, use_graphs: bool = True):
+                 time_steps: bool = False, use_graphs: bool = True, device_plan: bool = False):
         if dtype not in _TORCH_DTYPE:
             raise InvalidParam(f"dtype must be f32 or bf16, got {dtype}")
         self.lib = _lib.load()
+        self.device_plan = bool(device_plan)   # plan every shuffle boundary on the device too
+        self.device_plans = 0
         self.spec = spec
         self.prompts = prompts
         self.dtype = dtype
@@ -402,6 +404,16 @@ class CudaExecutor:
             self.shuffle_log.append((len(moves), nbytes, ms))
             return self.clock_reduce(ms) if self.clock_reduce else ms
         return None
+
+    def check_device_plan(self, layout, plan) -> None:
+        """Run Alg. 1 + plan_shuffle on the device (csrc/planner.cu) for this
+        boundary and require it to equal the host plan (SURVEY 8f #3)."""
+        from .devplan import device_plan_shuffle
+        from .errors import DeviceError
+        dplan = device_plan_shuffle(layout, device=self.device, stream=self.cs)
+        self.device_plans += 1
+        if dplan != plan:
+            raise DeviceError(f"device plan {dplan} != host plan {plan}")
 
     def on_drain(self, stream):
         self.cs.synchronize()

@@ -1,0 +1,79 @@
+"""Device-resident Alg. 1 + plan_shuffle (csrc/planner.cu) against the
+reference's golden vectors (tests/golden/alg1.json, plans.json -- generated
+by running the reference) and the host planner on random layouts: bit-exact."""
+
+import random
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+import paper_2305_13484_b200 as fl  # noqa: E402
+from paper_2305_13484_b200 import devplan  # noqa: E402
+from schedule_dump import load  # noqa: E402
+
+
+def _layout(sizes, evicted, trim=True):
+    lay = fl.BufferLayout()
+    for rid, size in enumerate(sizes):
+        lay.fuse_request(rid, size)
+    for rid in evicted:
+        lay.evict_request(rid)
+    if trim:
+        lay.trim_boundaries()
+    return lay
+
+
+def test_device_alg1_matches_reference_golden():
+    cases = load("alg1.json")["cases"]
+    for arr, off, _cost in cases:
+        if not arr:
+            continue
+        # BufferLayout sizes must be positive: a zero entry is a hole
+        sizes = [v if v else 1 for v in arr]
+        lay = _layout(sizes, [i for i, v in enumerate(arr) if not v], trim=False)
+        assert lay.size_array() == list(arr)
+        plan = devplan.device_plan_shuffle(lay)
+        assert plan.window_offset - lay.buffer_offset == off, arr
+
+
+def test_device_plans_match_reference_golden():
+    for c in load("plans.json")["cases"]:
+        lay = _layout(c["sizes"], c["evicted"])
+        plan = devplan.device_plan_shuffle(lay)
+        assert [[m.request_id, m.src_slot, m.dst_slot, m.size] for m in plan.moves] == c["moves"]
+        assert [plan.window_offset, plan.window_len] == c["plan_window"]
+        assert plan.total_bytes_moved == c["bytes"]
+        assert plan == fl.plan_shuffle(lay)
+
+
+@pytest.mark.parametrize("n", [1, 7, 64, 353, 1024, 1025, 4096, 8192])
+def test_device_plan_matches_host_random(n):
+    rng = random.Random(n)
+    for trial in range(4):
+        sizes = [rng.choice([1, 3, 1 << 20, rng.randint(1, 1 << 30)]) for _ in range(n)]
+        p = rng.random()
+        evicted = [i for i in range(n) if rng.random() < p and i not in (0, n - 1)]
+        lay = _layout(sizes, evicted)
+        assert devplan.device_plan_shuffle(lay) == fl.plan_shuffle(lay), (n, trial)
+
+
+def test_device_plan_rejects_oversized_window():
+    lay = _layout([1] * 8193, [])
+    with pytest.raises(ValueError):
+        devplan.device_plan_shuffle(lay)
+
+
+def test_device_planner_in_the_serving_loop():
+    """C1 with every shuffle boundary also planned on the device: plans equal
+    the host's (the executor raises otherwise) and the trace is still the
+    reference's golden trace."""
+    from harness import run_device, scenario_requests
+    from schedule_dump import sha
+    gold = {c["name"]: c for c in load("schedules.json.gz")["cases"]}["c1/tp1/on"]
+    reqs = scenario_requests(32, 20.0, 8, 64, 64, 16, seed=1)
+    trace, st, ex, prompts, w32 = run_device("tiny", reqs, dtype="f32", shuffle=True, device_plan=True)
+    assert sha(trace.format_lines()) == gold["trace_sha"]
+    assert ex.device_plans > 0

@@ -14,7 +14,7 @@ ncu --profile-from-start off --metrics gpu__time_duration.sum,dram__bytes_read.s
     python tools/prof_step.py --config $CFG --rows $ROWS --pre ${PRE:-350} --iters 2 > $OUT/launches_${CFG}.log 2>&1
 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:k_attn_tma -c 1 \
     -o $OUT/attn_${CFG} python tools/prof_step.py --config $CFG --rows $ROWS --pre ${PRE:-350} --iters 2 > $OUT/attn_${CFG}.log 2>&1
-ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:k_gemm_tc -c 4 \
+ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:k_gemm_sk -c 5 \
     -o $OUT/gemm_${CFG} python tools/prof_step.py --config $CFG --rows $ROWS --pre ${PRE:-350} --iters 2 > $OUT/gemm_${CFG}.log 2>&1
 ncu --set full --clock-control none -k regex:k_shuffle -s 3 -c 1 \
     -o $OUT/shuffle python tools/shuffle_bench.py 512 2 > $OUT/shuffle.log 2>&1
