@@ -351,9 +351,22 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       const int wpart = -1 - role;                        // weight part of this producer
       const int wprows = SK_BM / P.wsplit;
       const uint32_t my_tx = 2u * (role < 0 ? SK_A_BYTES / P.wsplit : XB);   // both CTAs' bytes
+      // units are issued strictly in order: walk the coordinates incrementally
+      // (no divisions on the producer's critical path)
+      int cur_u = u0, cur_m0, cur_n0, cur_k;
+      coords(u0, cur_m0, cur_n0, cur_k);
+      int cur_kk = cur_k / SK_BK, cur_t = u0 / kch;
       auto issue = [&](int u, int st) {
-        int m0, n0, k;
-        coords(u, m0, n0, k);
+        if (u != cur_u) {                     // advance by one unit
+          cur_u = u;
+          if (++cur_kk == kch || rot) {
+            if (cur_kk == kch) { cur_kk = 0; ++cur_t; }
+            coords(u, cur_m0, cur_n0, cur_k);
+          } else {
+            cur_k += SK_BK;
+          }
+        }
+        const int m0 = cur_m0, n0 = cur_n0, k = cur_k;
         if (leader) mbar_expect_tx(&full_bar[st], my_tx);
         if (P.dbg && role < 0) issue_clk[st] = clock64();
         if (role < 0 && CN == 1)
