@@ -103,6 +103,17 @@ FL_DEV void tma_load_pair(const CUtensorMap* map, uint64_t* bar, void* dst, int 
       "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1)
       : "memory");
 }
+// 3-D variant: box {64, rows, kpb} of a [k/64][rows][64] view -> kpb stacked
+// SW128 tiles in one request (a request costs its issuing thread a fixed
+// ~250 cycles, so bigger boxes stream proportionally faster)
+FL_DEV void tma_load_pair3(const CUtensorMap* map, uint64_t* bar, void* dst, int row, int kc) {
+  const uint32_t leader_bar = smem_u32(bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, "
+      "{%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(0), "r"(row), "r"(kc)
+      : "memory");
+}
 // 2-SM load multicast to the CTAs of `mask` (same smem offset in each);
 // complete_tx lands on each destination pair's leader barrier
 FL_DEV void tma_load_pair_mc(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1, uint16_t mask) {
@@ -211,6 +222,7 @@ struct SkParams {
   int slice;        // tokens per pair (mt * bn)
   int krot;         // rotate the K walk of whole tiles per cluster
   int wsplit;       // weight producers per CTA (each loads 128 / wsplit rows per chunk)
+  int kpb;          // 64-wide K sub-chunks per unit/stage (2: one 3-D request per operand)
   RopeArgs rope;
   unsigned long long* dbg;   // diagnostics: per CTA [prod wait, prod total, mma wait, mma total]
 };
@@ -299,8 +311,10 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
   for (int q = 0; q < CN; ++q) wmask |= static_cast<uint16_t>(1u << (2 * q + xi));
   const uint16_t allmask = static_cast<uint16_t>((1u << (2 * CN)) - 1u);
   const int wrows = SK_BM / CN;                  // weight rows this CTA loads per chunk
-  const int XB = (P.bn / 2) * SK_BK * 2;         // this CTA's half of a token sub-tile
-  const int STAGE = SK_A_BYTES + P.mt * XB;
+  const int XB = (P.bn / 2) * SK_BK * 2;         // this CTA's half of a token sub-tile (64 K)
+  const int KPB = P.kpb;                         // 64-wide K sub-chunks per unit
+  const int AB = KPB * SK_A_BYTES;               // weight bytes per stage and CTA
+  const int STAGE = AB + P.mt * KPB * XB;
   const int stages = P.stages, kch = P.kch;
   const int u0 = range_lo(clu, P), u1 = range_lo(clu + 1, P);
 
@@ -343,19 +357,19 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         const int t = u / kch;
         int kk = u - t * kch;
         if (rot && t * kch >= u0 && (t + 1) * kch <= u1) kk = kk + rot < kch ? kk + rot : kk + rot - kch;
-        k = kk * SK_BK;
+        k = kk * SK_BK * KPB;
         const int tm = t / P.ntn, tn = t - tm * P.ntn;
         m0 = tm * P.span + c * P.slice;          // this pair's token slice
         n0 = tn * 2 * SK_BM + xi * SK_BM;
       };
       const int wpart = -1 - role;                        // weight part of this producer
       const int wprows = SK_BM / P.wsplit;
-      const uint32_t my_tx = 2u * (role < 0 ? SK_A_BYTES / P.wsplit : XB);   // both CTAs' bytes
+      const uint32_t my_tx = 2u * (role < 0 ? AB / P.wsplit : KPB * XB);   // both CTAs' bytes
       // units are issued strictly in order: walk the coordinates incrementally
       // (no divisions on the producer's critical path)
       int cur_u = u0, cur_m0, cur_n0, cur_k;
       coords(u0, cur_m0, cur_n0, cur_k);
-      int cur_kk = cur_k / SK_BK, cur_t = u0 / kch;
+      int cur_kk = cur_k / (SK_BK * KPB), cur_t = u0 / kch;
       auto issue = [&](int u, int st) {
         if (u != cur_u) {                     // advance by one unit
           cur_u = u;
@@ -363,18 +377,23 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
             if (cur_kk == kch) { cur_kk = 0; ++cur_t; }
             coords(u, cur_m0, cur_n0, cur_k);
           } else {
-            cur_k += SK_BK;
+            cur_k += SK_BK * KPB;
           }
         }
         const int m0 = cur_m0, n0 = cur_n0, k = cur_k;
         if (leader) mbar_expect_tx(&full_bar[st], my_tx);
         if (P.dbg && role < 0) issue_clk[st] = clock64();
-        if (role < 0 && CN == 1)
+        if (role < 0 && KPB > 1)
+          tma_load_pair3(&tma_w, &full_bar[st], smem + st * STAGE, n0, k / SK_BK);
+        else if (role >= 0 && KPB > 1)
+          tma_load_pair3(&tma_x, &full_bar[st], smem + st * STAGE + AB + role * KPB * XB,
+                         m0 + role * P.bn + xi * (P.bn / 2), k / SK_BK);
+        else if (role < 0 && CN == 1)
           tma_load_pair(&tma_w, &full_bar[st], smem + st * STAGE + wpart * wprows * 128, k, n0 + wpart * wprows);
         else if (role < 0)
           tma_load_pair_mc(&tma_w, &full_bar[st], smem + st * STAGE + c * wrows * 128, k, n0 + c * wrows, wmask);
         else
-          tma_load_pair(&tma_x, &full_bar[st], smem + st * STAGE + SK_A_BYTES + role * XB, k,
+          tma_load_pair(&tma_x, &full_bar[st], smem + st * STAGE + AB + role * XB, k,
                         m0 + role * P.bn + xi * (P.bn / 2));
       };
       // weights are also prefetched into L2 `D` chunks beyond the ring: the
@@ -383,7 +402,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       auto prefetch = [&](int u) {
         int m0, n0, k;
         coords(u, m0, n0, k);
-        l2_prefetch_2d(&tma_w, k, CN == 1 ? n0 + wpart * wprows : n0 + c * wrows);
+        if (KPB == 1) l2_prefetch_2d(&tma_w, k, CN == 1 ? n0 + wpart * wprows : n0 + c * wrows);
       };
       const int pre = min(u1 - u0, stages);
       if (role >= 0) pdl_wait();            // activations are the predecessor's output
@@ -433,12 +452,14 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
           }
           tc_fence_after();
           const uint8_t* st = smem + s * STAGE;
-          const uint64_t ad = desc_sw128(st);
-          for (int j = 0; j < P.mt; ++j) {
-            const uint64_t bd = desc_sw128(st + SK_A_BYTES + j * XB);
+          for (int kc = 0; kc < KPB; ++kc) {
+            const uint64_t ad = desc_sw128(st + kc * SK_A_BYTES);
+            for (int j = 0; j < P.mt; ++j) {
+              const uint64_t bd = desc_sw128(st + AB + (j * KPB + kc) * XB);
 #pragma unroll
-            for (int kk = 0; kk < SK_BK / 16; ++kk)
-              mma_pair(acc + j * P.bn, ad + 2 * kk, bd + 2 * kk, idesc, (c > klo) | kk);
+              for (int kk = 0; kk < SK_BK / 16; ++kk)
+                mma_pair(acc + j * P.bn, ad + 2 * kk, bd + 2 * kk, idesc, (c > klo) | kc | kk);
+            }
           }
           commit_pair(&empty_bar[s], CN == 1 ? pmask : allmask);
           if (++s == stages) { s = 0; ph ^= 1; }
@@ -812,9 +833,10 @@ struct MapKey {
   uint64_t rows, cols, ld_bytes;
   uint32_t box_c, box_r;
   int swz;
+  int kpb;                 // > 1: 3-D view [cols/64][rows][64], box {64, box_r, kpb}
   bool operator<(const MapKey& o) const {
-    return std::tie(ptr, dtype, rows, cols, ld_bytes, box_c, box_r, swz) <
-           std::tie(o.ptr, o.dtype, o.rows, o.cols, o.ld_bytes, o.box_c, o.box_r, o.swz);
+    return std::tie(ptr, dtype, rows, cols, ld_bytes, box_c, box_r, swz, kpb) <
+           std::tie(o.ptr, o.dtype, o.rows, o.cols, o.ld_bytes, o.box_c, o.box_r, o.swz, o.kpb);
   }
 };
 std::map<MapKey, CUtensorMap> g_sk_maps;
@@ -836,12 +858,14 @@ bool sk_map(const MapKey& key, CUtensorMap** out) {
     g_encode_sk = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
   CUtensorMap map;
-  cuuint64_t dims[2] = {key.cols, key.rows};
-  cuuint64_t strides[1] = {key.ld_bytes};
-  cuuint32_t box[2] = {key.box_c, key.box_r};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = g_encode_sk(&map, key.dtype ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
-                           const_cast<void*>(key.ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+  const bool d3 = key.kpb > 1;
+  cuuint64_t dims[3] = {d3 ? 64 : key.cols, key.rows, key.cols / 64};
+  cuuint64_t strides[2] = {key.ld_bytes, 128};
+  cuuint32_t box[3] = {key.box_c, key.box_r, static_cast<cuuint32_t>(key.kpb)};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = g_encode_sk(&map, key.dtype ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                           d3 ? 3 : 2, const_cast<void*>(key.ptr), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE,
                            key.swz ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
@@ -901,6 +925,9 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   P.N = a.N;
   P.ldo = a.ldo;
   P.epi = a.epi;
+  // two 64-wide K sub-chunks per unit when the deeper stage still leaves >= 4
+  // stages (narrow windows) -- decided below once the token tiling is known
+  P.kpb = 1;
   P.kch = a.K / SK_BK;
   P.ntn = (a.N + 2 * SK_BM - 1) / (2 * SK_BM);
   // CN pairs per cluster split the token tile into slices and share (multicast)
@@ -919,7 +946,15 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   P.slice = P.mt * P.bn;
   P.span = CN * P.slice;
   P.cn = CN;
-  const int stage = SK_A_BYTES + P.mt * (P.bn / 2) * SK_BK * 2;
+  static const int force_kpb = getenv("FL_SK_KPB") ? atoi(getenv("FL_SK_KPB")) : 0;
+  {
+    const int st2 = 2 * (SK_A_BYTES + P.mt * (P.bn / 2) * SK_BK * 2);
+    const bool ok2 = CN == 1 && a.K % (2 * SK_BK) == 0;
+    if (ok2 && SK_RING_BUDGET / st2 >= 2 && (force_kpb == 2 || (force_kpb == 0 && SK_RING_BUDGET / st2 >= 4)))
+      P.kpb = 2;
+    P.kch = a.K / (SK_BK * P.kpb);
+  }
+  const int stage = P.kpb * (SK_A_BYTES + P.mt * (P.bn / 2) * SK_BK * 2);
   P.stages = SK_RING_BUDGET / stage;
   if (P.stages > SK_MAXST) P.stages = SK_MAXST;
   static const int force_st = getenv("FL_SK_STAGES") ? atoi(getenv("FL_SK_STAGES")) : 0;
@@ -984,6 +1019,7 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   if (!no_csplit && a.M >= 96 && tiles <= nclus && nclus / tiles >= 2 &&
       (a.epi == EPI_ACC_F32 || a.epi == EPI_STORE_F32 || a.epi == EPI_STORE || a.epi == EPI_GELU)) {
     P.csplit = nclus / tiles > 4 ? 4 : nclus / tiles;
+    if (P.csplit > P.kch) P.csplit = P.kch;             // every piece holds >= 1 K unit
     nclus = tiles * P.csplit;
   }
   const int cap = (P.units + 3) / 4;                       // >= 4 chunks per range
@@ -1007,13 +1043,14 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   static const int krot = getenv("FL_SK_KROT") ? atoi(getenv("FL_SK_KROT")) : 0;
   P.krot = krot;
   static const int wsplit = getenv("FL_SK_WSPLIT") ? atoi(getenv("FL_SK_WSPLIT")) : 1;
-  P.wsplit = (CN == 1 && wsplit == 2) ? 2 : 1;
+  P.wsplit = (CN == 1 && wsplit == 2 && P.kpb == 1) ? 2 : 1;
   P.vec = (a.ldo % 4 == 0 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0) ? 1 : 0;
   CUtensorMap *mw, *mx;
-  if (!sk_map({a.w, 0, (uint64_t)a.N, (uint64_t)a.K, (uint64_t)a.K * 2, SK_BK, (uint32_t)(SK_BM / CN / P.wsplit), 1}, &mw))
+  if (!sk_map({a.w, 0, (uint64_t)a.N, (uint64_t)a.K, (uint64_t)a.K * 2, SK_BK, (uint32_t)(SK_BM / CN / P.wsplit), 1,
+               P.kpb}, &mw))
     return -1;
   if (!sk_map({a.x, 0, (uint64_t)(a.mcap > a.M ? a.mcap : a.M), (uint64_t)a.K, (uint64_t)a.ldx * 2, SK_BK,
-               (uint32_t)(P.bn / 2), 1}, &mx))
+               (uint32_t)(P.bn / 2), 1, P.kpb}, &mx))
     return -1;
   cudaError_t e = launch_k(kern, dim3(2 * P.npairs), dim3(SK_THREADS), smem, s, dim3(2 * CN, 1, 1), *mw, *mx, P);
   if (e != cudaSuccess) {
