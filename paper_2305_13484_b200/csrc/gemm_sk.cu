@@ -223,6 +223,8 @@ struct SkParams {
   int krot;         // rotate the K walk of whole tiles per cluster
   int wsplit;       // weight producers per CTA (each loads 128 / wsplit rows per chunk)
   int kpb;          // 64-wide K sub-chunks per unit/stage (2: one 3-D request per operand)
+  int ntm;          // token tiles
+  int tmi;          // tile order: token tile inner (consecutive tiles share a weight tile)
   RopeArgs rope;
   unsigned long long* dbg;   // diagnostics: per CTA [prod wait, prod total, mma wait, mma total]
 };
@@ -358,7 +360,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         int kk = u - t * kch;
         if (rot && t * kch >= u0 && (t + 1) * kch <= u1) kk = kk + rot < kch ? kk + rot : kk + rot - kch;
         k = kk * SK_BK * KPB;
-        const int tm = t / P.ntn, tn = t - tm * P.ntn;
+        const int tm = P.tmi ? t % P.ntm : t / P.ntn, tn = P.tmi ? t / P.ntm : t - tm * P.ntn;
         m0 = tm * P.span + c * P.slice;          // this pair's token slice
         n0 = tn * 2 * SK_BM + xi * SK_BM;
       };
@@ -489,7 +491,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       // fix-up is spread over the S pairs instead of serialised in one owner.
       const int S = P.csplit;
       const int t = u0 / kch, piece = clu - t * S;
-      const int tm = t / P.ntn, tn = t - tm * P.ntn;
+      const int tm = P.tmi ? t % P.ntm : t / P.ntn, tn = P.tmi ? t / P.ntm : t - tm * P.ntn;
       const int m0 = tm * P.span + c * P.slice;   // this pair's token slice
       const int mcount = min(P.slice, P.M - m0);
       const int nbase = tn * 2 * SK_BM + xi * SK_BM;
@@ -589,7 +591,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       const int khi = min(kch, klo + (u1 - u));
       const int b = P.nbuf == 2 ? (seg & 1) : 0;
       const uint32_t use = P.nbuf == 2 ? (seg >> 1) : seg;
-      const int tm = t / P.ntn, tn = t - tm * P.ntn;
+      const int tm = P.tmi ? t % P.ntm : t / P.ntn, tn = P.tmi ? t / P.ntm : t - tm * P.ntn;
       const int m0 = tm * P.span + c * P.slice;   // this pair's token slice
       const int mcount = min(P.slice, P.M - m0);
       const int nbase = tn * 2 * SK_BM + xi * SK_BM;
@@ -935,7 +937,14 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   static const int force_cn = getenv("FL_SK_CN") ? atoi(getenv("FL_SK_CN")) : 0;
   int CN = 1;
   if (force_cn == 1 || force_cn == 2 || force_cn == 4) CN = force_cn;
-  const int smax = CN == 1 ? SK_MAX_SPAN : 256;           // tokens per pair
+  // wide windows > 256 tokens: two token tiles of <= 256 with the token tile
+  // as the inner tile index -- the second pass over a weight tile comes from
+  // L2, the accumulators (<= 256 columns) double-buffer, and stream-K keeps all
+  // 148 SMs streaming (a 320-column accumulator stalls the MMA at every
+  // segment end)
+  static const int msplit = getenv("FL_SK_MSPLIT") ? atoi(getenv("FL_SK_MSPLIT")) : 0;
+  const bool tsplit = msplit && CN == 1 && a.M > 256;
+  const int smax = (CN == 1 && !tsplit) ? SK_MAX_SPAN : 256;           // tokens per pair
   const int ntm = (a.M + CN * smax - 1) / (CN * smax);
   const int per = (a.M + ntm - 1) / ntm;                   // tokens per token tile
   const int slice0 = (per + CN - 1) / CN;
@@ -963,6 +972,8 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   const int cols = P.nbuf * P.slice;
   P.ncols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
   P.units = ntm * P.ntn * P.kch;
+  P.ntm = ntm;
+  P.tmi = tsplit ? 1 : 0;
   void (*kern)(const CUtensorMap, const CUtensorMap, const SkParams) = nullptr;
   switch (a.epi) {
     case EPI_STORE: kern = k_gemm_sk<EPI_STORE>; break;
@@ -1010,13 +1021,14 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   // stalls its MMA on a mid-range epilogue; narrow windows (HBM-bound): every
   // SM streams an equal share (stream-K)
   const int tiles = ntm * P.ntn;
-  if (a.M >= 96 && tiles <= nclus) nclus = tiles * (nclus / tiles);
+  static const int align_m = getenv("FL_SK_ALIGN_M") ? atoi(getenv("FL_SK_ALIGN_M")) : 64;
+  if (a.M >= align_m && tiles <= nclus && !tsplit) nclus = tiles * (nclus / tiles);
   static const int force_pairs = getenv("FL_SK_PAIRS") ? atoi(getenv("FL_SK_PAIRS")) : 0;
   if (force_pairs > 0 && force_pairs / CN < nclus) nclus = force_pairs / CN;
   // evenly split tiles of the direct epilogues: spread reduction (no owner)
   P.csplit = 1;
   static const int no_csplit = getenv("FL_SK_NO_CSPLIT") != nullptr;
-  if (!no_csplit && a.M >= 96 && tiles <= nclus && nclus / tiles >= 2 &&
+  if (!no_csplit && !tsplit && a.M >= align_m && tiles <= nclus && nclus / tiles >= 2 &&
       (a.epi == EPI_ACC_F32 || a.epi == EPI_STORE_F32 || a.epi == EPI_STORE || a.epi == EPI_GELU)) {
     P.csplit = nclus / tiles > 4 ? 4 : nclus / tiles;
     if (P.csplit > P.kch) P.csplit = P.kch;             // every piece holds >= 1 K unit
