@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
     const T* __restrict__ q, const fl_row* __restrict__ rows, const int32_t* __restrict__ row_ctx,
     int M, int Hl, const T* __restrict__ kv_layer, int S, T* __restrict__ out,
     float* __restrict__ ws_o, float* __restrict__ ws_ml, int max_splits, int keys_per_split,
-    int splits) {
+    int splits, const int32_t* __restrict__ order) {
   using Cfg = AttnCfg<T, HD>;
   constexpr int VEC = Cfg::VEC, NV = Cfg::NV, G = Cfg::G, PER = Cfg::PER, KPW = Cfg::KPW;
   constexpr int CW = Cfg::CW, TK = Cfg::TK, STAGES = Cfg::STAGES, NP = CW;
@@ -137,6 +137,14 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
 
   const int n_items = M * Hl * splits;
   const int D = Hl * HD;
+  // items (rank of the row by descending context, head, split) are dealt out
+  // boustrophedon-style: CTA b takes item b in even rounds and G-1-b in odd
+  // rounds, so with costs sorted longest-first every CTA gets a near-equal
+  // share (static round-robin over mixed contexts left a ~1.4x tail)
+  auto snake_item = [&](int round) {
+    const int G = static_cast<int>(gridDim.x);
+    return round * G + ((round & 1) ? (G - 1 - static_cast<int>(blockIdx.x)) : static_cast<int>(blockIdx.x));
+  };
   const size_t head_stride = static_cast<size_t>(S) * HD;
 
   if (warp == CW) {
@@ -144,10 +152,12 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
     if (lane == 0) {
       int st = 0;
       uint32_t ph = 0;
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      for (int round = 0; round * static_cast<int>(gridDim.x) < n_items; ++round) {
+        const int item = snake_item(round);
+        if (item >= n_items) continue;
         const int sp = item % splits;
         const int rh = item / splits;
-        const int h = rh % Hl, r = rh / Hl;
+        const int h = rh % Hl, r = order ? order[rh / Hl] : rh / Hl;
         const int ctx = row_ctx[r];
         const int k0 = sp * keys_per_split;
         if (k0 >= ctx) continue;
@@ -176,10 +186,12 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
   const float scale = rsqrtf(static_cast<float>(HD));
   int st = 0;
   uint32_t ph = 0;
-  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+  for (int round = 0; round * static_cast<int>(gridDim.x) < n_items; ++round) {
+    const int item = snake_item(round);
+    if (item >= n_items) continue;
     const int sp = item % splits;
     const int rh = item / splits;
-    const int h = rh % Hl, r = rh / Hl;
+    const int h = rh % Hl, r = order ? order[rh / Hl] : rh / Hl;
     const int ctx = row_ctx[r];
     const int k0 = sp * keys_per_split;
     if (k0 >= ctx) continue;
@@ -331,7 +343,7 @@ __global__ void k_attn_combine(const int32_t* __restrict__ row_ctx, int Hl,
 template <typename T, int HD>
 static int attn_launch(const void* q, const fl_row* rows, const int32_t* row_ctx, int M, int Hl,
                        const void* kv_layer, int S, int kps, void* out, float* ws_o, float* ws_ml,
-                       cudaStream_t s) {
+                       const int32_t* order, cudaStream_t s) {
   using Cfg = AttnCfg<T, HD>;
   static int num_sms = 0;
   if (!num_sms) {
@@ -345,7 +357,7 @@ static int attn_launch(const void* q, const fl_row* rows, const int32_t* row_ctx
   const int items = M * Hl * splits;
   const int grid = items < 2 * num_sms ? items : 2 * num_sms;
   launch_k(k_attn_tma<T, HD>, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM, s, 1, (const T*)q, rows,
-           row_ctx, M, Hl, (const T*)kv_layer, S, (T*)out, ws_o, ws_ml, ms, kps, splits);
+           row_ctx, M, Hl, (const T*)kv_layer, S, (T*)out, ws_o, ws_ml, ms, kps, splits, order);
   if (splits > 1) {
     launch_k(k_attn_combine<T, HD>, dim3(Hl, M), dim3(HD < 128 ? HD : 128), 0, s, 1, row_ctx, Hl,
              ws_o, ws_ml, ms, kps, (T*)out);
@@ -354,17 +366,50 @@ static int attn_launch(const void* q, const fl_row* rows, const int32_t* row_ctx
   return 1;
 }
 
+// Row ranks by descending context (ties: lower row first) for the snake
+// schedule: one CTA bitonic-sorts packed (~ctx, row) keys, M <= 1024.
+__global__ void __launch_bounds__(1024) k_row_order(const int32_t* __restrict__ row_ctx, int M,
+                                                   int32_t* __restrict__ order) {
+  __shared__ unsigned long long key[1024];
+  pdl_trigger();
+  pdl_wait();
+  int P = 1;
+  while (P < M) P <<= 1;
+  for (int i = threadIdx.x; i < P; i += blockDim.x)
+    key[i] = i < M ? (static_cast<unsigned long long>(0x7fffffffu - static_cast<uint32_t>(row_ctx[i])) << 32) | i
+                   : ~0ull;
+  __syncthreads();
+  for (int k = 2; k <= P; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const int l = i ^ j;
+        if (l > i) {
+          const unsigned long long a = key[i], b = key[l];
+          const bool up = (i & k) == 0;
+          if ((a > b) == up) { key[i] = b; key[l] = a; }
+        }
+      }
+      __syncthreads();
+    }
+  for (int i = threadIdx.x; i < M; i += blockDim.x) order[i] = static_cast<int32_t>(key[i] & 0xffffffffu);
+}
+
+void launch_row_order(const int32_t* row_ctx, int M, int32_t* order, cudaStream_t s) {
+  if (M <= 0 || M > 1024) return;
+  launch_k(k_row_order, dim3(1), dim3(M > 512 ? 1024 : 512), 0, s, 1, row_ctx, M, order);
+}
+
 int launch_attention(const void* q, const fl_row* rows, const int32_t* row_ctx, int M, int Hl,
                      int hd, const void* kv_layer, int C, int S, int kps, void* out, float* ws_o,
-                     float* ws_ml, int dtype, cudaStream_t s) {
+                     float* ws_ml, int dtype, cudaStream_t s, const int32_t* order) {
   if (M <= 0) return 0;
 #define FL_ATT(HDV)                                                                          \
   case HDV:                                                                                  \
     return dtype == FL_DTYPE_BF16                                                            \
                ? attn_launch<bf16, HDV>(q, rows, row_ctx, M, Hl, kv_layer, S, kps, out, ws_o, \
-                                        ws_ml, s)                                            \
+                                        ws_ml, order, s)                                     \
                : attn_launch<float, HDV>(q, rows, row_ctx, M, Hl, kv_layer, S, kps, out,      \
-                                         ws_o, ws_ml, s);
+                                         ws_o, ws_ml, order, s);
   switch (hd) {
     FL_ATT(64)
     FL_ATT(96)

@@ -90,7 +90,7 @@ struct fl_handle {
   int Hl, Dl, Fl, Vl, Vloc, es, ms;
   // workspace carve
   fl_row* rows;
-  int32_t *row_tok, *row_pos, *row_ctx, *moves;
+  int32_t *row_tok, *row_pos, *row_ctx, *row_order, *moves;
   float *x, *y, *logits, *att_o, *att_ml;
   void *h, *h2, *qkv, *q, *a, *f;
   unsigned long long* keys;
@@ -177,7 +177,7 @@ struct Carve {
 };
 
 struct Layout {
-  size_t rows, row_tok, row_pos, row_ctx, moves, x, y, logits, att_o, att_ml, h, h2, qkv, q, a, f, keys,
+  size_t rows, row_tok, row_pos, row_ctx, row_order, moves, x, y, logits, att_o, att_ml, h, h2, qkv, q, a, f, keys,
       tc, total;
 };
 
@@ -213,6 +213,7 @@ Layout plan(const fl_model_desc* m, const fl_pool_desc* p) {
   L.row_tok = c.take(Mr * 4);
   L.row_pos = c.take(Mr * 4);
   L.row_ctx = c.take(Mr * 4);
+  L.row_order = c.take(Mr * 4);
   L.moves = c.take(size_t(p->pool_slots) * 3 * 4 + 16);
   L.x = c.take(Mr * d * 4);
   L.y = c.take(Mr * d * 4);
@@ -274,6 +275,7 @@ int fl_create(const fl_model_desc* m, const fl_pool_desc* p, fl_handle** out) {
   h->row_tok = (int32_t*)(w + L.row_tok);
   h->row_pos = (int32_t*)(w + L.row_pos);
   h->row_ctx = (int32_t*)(w + L.row_ctx);
+  h->row_order = (int32_t*)(w + L.row_order);
   h->moves = (int32_t*)(w + L.moves);
   h->x = (float*)(w + L.x);
   h->y = (float*)(w + L.y);
@@ -479,6 +481,12 @@ int enqueue_step(fl_handle* h, int n_rows, int n_dec, bool want_logits, cudaStre
                    m.wpe, d, dt, h->x, h->row_tok, h->row_pos, h->row_ctx, h->keys, s);
   fl::g_launches += 1;
   const int att_keys = fl::attn_keys_per_split(n_rows * Hl, p.max_seq);
+  // rows ranked by descending context once per step (attention's schedule)
+  const bool ordered = n_rows <= 1024 && getenv("FL_ATT_NO_ORDER") == nullptr;
+  if (ordered) {
+    fl::launch_row_order(h->row_ctx, n_rows, h->row_order, s);
+    fl::g_launches += 1;
+  }
   for (int l = 0; l < L; ++l) {
     const void* const* W = m.layers + (size_t)l * FL_W_LAYER_COUNT;
     void* kvl = kv + kv_layer_elems * es * l;
@@ -509,7 +517,7 @@ int enqueue_step(fl_handle* h, int n_rows, int n_dec, bool want_logits, cudaStre
       ProfScope ps(h, FL_PROF_ATTENTION, s);
       fl::g_launches += fl::launch_attention(h->q, h->rows, h->row_ctx, n_rows, Hl, hd, kvl,
                                              p.pool_slots, p.max_seq, att_keys, h->a, h->att_o,
-                                             h->att_ml, dt, s);
+                                             h->att_ml, dt, s, ordered ? h->row_order : nullptr);
     }
     fl::g_launches += 1;
     // MLP input: GPT-2 = LN2 of the updated residual; GPT-J = LN1 output;
