@@ -224,6 +224,7 @@ struct SkParams {
   int wsplit;       // weight producers per CTA (each loads 128 / wsplit rows per chunk)
   int kpb;          // 64-wide K sub-chunks per unit/stage (2: one 3-D request per operand)
   int ntm;          // token tiles
+  int aorder;       // MMA issue order k-step outer, sub-tile inner
   int tmi;          // tile order: token tile inner (consecutive tiles share a weight tile)
   RopeArgs rope;
   unsigned long long* dbg;   // diagnostics: per CTA [prod wait, prod total, mma wait, mma total]
@@ -456,6 +457,16 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
           const uint8_t* st = smem + s * STAGE;
           for (int kc = 0; kc < KPB; ++kc) {
             const uint64_t ad = desc_sw128(st + kc * SK_A_BYTES);
+            if (P.mt == 2 && P.aorder) {
+              // consecutive MMAs share the weight slab (A) across the two token sub-tiles
+              const uint64_t bd0 = desc_sw128(st + AB + kc * XB), bd1 = desc_sw128(st + AB + (KPB + kc) * XB);
+#pragma unroll
+              for (int kk = 0; kk < SK_BK / 16; ++kk) {
+                mma_pair(acc, ad + 2 * kk, bd0 + 2 * kk, idesc, (c > klo) | kc | kk);
+                mma_pair(acc + P.bn, ad + 2 * kk, bd1 + 2 * kk, idesc, (c > klo) | kc | kk);
+              }
+              continue;
+            }
             for (int j = 0; j < P.mt; ++j) {
               const uint64_t bd = desc_sw128(st + AB + (j * KPB + kc) * XB);
 #pragma unroll
@@ -974,6 +985,8 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   P.units = ntm * P.ntn * P.kch;
   P.ntm = ntm;
   P.tmi = tsplit ? 1 : 0;
+  static const int aorder = getenv("FL_SK_AORDER") ? atoi(getenv("FL_SK_AORDER")) : 1;
+  P.aorder = aorder;
   void (*kern)(const CUtensorMap, const CUtensorMap, const SkParams) = nullptr;
   switch (a.epi) {
     case EPI_STORE: kern = k_gemm_sk<EPI_STORE>; break;
