@@ -675,16 +675,24 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
           if (EPI == EPI_QKV) {
             epi_qkv(P, v, n, nok, m0 + cb, ncol, lane);
           } else if (EPI == EPI_ARGMAX) {
+            // transpose through smem (stride 33: conflict-free both ways) so
+            // lane t scans token t's 32 weight rows: 64 shared accesses per
+            // block instead of 10 shuffles per token
+            float* tb = stg + quarter * (32 * SK_STG_LD);
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              unsigned long long key = (nok && j < ncol) ? argmax_key(v[j], P.index_base + n) : 0ull;
-#pragma unroll
-              for (int o = 1; o < 32; o <<= 1) {
-                const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
-                key = other > key ? other : key;
+            for (int j = 0; j < 32; ++j) tb[j * 33 + lane] = v[j];
+            __syncwarp();
+            const int nb = nbase + quarter * 32;
+            unsigned long long key = 0ull;
+#pragma unroll 8
+            for (int cc = 0; cc < 32; ++cc) {
+              if (nb + cc < P.N) {
+                const unsigned long long k2 = argmax_key(tb[lane * 33 + cc], P.index_base + nb + cc);
+                key = k2 > key ? k2 : key;
               }
-              if (lane == 0 && key) atomicMax(&P.keys[m0 + cb + j], key);
             }
+            __syncwarp();
+            if (lane < ncol && key) atomicMax(&P.keys[m0 + cb + lane], key);
           } else if (nok) {
             const size_t o0 = static_cast<size_t>(m0 + cb) * P.ldo + n;
 #pragma unroll
