@@ -218,12 +218,83 @@ __global__ void k_rope_append(const T* __restrict__ qkv, const fl_row* __restric
   }
 }
 
+// bf16 variant: one thread per 16-byte vector (8 elements) of q, k and v --
+// 16-byte loads and stores instead of 2-byte ones.  GPT-J's interleaved pairs
+// (2j, 2j+1) sit inside one vector; NeoX's rotate-half partner (i +- rot/2) is
+// read element-wise from the (L1-resident) row.
+__global__ void __launch_bounds__(256) k_rope_append_v(const bf16* __restrict__ qkv,
+                                                      const fl_row* __restrict__ rows,
+                                                      const int32_t* __restrict__ row_pos, int Hl,
+                                                      int hd, int rot, int family,
+                                                      bf16* __restrict__ kv_layer, int S,
+                                                      bf16* __restrict__ qout) {
+  pdl_trigger();
+  pdl_wait();
+  const int r = blockIdx.x;
+  const int D = Hl * hd;
+  const int vec = blockIdx.y * blockDim.x + threadIdx.x;      // vector index within the row's D
+  if (vec * 8 >= D) return;
+  const int e0 = vec * 8;
+  const int h = e0 / hd, i0 = e0 - h * hd;
+  const bf16* base = qkv + static_cast<size_t>(r) * 3 * D;
+  float q[8], k[8], v[8];
+  load16(base + e0, q);
+  load16(base + D + e0, k);
+  load16(base + 2 * D + e0, v);
+  const int pos = row_pos[r];
+  if (rot > 0 && i0 < rot) {
+    float qo[8], ko[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int i = i0 + t;
+      if (i >= rot) { qo[t] = q[t]; ko[t] = k[t]; continue; }
+      int j;
+      float sign, qp, kp;
+      if (family == FL_FAMILY_GPTJ) {
+        j = i >> 1;
+        sign = (i & 1) ? 1.f : -1.f;
+        qp = q[t ^ 1];
+        kp = k[t ^ 1];
+      } else {
+        const int half = rot >> 1;
+        j = i < half ? i : i - half;
+        const int partner = i < half ? i + half : i - half;
+        sign = i < half ? -1.f : 1.f;
+        qp = __bfloat162float(base[h * hd + partner]);
+        kp = __bfloat162float(base[D + h * hd + partner]);
+      }
+      const float inv_freq = exp2f(-(2.f * j / rot) * 13.287712379549449f);
+      float sn, cs;
+      sincosf(static_cast<float>(pos) * inv_freq, &sn, &cs);
+      qo[t] = q[t] * cs + sign * qp * sn;
+      ko[t] = k[t] * cs + sign * kp * sn;
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) { q[t] = qo[t]; k[t] = ko[t]; }
+  }
+  store16(qout + static_cast<size_t>(r) * D + e0, q);
+  const fl_row row = rows[r];
+  if (row.kind != FL_ROW_ORPHAN) {
+    const size_t kb = ((static_cast<size_t>(row.slot) * 2 + 0) * Hl + h) * S + pos;
+    const size_t vb = ((static_cast<size_t>(row.slot) * 2 + 1) * Hl + h) * S + pos;
+    store16(kv_layer + kb * hd + i0, k);
+    store16(kv_layer + vb * hd + i0, v);
+  }
+}
+
 void launch_rope_append(const void* qkv, const fl_row* rows, const int32_t* row_pos, int M,
                         int Hl, int hd, int rot, int family, void* kv_layer, int C, int S,
                         void* qout, int dtype, cudaStream_t s) {
   if (M <= 0) return;
   dim3 grid(M, Hl);
   if (family == FL_FAMILY_GPT2) rot = 0;
+  if (dtype == FL_DTYPE_BF16 && hd % 8 == 0) {
+    const int vecs = Hl * hd / 8;
+    const int bs = vecs < 256 ? (vecs + 31) / 32 * 32 : 256;
+    launch_k(k_rope_append_v, dim3(M, (vecs + bs - 1) / bs), dim3(bs), 0, s, 1, (const bf16*)qkv, rows, row_pos,
+             Hl, hd, rot, family, (bf16*)kv_layer, S, (bf16*)qout);
+    return;
+  }
   if (dtype == FL_DTYPE_BF16)
     launch_k(k_rope_append<bf16>, dim3(grid), dim3(hd), 0, s, 1, (const bf16*)qkv, rows, row_pos, Hl, hd, rot, family,
                                             (bf16*)kv_layer, C, S, (bf16*)qout);
