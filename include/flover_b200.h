@@ -99,7 +99,8 @@ typedef struct fl_pool_desc {
   int32_t max_rows;         /* rows per fused iteration (decode + orphan + prefill)      */
   int32_t state_slots;      /* R: per-request state ring, indexed rid % R                */
   int32_t max_new_tokens;   /* token history length per request                         */
-  int32_t use_tensor_cores; /* 1: tcgen05 GEMMs (bf16 only); 0: SIMT FFMA GEMMs          */
+  int32_t use_tensor_cores; /* 1: tcgen05 GEMMs (bf16 only), 2: same with weights tiled  */
+                            /*    (fl_tile_weight); 0: SIMT FFMA GEMMs                   */
   void* kv;                 /* [L][C][2][Hl][S][hd] in the model dtype                   */
   int32_t* req_tok;         /* [R] next input token of a running request                 */
   int32_t* req_pos;         /* [R] position of that token                                */
@@ -194,6 +195,14 @@ int fl_attention(const void* q, const fl_row* rows, const int32_t* row_ctx, int 
                  void* cuda_stream);
 int fl_gemm(const void* x, int ldx, const void* w, const void* bias, void* out, int ldo, int M,
             int N, int K, int epi, int dtype, int use_tc, void* workspace, void* cuda_stream);
+
+/* Tensor-core weight layout: bytes of the tiled copy of a bf16 W [N][K]
+ * (K % 64 == 0) and the stream-ordered re-layout into `out`.  A pool created
+ * with use_tensor_cores = 2 expects every projection weight (w_qkv, w_o, w_fc,
+ * w_proj of each layer, and w_lm) in this layout: [ceil(N/128)][K/64][128][64],
+ * so each 128 x 64 tile the GEMM streams is 16 KB of contiguous memory. */
+size_t fl_tiled_weight_bytes(int N, int K);
+int fl_tile_weight(const void* w, int N, int K, void* out, void* cuda_stream);
 
 /* Device-resident shuffle planner: Algorithm 1
  * (find_shuffled_memory_region, reference buffer.py:59-88) and plan_shuffle

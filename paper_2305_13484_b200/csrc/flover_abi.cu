@@ -195,6 +195,7 @@ int check_desc(const fl_model_desc* m, const fl_pool_desc* p) {
   if (m->d_model % 64 || m->d_model > 8192) return fail(FL_EINVAL, "d_model %d", m->d_model);
   if (p->pool_slots < 1 || p->max_seq < 1 || p->max_rows < 1 || p->state_slots < 1)
     return fail(FL_EINVAL, "bad pool sizes");
+  if (p->use_tensor_cores < 0 || p->use_tensor_cores > 2) return fail(FL_EINVAL, "use_tensor_cores must be 0, 1 or 2");
   if (p->use_tensor_cores && m->dtype != FL_DTYPE_BF16)
     return fail(FL_EINVAL, "tensor-core GEMMs need the bf16 path");
   return FL_OK;
@@ -420,6 +421,7 @@ int gemm(fl_handle* h, const void* x, int ldx, const void* w, const void* bias, 
           int ldo, int M, int N, int K, int epi, cudaStream_t s,
           const fl::RopeArgs* rope = nullptr, bool* fused = nullptr) {
   GemmArgs a{x, w, bias, out, M, N, K, ldx, ldo, epi, h->m.dtype, h->p.max_rows};
+  a.w_tiled = h->p.use_tensor_cores == 2 ? 1 : 0;
   if (epi == fl::EPI_ARGMAX) {
     a.keys = h->keys;
     a.index_base = h->m.tp_rank * h->Vl;
@@ -704,6 +706,7 @@ extern "C" int fl_gemm(const void* x, int ldx, const void* w, const void* bias, 
                        void* stream) {
   if (!x || !w || !out || M < 1 || N < 1 || K < 1) return fail(FL_EINVAL, "bad gemm arguments");
   fl::GemmArgs a{x, w, bias, out, M, N, K, ldx, ldo, epi, dtype, M};
+  a.w_tiled = use_tc == 2 ? 1 : 0;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (use_tc) {
     if (g_dbg_base != workspace) {
@@ -758,5 +761,21 @@ extern "C" int fl_plan_shuffle(const int32_t* occ, const int64_t* size, int n, i
   if (fl::launch_plan_shuffle(occ, size, n, lo, out, bytes, static_cast<cudaStream_t>(stream)))
     return fail(FL_ECUDA, "planner launch: %s", cudaGetErrorString(cudaGetLastError()));
   fl::g_launches += 1;
+  return FL_OK;
+}
+
+namespace fl {
+size_t tiled_weight_bytes(int N, int K);
+int launch_tile_weight(const void* w, int N, int K, void* out, cudaStream_t s);
+}
+
+extern "C" size_t fl_tiled_weight_bytes(int N, int K) {
+  return (N > 0 && K > 0 && K % 64 == 0) ? fl::tiled_weight_bytes(N, K) : 0;
+}
+
+extern "C" int fl_tile_weight(const void* w, int N, int K, void* out, void* stream) {
+  if (!w || !out || N <= 0 || K <= 0 || K % 64) return fail(FL_EINVAL, "bad tile_weight arguments");
+  if (fl::launch_tile_weight(w, N, K, out, static_cast<cudaStream_t>(stream)))
+    return fail(FL_ECUDA, "tile_weight launch: %s", cudaGetErrorString(cudaGetLastError()));
   return FL_OK;
 }

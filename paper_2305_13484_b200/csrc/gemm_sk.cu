@@ -224,6 +224,8 @@ struct SkParams {
   int wsplit;       // weight producers per CTA (each loads 128 / wsplit rows per chunk)
   int kpb;          // 64-wide K sub-chunks per unit/stage (2: one 3-D request per operand)
   int ntm;          // token tiles
+  int w_tiled;      // weights in the fl_tile_weight layout [N/128][K/64][128][64]
+  int kch64;        // K / 64
   int aorder;       // MMA issue order k-step outer, sub-tile inner
   int tmi;          // tile order: token tile inner (consecutive tiles share a weight tile)
   RopeArgs rope;
@@ -384,17 +386,23 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
           }
         }
         const int m0 = cur_m0, n0 = cur_n0, k = cur_k;
+        // weight coordinates: row-major W -> (k, n0); tiled W -> the first
+        // row of the contiguous 128 x 64 chunk (tile n0/128, K chunk k/64)
+        const int wcol = P.w_tiled ? 0 : k;
+        const int wrow = P.w_tiled ? ((n0 >> 7) * P.kch64 + (k >> 6)) * SK_BM : n0;
         if (leader) mbar_expect_tx(&full_bar[st], my_tx);
         if (P.dbg && role < 0) issue_clk[st] = clock64();
-        if (role < 0 && KPB > 1)
+        if (role < 0 && KPB > 1 && P.w_tiled)
+          tma_load_pair(&tma_w, &full_bar[st], smem + st * STAGE, 0, wrow);   // 2 chunks, 32 KB contiguous
+        else if (role < 0 && KPB > 1)
           tma_load_pair3(&tma_w, &full_bar[st], smem + st * STAGE, n0, k / SK_BK);
         else if (role >= 0 && KPB > 1)
           tma_load_pair3(&tma_x, &full_bar[st], smem + st * STAGE + AB + role * KPB * XB,
                          m0 + role * P.bn + xi * (P.bn / 2), k / SK_BK);
         else if (role < 0 && CN == 1)
-          tma_load_pair(&tma_w, &full_bar[st], smem + st * STAGE + wpart * wprows * 128, k, n0 + wpart * wprows);
+          tma_load_pair(&tma_w, &full_bar[st], smem + st * STAGE + wpart * wprows * 128, wcol, wrow + wpart * wprows);
         else if (role < 0)
-          tma_load_pair_mc(&tma_w, &full_bar[st], smem + st * STAGE + c * wrows * 128, k, n0 + c * wrows, wmask);
+          tma_load_pair_mc(&tma_w, &full_bar[st], smem + st * STAGE + c * wrows * 128, wcol, wrow + c * wrows, wmask);
         else
           tma_load_pair(&tma_x, &full_bar[st], smem + st * STAGE + AB + role * XB, k,
                         m0 + role * P.bn + xi * (P.bn / 2));
@@ -405,7 +413,9 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       auto prefetch = [&](int u) {
         int m0, n0, k;
         coords(u, m0, n0, k);
-        if (KPB == 1) l2_prefetch_2d(&tma_w, k, CN == 1 ? n0 + wpart * wprows : n0 + c * wrows);
+        const int wcol = P.w_tiled ? 0 : k;
+        const int wrow = P.w_tiled ? ((n0 >> 7) * P.kch64 + (k >> 6)) * SK_BM : n0;
+        if (KPB == 1 || P.w_tiled) l2_prefetch_2d(&tma_w, wcol, CN == 1 ? wrow + wpart * wprows : wrow + c * wrows);
       };
       const int pre = min(u1 - u0, stages);
       if (role >= 0) pdl_wait();            // activations are the predecessor's output
@@ -1079,9 +1089,17 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   P.wsplit = (CN == 1 && wsplit == 2 && P.kpb == 1) ? 2 : 1;
   P.vec = (a.ldo % 4 == 0 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0) ? 1 : 0;
   CUtensorMap *mw, *mx;
-  if (!sk_map({a.w, 0, (uint64_t)a.N, (uint64_t)a.K, (uint64_t)a.K * 2, SK_BK, (uint32_t)(SK_BM / CN / P.wsplit), 1,
-               P.kpb}, &mw))
+  P.w_tiled = a.w_tiled;
+  P.kch64 = a.K / SK_BK;
+  if (a.w_tiled) {
+    // [rows = ceil(N/128) * 128 * K/64][64]: 128-byte rows, contiguous chunks
+    const uint64_t trows = (uint64_t)((a.N + SK_BM - 1) / SK_BM) * SK_BM * (a.K / SK_BK);
+    const uint32_t box = P.kpb > 1 ? 2 * SK_BM : (uint32_t)(SK_BM / CN / P.wsplit);
+    if (!sk_map({a.w, 0, trows, (uint64_t)SK_BK, (uint64_t)SK_BK * 2, SK_BK, box, 1, 1}, &mw)) return -1;
+  } else if (!sk_map({a.w, 0, (uint64_t)a.N, (uint64_t)a.K, (uint64_t)a.K * 2, SK_BK,
+                      (uint32_t)(SK_BM / CN / P.wsplit), 1, P.kpb}, &mw)) {
     return -1;
+  }
   if (!sk_map({a.x, 0, (uint64_t)(a.mcap > a.M ? a.mcap : a.M), (uint64_t)a.K, (uint64_t)a.ldx * 2, SK_BK,
                (uint32_t)(P.bn / 2), 1, P.kpb}, &mx))
     return -1;

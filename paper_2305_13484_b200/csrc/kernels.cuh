@@ -38,6 +38,7 @@ struct GemmArgs {
   unsigned long long* keys = nullptr;   // EPI_ARGMAX: per-row packed (logit, index) keys
   int index_base = 0;                   // EPI_ARGMAX: global index of weight row 0
   RopeArgs rope;                        // EPI_QKV
+  int w_tiled = 0;                      // w in the fl_tile_weight layout
 };
 
 // SIMT FFMA GEMM (fp32 path and the reference path for the tensor-core GEMM).

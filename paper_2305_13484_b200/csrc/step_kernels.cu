@@ -371,3 +371,37 @@ void launch_apply_tokens(const unsigned long long* keys, const fl_row* rows,
 }
 
 }  // namespace fl
+
+namespace fl {
+// Weight re-layout for the tensor-core GEMM: W [N][K] row-major (rows K*2 bytes
+// apart, so a 128-row x 64-column TMA box touches 128 DRAM pages) becomes
+// [ceil(N/128)][K/64][128][64]: every box the GEMM loads is 16 KB contiguous
+// (two consecutive K chunks of a tile are 32 KB contiguous).  Padding rows are
+// zero.  One thread per 16-byte vector.
+__global__ void k_tile_weight(const bf16* __restrict__ w, int N, int K, bf16* __restrict__ out) {
+  const int kch = K / 64;
+  const size_t n_vec = static_cast<size_t>((N + 127) / 128) * 128 * K / 8;
+  for (size_t v = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; v < n_vec;
+       v += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t e = v * 8;                         // element index in the tiled layout
+    const int c = static_cast<int>(e % 64);
+    const size_t row = e / 64;                      // (tile * kch + kc) * 128 + r
+    const int r = static_cast<int>(row % 128);
+    const size_t tk = row / 128;
+    const int kc = static_cast<int>(tk % kch);
+    const size_t tile = tk / kch;
+    const size_t n = tile * 128 + r;
+    uint4 val = make_uint4(0u, 0u, 0u, 0u);
+    if (n < static_cast<size_t>(N)) val = *reinterpret_cast<const uint4*>(w + n * K + kc * 64 + c);
+    *reinterpret_cast<uint4*>(out + e) = val;
+  }
+}
+
+size_t tiled_weight_bytes(int N, int K) { return static_cast<size_t>((N + 127) / 128) * 128 * K * 2; }
+
+int launch_tile_weight(const void* w, int N, int K, void* out, cudaStream_t s) {
+  if (N <= 0 || K <= 0 || K % 64) return -1;
+  k_tile_weight<<<1184, 256, 0, s>>>(static_cast<const bf16*>(w), N, K, static_cast<bf16*>(out));
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+}  // namespace fl

@@ -27,12 +27,15 @@ to schedule: steady-state iterations upload nothing and read nothing back.
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import torch
 
 from . import _lib
 from .errors import CapacityExceeded, InvalidParam
 from .models import LAYER_KEYS, ModelSpec, init_weights
+
+GEMM_KEYS = ("w_qkv", "w_o", "w_fc", "w_proj")
 
 _TORCH_DTYPE = {"f32": torch.float32, "bf16": torch.bfloat16}
 _PAD = (0, -1, -1, -1, _lib.ROW_ORPHAN, 1)
@@ -90,6 +93,23 @@ class CudaExecutor:
             weights = init_weights(spec, seed=seed, device=self.device, dtype=tdt, rank=tp_rank,
                                    world=tp_size)
         self.w = {k: v.to(self.device, tdt).contiguous() for k, v in weights.items()}
+        # tensor-core path: projection weights in the GEMM's tiled layout
+        # (fl_tile_weight: every 128 x 64 tile the GEMM streams is contiguous);
+        # the caller's tensors are left untouched, our own copies are replaced
+        self.tiled = self.use_tc and dtype == "bf16" and not os.environ.get("FL_NO_TILED_WEIGHTS")
+        if self.tiled:
+            names = [f"layers.{l}.{k}" for l in range(spec.n_layer) for k in GEMM_KEYS] + ["w_lm"]
+            for name in names:
+                t = self.w.get(name)
+                if t is None:
+                    continue
+                n, k = t.shape
+                tt = torch.empty(self.lib.fl_tiled_weight_bytes(n, k) // 2, dtype=tdt, device=self.device)
+                _lib.check(self.lib.fl_tile_weight(C.c_void_p(t.data_ptr()), n, k, C.c_void_p(tt.data_ptr()),
+                                                   C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)))
+                self.w[name] = tt
+                del t
+        del weights       # our own row-major copies are freed before the KV pool is sized
         ptrs = []
         for layer in range(spec.n_layer):
             for key in LAYER_KEYS:
@@ -126,7 +146,8 @@ class CudaExecutor:
         self.req_ngen = torch.zeros(self.R, **i32)
         self.tok_hist = torch.zeros((self.R, self.max_new), **i32)
         self.pdesc = _lib.PoolDesc(self.C, self.S, self.max_rows, self.R, self.max_new,
-                                   int(self.use_tc), self.kv.data_ptr(), self.req_tok.data_ptr(),
+                                   (2 if self.tiled else 1) if self.use_tc else 0, self.kv.data_ptr(),
+                                   self.req_tok.data_ptr(),
                                    self.req_pos.data_ptr(), self.req_ngen.data_ptr(),
                                    self.tok_hist.data_ptr(), None, 0)
         nbytes = self.lib.fl_workspace_bytes(C.byref(self.mdesc), C.byref(self.pdesc))

@@ -21,6 +21,16 @@ def _gelu(x):
     return 0.5 * x * (1.0 + torch.tanh(0.7978845608028654 * (x + 0.044715 * x ** 3)))
 
 
+class _Tiled:
+    """A tiled weight buffer with the logical [N, K] shape (for _gemm)."""
+
+    def __init__(self, t, n, k):
+        self.t, self.shape = t, (n, k)
+
+    def data_ptr(self):
+        return self.t.data_ptr()
+
+
 def _gemm(x, w, bias, out, epi, use_tc, dtype):
     lib = _lib.load()
     ws = torch.empty(lib.fl_gemm_workspace_bytes(), dtype=torch.uint8, device="cuda")
@@ -105,3 +115,29 @@ def test_shuffle_kernel_bit_exact():
         ref[:, d, :, :, :n] = before[:, s, :, :, :n]
     assert torch.equal(ex.kv, ref)
     ex.close()
+
+
+@pytest.mark.parametrize("M,N,K", [(8, 12288, 4096), (320, 12288, 4096), (262, 4096, 16384), (100, 50257, 768),
+                                   (300, 1000, 256), (700, 1024, 512), (129, 1536, 4096)])
+@pytest.mark.parametrize("epi", [EPI_STORE, EPI_ACC])
+def test_tcgen05_gemm_tiled_weights(M, N, K, epi):
+    """fl_tile_weight layout ([N/128][K/64][128][64]) + use_tc = 2 gives the
+    same result as the row-major weights (bit-identical accumulation order)."""
+    lib = _lib.load()
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    x = (torch.randn(M, K, device="cuda", generator=g) * 0.5).bfloat16()
+    w = (torch.randn(N, K, device="cuda", generator=g) * 0.05).bfloat16()
+    b = (torch.randn(N, device="cuda", generator=g) * 0.1).bfloat16()
+    wt = torch.empty(lib.fl_tiled_weight_bytes(N, K) // 2, dtype=torch.bfloat16, device="cuda")
+    _lib.check(lib.fl_tile_weight(w.data_ptr(), N, K, wt.data_ptr(), C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    if epi == EPI_STORE:
+        o1 = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+    else:
+        o1 = torch.randn(M, N, device="cuda", generator=g)
+    o2 = o1.clone()
+    _gemm(x, w, b, o1, epi, 1, 1)
+    _gemm(x, _Tiled(wt, N, K), b, o2, epi, 2, 1)
+    if epi == EPI_STORE:
+        assert torch.equal(o1, o2)
+    else:
+        assert (o1 - o2).abs().max().item() <= 1e-4 * o1.abs().max().item()

@@ -22,6 +22,16 @@ g = torch.Generator(device="cuda").manual_seed(0)
 W = [[(torch.randn(n, k, device="cuda", generator=g) * 0.02).bfloat16() for n, k in
       ((3 * d, d), (d, d), (F, d), (d, F))] for _ in range(L)]
 Wlm = (torch.randn(V, d, device="cuda", generator=g) * 0.02).bfloat16()
+TILED = os.environ.get("TILED", "1") != "0"     # weights in the fl_tile_weight layout (as the executor runs)
+WT = None
+if TILED:
+    def _tile(w):
+        n, k = w.shape
+        t = torch.empty(lib.fl_tiled_weight_bytes(n, k) // 2, dtype=torch.bfloat16, device="cuda")
+        _lib.check(lib.fl_tile_weight(C.c_void_p(w.data_ptr()), n, k, C.c_void_p(t.data_ptr()), None))
+        return t
+    WT = [[_tile(w) for w in lw] for lw in W]
+    torch.cuda.synchronize()
 s = torch.cuda.Stream()
 Ms = [int(a) for a in sys.argv[1:]] or [8, 64, 128, 192, 256, 320]
 ONLY = os.environ.get("ONLY")      # e.g. "qkv" or "qkv,o": only these projections (28 cold layers)
@@ -34,17 +44,19 @@ for M in Ms:
     x = torch.zeros(M, d, device="cuda")
     keys = torch.zeros(M, device="cuda", dtype=torch.int64)
     st = C.c_void_p(0)
-    def gemm(xx, ww, out, epi, ldo):
+    def gemm(xx, ww, out, epi, ldo, wt=None):
         Mx, K = xx.shape
         N = ww.shape[0]
-        _lib.check(lib.fl_gemm(xx.data_ptr(), K, ww.data_ptr(), None, out.data_ptr(), ldo, Mx, N, K, epi, 1, 1,
+        wp = wt.data_ptr() if wt is not None else ww.data_ptr()
+        _lib.check(lib.fl_gemm(xx.data_ptr(), K, wp, None, out.data_ptr(), ldo, Mx, N, K, epi, 1,
+                               2 if wt is not None else 1,
                                ws.data_ptr(), C.c_void_p(torch.cuda.current_stream().cuda_stream)))
     def ours():
         for l in range(L):
-            if "qkv" in SEL: gemm(h, W[l][0], qkv, 0, 3 * d)
-            if "o" in SEL: gemm(a, W[l][1], x, 2, d)
-            if "fc" in SEL: gemm(h, W[l][2], f, 1, F)
-            if "proj" in SEL: gemm(f, W[l][3], x, 2, d)
+            if "qkv" in SEL: gemm(h, W[l][0], qkv, 0, 3 * d, WT[l][0] if WT else None)
+            if "o" in SEL: gemm(a, W[l][1], x, 2, d, WT[l][1] if WT else None)
+            if "fc" in SEL: gemm(h, W[l][2], f, 1, F, WT[l][2] if WT else None)
+            if "proj" in SEL: gemm(f, W[l][3], x, 2, d, WT[l][3] if WT else None)
     def ref():
         for l in range(L):
             if "qkv" in SEL: torch.matmul(h, W[l][0].T, out=qkv)
