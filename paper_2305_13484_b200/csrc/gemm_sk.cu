@@ -46,7 +46,7 @@ namespace {
 
 constexpr int SK_BM = 128;                 // weight rows per CTA (256 per pair)
 constexpr int SK_BK = 64;                  // K per stage (one 128-byte swizzle row)
-constexpr int SK_THREADS = 288;
+constexpr int SK_THREADS = 320;
 constexpr int SK_A_BYTES = SK_BM * SK_BK * 2;
 constexpr int SK_MAXST = 16;
 constexpr int SK_RING_BUDGET = 200 * 1024;
@@ -227,6 +227,7 @@ struct SkParams {
   int w_tiled;      // weights in the fl_tile_weight layout [N/128][K/64][128][64]
   int kch64;        // K / 64
   int aorder;       // MMA issue order k-step outer, sub-tile inner
+  int helpers;      // warps 6-9 help drain the last whole tile
   int tmi;          // tile order: token tile inner (consecutive tiles share a weight tile)
   RopeArgs rope;
   unsigned long long* dbg;   // diagnostics: per CTA [prod wait, prod total, mma wait, mma total]
@@ -283,6 +284,54 @@ FL_DEV void epi_qkv(const SkParams& P, const float* v, int n, bool nok, int mbas
       static_cast<bf16*>(rope.kv_layer)[o] = __float2bfloat16_rn(x);
     }
   }
+}
+
+// Final epilogue of one 32-token block of a whole tile through the per-warp
+// smem transpose (lane -> 4 weight rows of one token, 16-byte accesses).
+template <int EPI>
+FL_DEV void final_block(const SkParams& P, const uint32_t* r, float bv, float* ws_, int lane, int quarter,
+                        int nbase, int m0, int cb, int ncol) {
+#pragma unroll
+  for (int j = 0; j < 32; ++j) ws_[j * SK_STG_LD + lane] = __uint_as_float(r[j]) + bv;
+  __syncwarp();
+  const int c4 = (lane & 7) * 4, jb = lane >> 3;
+  const int nn = nbase + quarter * 32 + c4;
+  float4 w[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) w[i] = *reinterpret_cast<const float4*>(ws_ + (i * 4 + jb) * SK_STG_LD + c4);
+  const size_t o0 = static_cast<size_t>(m0 + cb) * P.ldo + nn;
+  if (EPI == EPI_STORE || EPI == EPI_GELU) {
+    bf16* dst = static_cast<bf16*>(P.out) + o0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int j = i * 4 + jb;
+      if (j >= ncol) continue;
+      float4 x = w[i];
+      if (EPI == EPI_GELU) { x.x = gelu_tanh(x.x); x.y = gelu_tanh(x.y); x.z = gelu_tanh(x.z); x.w = gelu_tanh(x.w); }
+      __nv_bfloat162 lo = __floats2bfloat162_rn(x.x, x.y), hi = __floats2bfloat162_rn(x.z, x.w);
+      *reinterpret_cast<uint2*>(dst + static_cast<size_t>(j) * P.ldo) =
+          make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+    }
+  } else {
+    float* dst = static_cast<float*>(P.out) + o0;
+    float4 y[8];
+    if (EPI == EPI_ACC_F32) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int j = i * 4 + jb;
+        y[i] = j < ncol ? *reinterpret_cast<const float4*>(dst + static_cast<size_t>(j) * P.ldo) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int j = i * 4 + jb;
+      if (j >= ncol) continue;
+      float4 x = w[i];
+      if (EPI == EPI_ACC_F32) { x.x += y[i].x; x.y += y[i].y; x.z += y[i].z; x.w += y[i].w; }
+      *reinterpret_cast<float4*>(dst + static_cast<size_t>(j) * P.ldo) = x;
+    }
+  }
+  __syncwarp();
 }
 
 template <int EPI>
@@ -435,6 +484,43 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       if (P.dbg && role == -1) {
         P.dbg[4 * blockIdx.x + 0] = waited;
         P.dbg[4 * blockIdx.x + 1] = clock64() - t_start;
+      }
+    }
+    __syncwarp();
+    if (warp >= 6 && P.helpers && P.csplit == 1) {
+      // ---- helpers: the odd 32-token blocks of the pair's last segment when
+      // it is a whole tile (the ring is idle once its accumulator is full, so
+      // the transpose buffers live there)
+      int seg = 0, u = u0, t = 0, klo = 0, khi = 0;
+      for (;;) {
+        t = u / kch;
+        klo = u - t * kch;
+        khi = min(kch, klo + (u1 - u));
+        if (u + (khi - klo) >= u1) break;
+        u += khi - klo;
+        ++seg;
+      }
+      const int tm = P.tmi ? t % P.ntm : t / P.ntn, tn = P.tmi ? t / P.ntm : t - tm * P.ntn;
+      const int m0 = tm * P.span + c * P.slice;
+      const int mcount = min(P.slice, P.M - m0);
+      const int nbase = tn * 2 * SK_BM + xi * SK_BM;
+      const bool vec = P.vec && nbase + SK_BM <= P.N;
+      if (vec && klo == 0 && khi == kch && u0 < u1) {
+        const int quarter = warp & 3;
+        const int n = nbase + quarter * 32 + lane;
+        const float bv = (P.bias && n < P.N) ? __bfloat162float(P.bias[n]) : 0.f;
+        const int b = P.nbuf == 2 ? (seg & 1) : 0;
+        const uint32_t use = P.nbuf == 2 ? (seg >> 1) : seg;
+        if (warp == 6 && lane == 0) mbar_wait_sleep(&tfull_bar[b], use & 1);
+        asm volatile("bar.sync 2, 128;" ::: "memory");
+        tc_fence_after();
+        const uint32_t tacc = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + b * acc_cols;
+        float* ws_ = reinterpret_cast<float*>(smem) + (warp - 6) * (32 * SK_STG_LD);
+        for (int cb = 32; cb < mcount; cb += 64) {
+          uint32_t r[32];
+          tmem_ld32(tacc + cb, r);
+          final_block<EPI>(P, r, bv, ws_, lane, quarter, nbase, m0, cb, min(32, mcount - cb));
+        }
       }
     }
   } else if (warp == 1) {
@@ -662,7 +748,18 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       // (4 weight rows of one token): a 32x32 block is 8 vector accesses per
       // lane instead of 32 scalar ones (tools/probes/store_probe.cu: 2.8x).
       const bool vec = P.vec && nbase + SK_BM <= P.N;
-      for (int cb = 0; cb < mcount; cb += 32) {
+      // last whole tile with helpers: warps 6-9 (done producing) drain the odd
+      // 32-token blocks, these warps the even ones
+      const bool helped = P.helpers && vec && whole && u + (khi - klo) >= u1;
+      if (helped) {
+        float* ws_ = stg + quarter * (32 * SK_STG_LD);
+        for (int cb = 0; cb < mcount; cb += 64) {
+          uint32_t r[32];
+          tmem_ld32(tacc + cb, r);
+          final_block<EPI>(P, r, bv, ws_, lane, quarter, nbase, m0, cb, min(32, mcount - cb));
+        }
+      }
+      for (int cb = 0; cb < mcount && !helped; cb += 32) {
         uint32_t r[32];
         const unsigned long long tl0 = P.dbg ? clock64() : 0;
         tmem_ld32(tacc + cb, r);
@@ -1005,6 +1102,9 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   P.tmi = tsplit ? 1 : 0;
   static const int aorder = getenv("FL_SK_AORDER") ? atoi(getenv("FL_SK_AORDER")) : 1;
   P.aorder = aorder;
+  static const int helpers = getenv("FL_SK_HELPERS") ? atoi(getenv("FL_SK_HELPERS")) : 1;
+  P.helpers = (helpers && CN == 1 && (a.epi == EPI_STORE || a.epi == EPI_GELU || a.epi == EPI_ACC_F32 ||
+                                      a.epi == EPI_STORE_F32)) ? 1 : 0;
   void (*kern)(const CUtensorMap, const CUtensorMap, const SkParams) = nullptr;
   switch (a.epi) {
     case EPI_STORE: kern = k_gemm_sk<EPI_STORE>; break;
