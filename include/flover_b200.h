@@ -196,6 +196,16 @@ int fl_attention(const void* q, const fl_row* rows, const int32_t* row_ctx, int 
 int fl_gemm(const void* x, int ldx, const void* w, const void* bias, void* out, int ldo, int M,
             int N, int K, int epi, int dtype, int use_tc, void* workspace, void* cuda_stream);
 
+/* Parallel-residual families (gptj, neox): run the attention output projection
+ * and the FFN down projection as ONE GEMM over K = Dl + Fl,
+ *   x += [a | f] . [W_o | W_proj]^T + b_o + b_proj
+ * (one reduction, and under tensor parallelism one all-reduce per layer instead
+ * of two).  w_cat[l]: [d_model][Dl + Fl] in the layout the pool's
+ * use_tensor_cores selects; b_cat[l]: b_o + b_proj or NULL (b_cat may be NULL).
+ * Call after fl_create, before the first fl_step.  The per-layer W_O / W_PROJ
+ * pointers are then unused. */
+int fl_set_merged_out(fl_handle* h, const void* const* w_cat, const void* const* b_cat);
+
 /* Tensor-core weight layout: bytes of the tiled copy of a bf16 W [N][K]
  * (K % 64 == 0) and the stream-ordered re-layout into `out`.  A pool created
  * with use_tensor_cores = 2 expects every projection weight (w_qkv, w_o, w_fc,

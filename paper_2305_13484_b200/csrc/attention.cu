@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
     const T* __restrict__ q, const fl_row* __restrict__ rows, const int32_t* __restrict__ row_ctx,
     int M, int Hl, const T* __restrict__ kv_layer, int S, T* __restrict__ out,
     float* __restrict__ ws_o, float* __restrict__ ws_ml, int max_splits, int keys_per_split,
-    int splits, const int32_t* __restrict__ order) {
+    int splits, const int32_t* __restrict__ order, int ldo) {
   using Cfg = AttnCfg<T, HD>;
   constexpr int VEC = Cfg::VEC, NV = Cfg::NV, G = Cfg::G, PER = Cfg::PER, KPW = Cfg::KPW;
   constexpr int CW = Cfg::CW, TK = Cfg::TK, STAGES = Cfg::STAGES, NP = CW;
@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
 #pragma unroll
       for (int i = 0; i < NP; ++i) o += s_m[i] == -INFINITY ? 0.f : s_acc[i][e] * __expf(s_m[i] - Mx);
       if (nsplit == 1) {
-        out[static_cast<size_t>(r) * D + h * HD + e] = from_f<T>(o / L);
+        out[static_cast<size_t>(r) * ldo + h * HD + e] = from_f<T>(o / L);
       } else {
         const size_t w = (static_cast<size_t>(r) * Hl + h) * max_splits + sp;
         ws_o[w * HD + e] = o;
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
 template <typename T, int HD>
 __global__ void k_attn_combine(const int32_t* __restrict__ row_ctx, int Hl,
                                const float* __restrict__ ws_o, const float* __restrict__ ws_ml,
-                               int max_splits, int keys_per_split, T* __restrict__ out) {
+                               int max_splits, int keys_per_split, T* __restrict__ out, int ldo) {
   pdl_trigger();
   pdl_wait();
   const int h = blockIdx.x, r = blockIdx.y;
@@ -336,14 +336,14 @@ __global__ void k_attn_combine(const int32_t* __restrict__ row_ctx, int Hl,
   for (int e = threadIdx.x; e < HD; e += blockDim.x) {
     float o = 0.f;
     for (int s = 0; s < nsplit; ++s) o += ws_o[(w0 + s) * HD + e] * __expf(ws_ml[2 * (w0 + s)] - M);
-    out[static_cast<size_t>(r) * Hl * HD + h * HD + e] = from_f<T>(o / L);
+    out[static_cast<size_t>(r) * ldo + h * HD + e] = from_f<T>(o / L);
   }
 }
 
 template <typename T, int HD>
 static int attn_launch(const void* q, const fl_row* rows, const int32_t* row_ctx, int M, int Hl,
                        const void* kv_layer, int S, int kps, void* out, float* ws_o, float* ws_ml,
-                       const int32_t* order, cudaStream_t s) {
+                       const int32_t* order, int ldo, cudaStream_t s) {
   using Cfg = AttnCfg<T, HD>;
   static int num_sms = 0;
   if (!num_sms) {
@@ -357,10 +357,10 @@ static int attn_launch(const void* q, const fl_row* rows, const int32_t* row_ctx
   const int items = M * Hl * splits;
   const int grid = items < 2 * num_sms ? items : 2 * num_sms;
   launch_k(k_attn_tma<T, HD>, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM, s, 1, (const T*)q, rows,
-           row_ctx, M, Hl, (const T*)kv_layer, S, (T*)out, ws_o, ws_ml, ms, kps, splits, order);
+           row_ctx, M, Hl, (const T*)kv_layer, S, (T*)out, ws_o, ws_ml, ms, kps, splits, order, ldo);
   if (splits > 1) {
     launch_k(k_attn_combine<T, HD>, dim3(Hl, M), dim3(HD < 128 ? HD : 128), 0, s, 1, row_ctx, Hl,
-             ws_o, ws_ml, ms, kps, (T*)out);
+             ws_o, ws_ml, ms, kps, (T*)out, ldo);
     return 2;
   }
   return 1;
@@ -401,15 +401,16 @@ void launch_row_order(const int32_t* row_ctx, int M, int32_t* order, cudaStream_
 
 int launch_attention(const void* q, const fl_row* rows, const int32_t* row_ctx, int M, int Hl,
                      int hd, const void* kv_layer, int C, int S, int kps, void* out, float* ws_o,
-                     float* ws_ml, int dtype, cudaStream_t s, const int32_t* order) {
+                     float* ws_ml, int dtype, cudaStream_t s, const int32_t* order, int ldo) {
+  if (ldo <= 0) ldo = Hl * hd;
   if (M <= 0) return 0;
 #define FL_ATT(HDV)                                                                          \
   case HDV:                                                                                  \
     return dtype == FL_DTYPE_BF16                                                            \
                ? attn_launch<bf16, HDV>(q, rows, row_ctx, M, Hl, kv_layer, S, kps, out, ws_o, \
-                                        ws_ml, order, s)                                     \
+                                        ws_ml, order, ldo, s)                                \
                : attn_launch<float, HDV>(q, rows, row_ctx, M, Hl, kv_layer, S, kps, out,      \
-                                         ws_o, ws_ml, order, s);
+                                         ws_o, ws_ml, order, ldo, s);
   switch (hd) {
     FL_ATT(64)
     FL_ATT(96)

@@ -95,6 +95,11 @@ struct fl_handle {
   void *h, *h2, *qkv, *q, *a, *f;
   unsigned long long* keys;
   fl::TcWorkspace tcws;
+  int ldaf = 0;                           // row stride (elements) of a and f
+  // merged out-projection (parallel residual): per layer [d][Dl + Fl] weight
+  // [W_o | W_proj] and bias b_o + b_proj (fl_set_merged_out)
+  std::vector<const void*> wcat, bcat;
+  bool merged = false;
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;
   // live profiling
@@ -225,8 +230,11 @@ Layout plan(const fl_model_desc* m, const fl_pool_desc* p) {
   L.h2 = c.take(m->family == FL_FAMILY_NEOX ? Mr * d * es : 0);
   L.qkv = c.take(Mr * 3 * Dl * es);
   L.q = c.take(Mr * Dl * es);
-  L.a = c.take(Mr * Dl * es);
-  L.f = c.take(Mr * Fl * es);
+  // attention output a and FFN activation f share rows: [Mr][Dl + Fl], so the
+  // parallel-residual families can run attn-out and FFN-down as ONE GEMM over
+  // K = Dl + Fl (fl_set_merged_out)
+  L.a = c.take(Mr * (Dl + Fl) * es);
+  L.f = 0;
   L.keys = c.take(Md * 8);
   const int nmax = (3 * Dl > Fl ? 3 * Dl : Fl) > Vl ? (3 * Dl > Fl ? 3 * Dl : Fl) : Vl;
   const int nmax2 = nmax > (int)d ? nmax : (int)d;
@@ -288,7 +296,8 @@ int fl_create(const fl_model_desc* m, const fl_pool_desc* p, fl_handle** out) {
   h->qkv = w + L.qkv;
   h->q = w + L.q;
   h->a = w + L.a;
-  h->f = w + L.f;
+  h->f = w + L.a + (size_t)h->Dl * h->es;    // same rows, after a's Dl columns
+  h->ldaf = h->Dl + h->Fl;
   h->keys = (unsigned long long*)(w + L.keys);
   if (p->use_tensor_cores) {
     int e = fl::tc_init(&h->tcws, w + L.tc, fl::tc_workspace_bytes(p->max_rows, 0));
@@ -519,7 +528,7 @@ int enqueue_step(fl_handle* h, int n_rows, int n_dec, bool want_logits, cudaStre
       ProfScope ps(h, FL_PROF_ATTENTION, s);
       fl::g_launches += fl::launch_attention(h->q, h->rows, h->row_ctx, n_rows, Hl, hd, kvl,
                                              p.pool_slots, p.max_seq, att_keys, h->a, h->att_o,
-                                             h->att_ml, dt, s, ordered ? h->row_order : nullptr);
+                                             h->att_ml, dt, s, ordered ? h->row_order : nullptr, h->ldaf);
     }
     fl::g_launches += 1;
     // MLP input: GPT-2 = LN2 of the updated residual; GPT-J = LN1 output;
@@ -528,14 +537,15 @@ int enqueue_step(fl_handle* h, int n_rows, int n_dec, bool want_logits, cudaStre
       fl::launch_layernorm(h->x, W[FL_W_LN2_G], W[FL_W_LN2_B], h->h2, n_rows, d, m.ln_eps, dt, s);
       fl::g_launches += 1;
     }
-    // K5 attn-out (+ all-reduce)
-    if (tp) {
-      FL_GEMM(h->a, Dl, W[FL_W_O], nullptr, h->y, d, n_rows, d, Dl, fl::EPI_STORE_F32, s);
+    // K5 attn-out (+ all-reduce); merged into K7 for parallel-residual models
+    if (h->merged) {
+    } else if (tp) {
+      FL_GEMM(h->a, h->ldaf, W[FL_W_O], nullptr, h->y, d, n_rows, d, Dl, fl::EPI_STORE_F32, s);
       if (int e = allreduce_f32(h, h->y, (size_t)n_rows * d, s)) return e;
       fl::launch_add_partial(h->x, h->y, W[FL_W_O_B], nullptr, n_rows, d, dt, s);
       fl::g_launches += 1;
     } else {
-      FL_GEMM(h->a, Dl, W[FL_W_O], W[FL_W_O_B], h->x, d, n_rows, d, Dl, fl::EPI_ACC_F32, s);
+      FL_GEMM(h->a, h->ldaf, W[FL_W_O], W[FL_W_O_B], h->x, d, n_rows, d, Dl, fl::EPI_ACC_F32, s);
     }
     const void* mlp_in = h->h;  // GPT-J: LN1 output
     if (m.family == FL_FAMILY_GPT2) {
@@ -545,14 +555,26 @@ int enqueue_step(fl_handle* h, int n_rows, int n_dec, bool want_logits, cudaStre
       mlp_in = h->h2;
     }
     // K6 + K7 (+ all-reduce)
-    FL_GEMM(mlp_in, d, W[FL_W_FC], W[FL_W_FC_B], h->f, Fl, n_rows, Fl, d, fl::EPI_GELU, s);
-    if (tp) {
-      FL_GEMM(h->f, Fl, W[FL_W_PROJ], nullptr, h->y, d, n_rows, d, Fl, fl::EPI_STORE_F32, s);
+    FL_GEMM(mlp_in, d, W[FL_W_FC], W[FL_W_FC_B], h->f, h->ldaf, n_rows, Fl, d, fl::EPI_GELU, s);
+    if (h->merged) {
+      // x += [a | f] . [W_o | W_proj]^T + b_o + b_proj: one GEMM, one reduction
+      // (and one all-reduce under TP instead of two)
+      const int Kc = Dl + Fl;
+      if (tp) {
+        FL_GEMM(h->a, h->ldaf, h->wcat[l], nullptr, h->y, d, n_rows, d, Kc, fl::EPI_STORE_F32, s);
+        if (int e = allreduce_f32(h, h->y, (size_t)n_rows * d, s)) return e;
+        fl::launch_add_partial(h->x, h->y, W[FL_W_O_B], W[FL_W_PROJ_B], n_rows, d, dt, s);
+        fl::g_launches += 1;
+      } else {
+        FL_GEMM(h->a, h->ldaf, h->wcat[l], h->bcat[l], h->x, d, n_rows, d, Kc, fl::EPI_ACC_F32, s);
+      }
+    } else if (tp) {
+      FL_GEMM(h->f, h->ldaf, W[FL_W_PROJ], nullptr, h->y, d, n_rows, d, Fl, fl::EPI_STORE_F32, s);
       if (int e = allreduce_f32(h, h->y, (size_t)n_rows * d, s)) return e;
       fl::launch_add_partial(h->x, h->y, W[FL_W_PROJ_B], nullptr, n_rows, d, dt, s);
       fl::g_launches += 1;
     } else {
-      FL_GEMM(h->f, Fl, W[FL_W_PROJ], W[FL_W_PROJ_B], h->x, d, n_rows, d, Fl, fl::EPI_ACC_F32, s);
+      FL_GEMM(h->f, h->ldaf, W[FL_W_PROJ], W[FL_W_PROJ_B], h->x, d, n_rows, d, Fl, fl::EPI_ACC_F32, s);
     }
   }
   if (n_dec > 0) {
@@ -777,5 +799,20 @@ extern "C" int fl_tile_weight(const void* w, int N, int K, void* out, void* stre
   if (!w || !out || N <= 0 || K <= 0 || K % 64) return fail(FL_EINVAL, "bad tile_weight arguments");
   if (fl::launch_tile_weight(w, N, K, out, static_cast<cudaStream_t>(stream)))
     return fail(FL_ECUDA, "tile_weight launch: %s", cudaGetErrorString(cudaGetLastError()));
+  return FL_OK;
+}
+
+extern "C" int fl_set_merged_out(fl_handle* h, const void* const* w_cat, const void* const* b_cat) {
+  if (!h || !w_cat) return fail(FL_EINVAL, "null merged-out argument");
+  if (h->m.family == FL_FAMILY_GPT2)
+    return fail(FL_EINVAL, "merged out-projection needs a parallel-residual family (gptj, neox)");
+  if (!h->graphs.empty()) return fail(FL_EINVAL, "fl_set_merged_out after the first step");
+  if ((h->Dl + h->Fl) % 64) return fail(FL_EINVAL, "Dl + Fl must be a multiple of 64");
+  h->wcat.assign(w_cat, w_cat + h->m.n_layer);
+  h->bcat.assign(h->m.n_layer, nullptr);
+  if (b_cat) h->bcat.assign(b_cat, b_cat + h->m.n_layer);
+  for (auto p : h->wcat)
+    if (!p) return fail(FL_EINVAL, "null merged weight");
+  h->merged = true;
   return FL_OK;
 }

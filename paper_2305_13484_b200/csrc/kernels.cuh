@@ -72,7 +72,7 @@ int attn_keys_per_split(int row_heads, int S);
 int launch_attention(const void* q, const fl_row* rows, const int32_t* row_ctx, int M, int Hl,
                      int hd, const void* kv_layer, int C, int S, int keys_per_split, void* out,
                      float* ws_o, float* ws_ml, int dtype, cudaStream_t s,
-                     const int32_t* order = nullptr);
+                     const int32_t* order = nullptr, int ldo = 0);
 // order[i] = row of rank i by descending context (attention's snake schedule)
 void launch_row_order(const int32_t* row_ctx, int M, int32_t* order, cudaStream_t s);
 

@@ -97,8 +97,22 @@ class CudaExecutor:
         # (fl_tile_weight: every 128 x 64 tile the GEMM streams is contiguous);
         # the caller's tensors are left untouched, our own copies are replaced
         self.tiled = self.use_tc and dtype == "bf16" and not os.environ.get("FL_NO_TILED_WEIGHTS")
+        # parallel residual (gptj, neox): attn-out and FFN-down as one GEMM over
+        # K = Dl + Fl with W_cat = [W_o | W_proj] and b_o + b_proj (tensor-core path)
+        self.merged = (self.use_tc and spec.family in ("gptj", "neox")
+                       and not os.environ.get("FL_NO_MERGED_OUT"))
+        self._wcat, self._bcat = [], []
+        if self.merged:
+            for l in range(spec.n_layer):
+                wo, wp = self.w.pop(f"layers.{l}.w_o"), self.w.pop(f"layers.{l}.w_proj")
+                self.w[f"layers.{l}.w_cat"] = torch.cat([wo, wp], dim=1).contiguous()
+                del wo, wp
+                bs = [b.float() for b in (self.w.get(f"layers.{l}.b_o"), self.w.get(f"layers.{l}.b_proj"))
+                      if b is not None]
+                if bs:
+                    self.w[f"layers.{l}.b_cat"] = sum(bs).to(tdt)
         if self.tiled:
-            names = [f"layers.{l}.{k}" for l in range(spec.n_layer) for k in GEMM_KEYS] + ["w_lm"]
+            names = [f"layers.{l}.{k}" for l in range(spec.n_layer) for k in GEMM_KEYS + ("w_cat",)] + ["w_lm"]
             for name in names:
                 t = self.w.get(name)
                 if t is None:
@@ -159,6 +173,13 @@ class CudaExecutor:
         h = C.c_void_p()
         _lib.check(self.lib.fl_create(C.byref(self.mdesc), C.byref(self.pdesc), C.byref(h)))
         self.handle = h
+        if self.merged:
+            wc = [self.w[f"layers.{l}.w_cat"].data_ptr() for l in range(spec.n_layer)]
+            bc = [self.w[f"layers.{l}.b_cat"].data_ptr() if f"layers.{l}.b_cat" in self.w else None
+                  for l in range(spec.n_layer)]
+            self._wcat = (C.c_void_p * len(wc))(*wc)
+            self._bcat = (C.c_void_p * len(bc))(*bc)
+            _lib.check(self.lib.fl_set_merged_out(self.handle, self._wcat, self._bcat))
         self.use_graphs = use_graphs
         self._lib_timing = False
         _lib.check(self.lib.fl_configure(self.handle, int(use_graphs), 8, 0))
