@@ -124,12 +124,6 @@ FL_DEV void tma_load_pair_mc(const CUtensorMap* map, uint64_t* bar, void* dst, i
       "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1), "h"(mask)
       : "memory");
 }
-FL_DEV void l2_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
-  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
-                   reinterpret_cast<uint64_t>(map)),
-               "r"(c0), "r"(c1)
-               : "memory");
-}
 FL_DEV void mma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -216,19 +210,15 @@ struct SkParams {
   int vec;          // out rows 16-byte aligned: vector stores
   int red;          // EPI_ACC_F32 split tiles: red.add pieces (else owner fix-up)
   int csplit;       // >1: tile K split evenly over S pairs, spread reduction
-  int l2_ahead;     // weight chunks prefetched into L2 beyond the ring
   int cn;           // pairs per cluster: token slices sharing multicast weight tiles
   int nclus;        // clusters (work ranges)
   int slice;        // tokens per pair (mt * bn)
-  int krot;         // rotate the K walk of whole tiles per cluster
-  int wsplit;       // weight producers per CTA (each loads 128 / wsplit rows per chunk)
   int kpb;          // 64-wide K sub-chunks per unit/stage (2: one 3-D request per operand)
   int ntm;          // token tiles
   int w_tiled;      // weights in the fl_tile_weight layout [N/128][K/64][128][64]
   int kch64;        // K / 64
   int aorder;       // MMA issue order k-step outer, sub-tile inner
   int helpers;      // warps 6-9 help drain the last whole tile
-  int tmi;          // tile order: token tile inner (consecutive tiles share a weight tile)
   RopeArgs rope;
   unsigned long long* dbg;   // diagnostics: per CTA [prod wait, prod total, mma wait, mma total]
 };
@@ -376,7 +366,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_w)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_x)) : "memory");
     for (int s = 0; s < stages; ++s) {
-      mbar_init(&full_bar[s], P.wsplit + P.mt);   // weight producers + one per token sub-tile
+      mbar_init(&full_bar[s], 1 + P.mt);   // weight producer + one per token sub-tile
       mbar_init(&empty_bar[s], CN);          // every pair's MMAs consumed the stage
     }
     for (int b = 0; b < 2; ++b) {
@@ -403,22 +393,16 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
     // sub-tile j -- one TMA request per thread per K chunk (a request costs
     // its issuing thread ~250 cycles, tools/probes/tma_rate.cu)
     const int role = warp == 0 ? -1 : warp == 8 ? -2 : warp - 6;   // -1/-2: weight parts, j >= 0: token sub-tile j
-    if (lane == 0 && role < P.mt && role >= -P.wsplit) {
-      // pairs walking a whole tile start at a pair-dependent K chunk, so the
-      // pairs do not all request the same activation chunk from L2 at once
-      const int rot = P.krot ? (clu * 7) % kch : 0;
+    if (lane == 0 && role < P.mt && role >= -1) {
       auto coords = [&](int u, int& m0, int& n0, int& k) {
         const int t = u / kch;
-        int kk = u - t * kch;
-        if (rot && t * kch >= u0 && (t + 1) * kch <= u1) kk = kk + rot < kch ? kk + rot : kk + rot - kch;
+        const int kk = u - t * kch;
         k = kk * SK_BK * KPB;
-        const int tm = P.tmi ? t % P.ntm : t / P.ntn, tn = P.tmi ? t / P.ntm : t - tm * P.ntn;
+        const int tm = t / P.ntn, tn = t - tm * P.ntn;
         m0 = tm * P.span + c * P.slice;          // this pair's token slice
         n0 = tn * 2 * SK_BM + xi * SK_BM;
       };
-      const int wpart = -1 - role;                        // weight part of this producer
-      const int wprows = SK_BM / P.wsplit;
-      const uint32_t my_tx = 2u * (role < 0 ? AB / P.wsplit : KPB * XB);   // both CTAs' bytes
+      const uint32_t my_tx = 2u * (role < 0 ? AB : KPB * XB);   // both CTAs' bytes
       // units are issued strictly in order: walk the coordinates incrementally
       // (no divisions on the producer's critical path)
       int cur_u = u0, cur_m0, cur_n0, cur_k;
@@ -427,8 +411,9 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       auto issue = [&](int u, int st) {
         if (u != cur_u) {                     // advance by one unit
           cur_u = u;
-          if (++cur_kk == kch || rot) {
-            if (cur_kk == kch) { cur_kk = 0; ++cur_t; }
+          if (++cur_kk == kch) {
+            cur_kk = 0;
+            ++cur_t;
             coords(u, cur_m0, cur_n0, cur_k);
           } else {
             cur_k += SK_BK * KPB;
@@ -449,27 +434,16 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
           tma_load_pair3(&tma_x, &full_bar[st], smem + st * STAGE + AB + role * KPB * XB,
                          m0 + role * P.bn + xi * (P.bn / 2), k / SK_BK);
         else if (role < 0 && CN == 1)
-          tma_load_pair(&tma_w, &full_bar[st], smem + st * STAGE + wpart * wprows * 128, wcol, wrow + wpart * wprows);
+          tma_load_pair(&tma_w, &full_bar[st], smem + st * STAGE, wcol, wrow);
         else if (role < 0)
           tma_load_pair_mc(&tma_w, &full_bar[st], smem + st * STAGE + c * wrows * 128, wcol, wrow + c * wrows, wmask);
         else
           tma_load_pair(&tma_x, &full_bar[st], smem + st * STAGE + AB + role * XB, k,
                         m0 + role * P.bn + xi * (P.bn / 2));
       };
-      // weights are also prefetched into L2 `D` chunks beyond the ring: the
-      // ring alone (~180 KB at wide windows) cannot cover HBM latency
-      const int D = role < 0 ? P.l2_ahead : 0;
-      auto prefetch = [&](int u) {
-        int m0, n0, k;
-        coords(u, m0, n0, k);
-        const int wcol = P.w_tiled ? 0 : k;
-        const int wrow = P.w_tiled ? ((n0 >> 7) * P.kch64 + (k >> 6)) * SK_BM : n0;
-        if (KPB == 1 || P.w_tiled) l2_prefetch_2d(&tma_w, wcol, CN == 1 ? wrow + wpart * wprows : wrow + c * wrows);
-      };
       const int pre = min(u1 - u0, stages);
       if (role >= 0) pdl_wait();            // activations are the predecessor's output
       for (int i = 0; i < pre; ++i) issue(u0 + i, i);   // weights stream ahead of the wait
-      for (int u = u0 + pre; u < min(u1, u0 + pre + D); ++u) prefetch(u);
       int s = pre % stages;
       uint32_t ph = pre == stages ? 1u : 0u;
       unsigned long long waited = 0, t_start = clock64();
@@ -478,7 +452,6 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         mbar_wait(&empty_bar[s], ph ^ 1);
         if (P.dbg) waited += clock64() - tw;
         issue(u, s);
-        if (D && u + D < u1) prefetch(u + D);
         if (++s == stages) { s = 0; ph ^= 1; }
       }
       if (P.dbg && role == -1) {
@@ -500,7 +473,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         u += khi - klo;
         ++seg;
       }
-      const int tm = P.tmi ? t % P.ntm : t / P.ntn, tn = P.tmi ? t / P.ntm : t - tm * P.ntn;
+      const int tm = t / P.ntn, tn = t - tm * P.ntn;
       const int m0 = tm * P.span + c * P.slice;
       const int mcount = min(P.slice, P.M - m0);
       const int nbase = tn * 2 * SK_BM + xi * SK_BM;
@@ -598,7 +571,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       // fix-up is spread over the S pairs instead of serialised in one owner.
       const int S = P.csplit;
       const int t = u0 / kch, piece = clu - t * S;
-      const int tm = P.tmi ? t % P.ntm : t / P.ntn, tn = P.tmi ? t / P.ntm : t - tm * P.ntn;
+      const int tm = t / P.ntn, tn = t - tm * P.ntn;
       const int m0 = tm * P.span + c * P.slice;   // this pair's token slice
       const int mcount = min(P.slice, P.M - m0);
       const int nbase = tn * 2 * SK_BM + xi * SK_BM;
@@ -698,7 +671,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       const int khi = min(kch, klo + (u1 - u));
       const int b = P.nbuf == 2 ? (seg & 1) : 0;
       const uint32_t use = P.nbuf == 2 ? (seg >> 1) : seg;
-      const int tm = P.tmi ? t % P.ntm : t / P.ntn, tn = P.tmi ? t / P.ntm : t - tm * P.ntn;
+      const int tm = t / P.ntn, tn = t - tm * P.ntn;
       const int m0 = tm * P.span + c * P.slice;   // this pair's token slice
       const int mcount = min(P.slice, P.M - m0);
       const int nbase = tn * 2 * SK_BM + xi * SK_BM;
@@ -1063,14 +1036,7 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   static const int force_cn = getenv("FL_SK_CN") ? atoi(getenv("FL_SK_CN")) : 0;
   int CN = 1;
   if (force_cn == 1 || force_cn == 2 || force_cn == 4) CN = force_cn;
-  // wide windows > 256 tokens: two token tiles of <= 256 with the token tile
-  // as the inner tile index -- the second pass over a weight tile comes from
-  // L2, the accumulators (<= 256 columns) double-buffer, and stream-K keeps all
-  // 148 SMs streaming (a 320-column accumulator stalls the MMA at every
-  // segment end)
-  static const int msplit = getenv("FL_SK_MSPLIT") ? atoi(getenv("FL_SK_MSPLIT")) : 0;
-  const bool tsplit = msplit && CN == 1 && a.M > 256;
-  const int smax = (CN == 1 && !tsplit) ? SK_MAX_SPAN : 256;           // tokens per pair
+  const int smax = CN == 1 ? SK_MAX_SPAN : 256;           // tokens per pair
   const int ntm = (a.M + CN * smax - 1) / (CN * smax);
   const int per = (a.M + ntm - 1) / ntm;                   // tokens per token tile
   const int slice0 = (per + CN - 1) / CN;
@@ -1099,7 +1065,6 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   P.ncols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
   P.units = ntm * P.ntn * P.kch;
   P.ntm = ntm;
-  P.tmi = tsplit ? 1 : 0;
   static const int aorder = getenv("FL_SK_AORDER") ? atoi(getenv("FL_SK_AORDER")) : 1;
   P.aorder = aorder;
   static const int helpers = getenv("FL_SK_HELPERS") ? atoi(getenv("FL_SK_HELPERS")) : 1;
@@ -1153,13 +1118,13 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   // SM streams an equal share (stream-K)
   const int tiles = ntm * P.ntn;
   static const int align_m = getenv("FL_SK_ALIGN_M") ? atoi(getenv("FL_SK_ALIGN_M")) : 64;
-  if (a.M >= align_m && tiles <= nclus && !tsplit) nclus = tiles * (nclus / tiles);
+  if (a.M >= align_m && tiles <= nclus) nclus = tiles * (nclus / tiles);
   static const int force_pairs = getenv("FL_SK_PAIRS") ? atoi(getenv("FL_SK_PAIRS")) : 0;
   if (force_pairs > 0 && force_pairs / CN < nclus) nclus = force_pairs / CN;
   // evenly split tiles of the direct epilogues: spread reduction (no owner)
   P.csplit = 1;
   static const int no_csplit = getenv("FL_SK_NO_CSPLIT") != nullptr;
-  if (!no_csplit && !tsplit && a.M >= align_m && tiles <= nclus && nclus / tiles >= 2 &&
+  if (!no_csplit && a.M >= align_m && tiles <= nclus && nclus / tiles >= 2 &&
       (a.epi == EPI_ACC_F32 || a.epi == EPI_STORE_F32 || a.epi == EPI_STORE || a.epi == EPI_GELU)) {
     P.csplit = nclus / tiles > 4 ? 4 : nclus / tiles;
     if (P.csplit > P.kch) P.csplit = P.kch;             // every piece holds >= 1 K unit
@@ -1181,12 +1146,6 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   P.dbg = g_sk_dbg;
   static const int use_red = getenv("FL_SK_RED") ? atoi(getenv("FL_SK_RED")) : 0;
   P.red = use_red;
-  static const int l2a = getenv("FL_SK_L2AHEAD") ? atoi(getenv("FL_SK_L2AHEAD")) : 0;
-  P.l2_ahead = l2a;
-  static const int krot = getenv("FL_SK_KROT") ? atoi(getenv("FL_SK_KROT")) : 0;
-  P.krot = krot;
-  static const int wsplit = getenv("FL_SK_WSPLIT") ? atoi(getenv("FL_SK_WSPLIT")) : 1;
-  P.wsplit = (CN == 1 && wsplit == 2 && P.kpb == 1) ? 2 : 1;
   P.vec = (a.ldo % 4 == 0 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0) ? 1 : 0;
   CUtensorMap *mw, *mx;
   P.w_tiled = a.w_tiled;
@@ -1194,10 +1153,10 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   if (a.w_tiled) {
     // [rows = ceil(N/128) * 128 * K/64][64]: 128-byte rows, contiguous chunks
     const uint64_t trows = (uint64_t)((a.N + SK_BM - 1) / SK_BM) * SK_BM * (a.K / SK_BK);
-    const uint32_t box = P.kpb > 1 ? 2 * SK_BM : (uint32_t)(SK_BM / CN / P.wsplit);
+    const uint32_t box = P.kpb > 1 ? 2 * SK_BM : (uint32_t)(SK_BM / CN);
     if (!sk_map({a.w, 0, trows, (uint64_t)SK_BK, (uint64_t)SK_BK * 2, SK_BK, box, 1, 1}, &mw)) return -1;
   } else if (!sk_map({a.w, 0, (uint64_t)a.N, (uint64_t)a.K, (uint64_t)a.K * 2, SK_BK,
-                      (uint32_t)(SK_BM / CN / P.wsplit), 1, P.kpb}, &mw)) {
+                      (uint32_t)(SK_BM / CN), 1, P.kpb}, &mw)) {
     return -1;
   }
   if (!sk_map({a.x, 0, (uint64_t)(a.mcap > a.M ? a.mcap : a.M), (uint64_t)a.K, (uint64_t)a.ldx * 2, SK_BK,
