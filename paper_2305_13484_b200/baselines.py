@@ -131,3 +131,116 @@ def run_dynamic_batching(requests, cfg: BatchWindowConfig, params: CostParams,
         executor.on_drain(None)
     trace.sort()
     return trace
+
+
+# --------------------------------------------------------------------------
+# Concurrent instances -- one model instance per request.
+#
+# Drop-in for the reference's ``run_concurrent_instances`` (baselines.py:
+# 130-229, contention model cost.py:112-116): an instance starts when its
+# request clears preprocessing and needs ``actual_output_length`` tokens at
+# its solo iteration time d; while k instances are live every one of them
+# advances at 1 / (d * (1 + gamma (k - 1))) tokens per ms, re-evaluated at
+# every start and finish with the fractional progress carried over.  The
+# trace (cost clock) is byte-identical to the reference's
+# (tests/test_baselines_golden.py).
+#
+# With a ``CudaExecutor`` every token of every instance is really computed:
+# each instance is its own single-row stream over its own KV slot, and the
+# token events are replayed in trace order as batch-1 decode steps -- so the
+# instance tokens can be checked against the fused run's (greedy decoding
+# does not depend on how requests are batched).
+
+def run_concurrent_instances(requests, params: CostParams, tp: TPConfig | None = None,
+                             record_tokens: bool = True, *, executor=None) -> Trace:
+    tp = tp or TPConfig()
+    ordered = sorted(requests, key=lambda r: (r.arrival_time, r.request_id))
+    ev = []
+    for r in ordered:
+        ev.append(TraceEvent(r.arrival_time, EventKind.ARRIVED, r.request_id, None))
+        ev.append(TraceEvent(r.arrival_time, EventKind.PREPROCESS_START, r.request_id, None))
+        ev.append(TraceEvent(r.arrival_time + params.preprocess_ms, EventKind.PREPROCESS_DONE,
+                             r.request_id, None))
+    trace = Trace("concurrent", ev)
+    if not ordered:
+        return trace
+    # per instance: [rid, ready, solo step time d, length, progress, time of its last token]
+    inst = [[r.request_id, r.arrival_time + params.preprocess_ms,
+             iteration_time(1, r.batch_size * params.request_bytes, params, tp),
+             r.actual_output_length, 0.0, 0.0] for r in ordered]
+    inst.sort(key=lambda x: (x[1], x[0]))
+    RID, READY, D, LEN, PROG, LAST = range(6)
+    live, nxt, now = [], 0, inst[0][READY]
+    token_log = []                       # (time, rid, j) for the device replay
+
+    def start_ready():
+        nonlocal nxt
+        while nxt < len(inst) and inst[nxt][READY] <= now:
+            x = inst[nxt]
+            nxt += 1
+            x[LAST] = now
+            live.append(x)
+            ev.append(TraceEvent(now, EventKind.FUSED, x[RID], None))
+
+    start_ready()
+    while live or nxt < len(inst):
+        if not live:
+            now = max(now, inst[nxt][READY])
+            start_ready()
+        f = 1.0 + params.contention_gamma * (len(live) - 1)
+        t_start = inst[nxt][READY] if nxt < len(inst) else None
+        t_fin = min(now + (x[LEN] - x[PROG]) * x[D] * f for x in live)
+        ends = t_start is None or t_fin <= t_start
+        t_next = t_fin if ends else t_start
+        finished = []
+        for x in live:
+            own_end = now + (x[LEN] - x[PROG]) * x[D] * f
+            fin = ends and own_end == t_fin
+            prog = float(x[LEN]) if fin else x[PROG] + (t_next - now) / (x[D] * f)
+            last = x[LEN] if fin else math.floor(prog)
+            for j in range(math.floor(x[PROG]) + 1, last + 1):
+                t_j = now + (j - x[PROG]) * x[D] * f
+                if record_tokens:
+                    ev.append(TraceEvent(t_j, EventKind.TOKEN_GENERATED, x[RID], j))
+                    ev.append(TraceEvent(t_j, EventKind.ITERATION_COMPLETED, x[RID], t_j - x[LAST]))
+                token_log.append((t_j, x[RID], j))
+                x[LAST] = t_j
+            x[PROG] = prog
+            if fin:
+                finished.append(x)
+        now = t_next
+        for x in finished:
+            live.remove(x)
+            ev.append(TraceEvent(t_fin, EventKind.EVICTED, x[RID], None))
+        start_ready()
+    if executor is not None:
+        _replay_instances(executor, ordered, token_log)
+    trace.sort()
+    return trace
+
+
+def _replay_instances(executor, ordered, token_log) -> None:
+    """Batch-1 decode steps on the device in token order, one KV slot per
+    live instance (slots recycled as instances finish)."""
+    length = {r.request_id: r.actual_output_length for r in ordered}
+    by_rid = {r.request_id: r for r in ordered}
+    streams, free, next_slot = {}, [], 0
+    for _, rid, j in sorted(token_log, key=lambda e: (e[0], e[1], e[2])):
+        bs = streams.get(rid)
+        if bs is None:
+            slot = free.pop() if free else next_slot
+            if slot == next_slot:
+                next_slot += 1
+            bs = _BatchStream("cost")
+            bs.layout.buffer_offset = slot          # this instance's own KV slot
+            executor.on_fuse(rid, bs.layout.fuse_request(rid, 1), by_rid[rid])
+            streams[rid] = bs
+        executor.run_iteration(bs)
+        bs.iteration_index += 1
+        if j == length[rid]:
+            slot = bs.layout.per_request_offset[rid]
+            bs.layout.evict_request(rid)
+            executor.on_evict(rid, slot)
+            free.append(slot)
+            del streams[rid]
+    executor.on_drain(None)

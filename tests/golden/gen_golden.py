@@ -19,6 +19,8 @@ The outputs are small JSON(.gz) fixtures next to this script:
   schedules.json.gz   per-iteration fused-loop dumps + full-trace digests for
                       hand cases, C1-C4 and randomized prop_helpers-style
                       cases (engine.py:128-207)
+  dynbatch.json.gz    run_dynamic_batching traces (baselines.py:51-127)
+  concurrent.json.gz  run_concurrent_instances traces (baselines.py:130-229)
 """
 
 from __future__ import annotations
@@ -333,7 +335,42 @@ def gen_dynbatch():
     _dump("dynbatch.json.gz", {"cases": cases}, gz=True)
 
 
+def gen_concurrent():
+    """run_concurrent_instances traces (baselines.py:130-229, cost.py:112-116)."""
+    from fusionsim.baselines import run_concurrent_instances
+    cases = []
+
+    def add(name, reqs, cost, tp=1, record_tokens=True):
+        tr = run_concurrent_instances(reqs, CostParams(**cost), TPConfig(tp_size=tp),
+                                      record_tokens=record_tokens).format_lines()
+        cases.append({"name": name, "requests": req_json(reqs),
+                      "cost": {k: (v.hex() if isinstance(v, float) else v) for k, v in cost.items()},
+                      "tp": tp, "record_tokens": record_tokens, "trace_sha": sha(tr),
+                      "n_events": len(tr), "trace_head": tr[:80]})
+
+    add("single", [_req(0, 0.0, 3)], {})
+    add("overlap", [_req(0, 0.0, 4), _req(1, 1.0, 2), _req(2, 2.5, 5)], TIGHT)
+    add("same_ready", [_req(i, 0.0, 2 + i) for i in range(4)], TIGHT)
+    add("idle_gap", [_req(0, 0.0, 2), _req(1, 1000.0, 3)], {})
+    add("tp2", [_req(i, 5.0 * i, 3 + i % 4) for i in range(7)], TIGHT, tp=2)
+    for lam in (1, 16, 64):
+        n, mean, lo, hi, mx, il = SCEN["c3"]
+        sc = Scenario(scenario_id="c5", discipline=Discipline.CONCURRENT, n_requests=32,
+                      arrival=PoissonArrival(1000.0 / lam), lengths=UniformLength(lo, hi),
+                      max_output_length=mx, input_len=il)
+        add(f"c5/lam{lam}", build_requests(sc, 1), {}, record_tokens=lam != 64)
+    g = Xorshift64Star(4242)
+    for i in range(30):
+        add(f"rand{i}", random_requests(g), random_cost(g), tp=2 if i % 4 == 0 else 1,
+            record_tokens=i % 5 != 0)
+    _dump("concurrent.json.gz", {"cases": cases}, gz=True)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:
+        globals()["gen_" + sys.argv[1]]()
+        sys.exit(0)
+    gen_concurrent()
     gen_dynbatch()
     gen_rng()
     gen_alg1()
