@@ -21,7 +21,7 @@ from __future__ import annotations
 import math
 from dataclasses import dataclass
 
-from .buffer import BufferLayout
+from .buffer import BufferLayout, Slot
 from .core import Request
 from .cost import CostParams, TPConfig, iteration_time
 from .errors import InvalidParam
@@ -232,7 +232,8 @@ def _replay_instances(executor, ordered, token_log) -> None:
             if slot == next_slot:
                 next_slot += 1
             bs = _BatchStream("cost")
-            bs.layout.buffer_offset = slot          # this instance's own KV slot
+            bs.layout.slots = [Slot(None, 0)] * slot   # this instance's own KV slot
+            bs.layout.buffer_offset = slot
             executor.on_fuse(rid, bs.layout.fuse_request(rid, 1), by_rid[rid])
             streams[rid] = bs
         executor.run_iteration(bs)

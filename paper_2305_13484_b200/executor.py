@@ -205,6 +205,7 @@ class CudaExecutor:
         self._live = {}                   # rid -> dict(P, stop, slot)
         self._orphans = {}                # logical slot -> stale context length
         self._prev_had_new = False
+        self._rows_layout = None
         self._rows_version = None
         self._rows = None
         self._n_rows = self._n_dec = self._n_real_dec = 0
@@ -239,6 +240,7 @@ class CudaExecutor:
         self._new, self._live, self._orphans = [], {}, {}
         self._prev_had_new = False
         self._rows_version = None
+        self._rows_layout = None
         self._rows = None
         self._n_rows = self._n_dec = 0
         self._pre_passes = []
@@ -341,10 +343,14 @@ class CudaExecutor:
     def run_iteration(self, stream) -> float | None:
         layout = stream.layout
         has_new = bool(self._new)
-        changed = has_new or self._prev_had_new or layout.version != self._rows_version
+        # rows are re-uploaded when the window changes -- or when another stream's
+        # layout is served (baselines interleave one layout per instance)
+        changed = (has_new or self._prev_had_new or layout.version != self._rows_version
+                   or layout is not self._rows_layout)
         if changed:
             self._rows, self._n_rows, self._n_dec = self._build_rows(layout)
             self._rows_version = layout.version
+            self._rows_layout = layout
             self.h2d_bytes += self._n_rows * C.sizeof(_lib.Row)
             self._orphan_ctx = sum(r.ctx for r in self._rows[:self._n_dec] if r.kind == _lib.ROW_ORPHAN)
         main_ctx = self._live_ctx + self._orphan_ctx + (self._tail_ctx if changed else 0)
