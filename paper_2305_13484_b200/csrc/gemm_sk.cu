@@ -1119,6 +1119,9 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   const int tiles = ntm * P.ntn;
   static const int align_m = getenv("FL_SK_ALIGN_M") ? atoi(getenv("FL_SK_ALIGN_M")) : 64;
   if (a.M >= align_m && tiles <= nclus) nclus = tiles * (nclus / tiles);
+  // short K (GPT-2 class, K <= 1024): a few whole tiles beat the fix-up of a
+  // stream-K split (fixed cost per launch dominates)
+  else if (a.K <= 1024 && tiles <= nclus) nclus = tiles;
   static const int force_pairs = getenv("FL_SK_PAIRS") ? atoi(getenv("FL_SK_PAIRS")) : 0;
   if (force_pairs > 0 && force_pairs / CN < nclus) nclus = force_pairs / CN;
   // evenly split tiles of the direct epilogues: spread reduction (no owner)
