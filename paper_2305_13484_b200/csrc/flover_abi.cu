@@ -443,10 +443,12 @@ int gemm(fl_handle* h, const void* x, int ldx, const void* w, const void* bias, 
   ps.bytes = (double)N * K * h->es + (double)M * K * h->es + (double)M * N * oes *
              (epi == fl::EPI_ACC_F32 ? 2.0 : 1.0);
   if (fused) *fused = false;
-  // the fused rotary/KV-append epilogue is opt-in: measured slower than the
-  // separate k_rope_append at C3 (per-element sincos + scattered KV stores)
+  // rotary + KV append in the QKV GEMM's epilogue (EPI_QKV; staged through
+  // the smem transpose for GPT-J / GPT-2) is opt-in: it lengthens the QKV
+  // GEMM's exposed epilogue by more than k_rope_append costs (C3 step at 320
+  // rows 7.72 -> 8.10 ms), scattered 8-byte KV stores + sincos per pair
   static const bool fuse = getenv("FL_QKV_FUSE") != nullptr;
-  if (!fuse) rope = nullptr;
+  if (!fuse || !h->p.use_tensor_cores) rope = nullptr;
   if (rope) {
     a.epi = h->p.use_tensor_cores ? fl::EPI_QKV : fl::EPI_STORE;
     a.rope = *rope;

@@ -219,6 +219,7 @@ struct SkParams {
   int kch64;        // K / 64
   int aorder;       // MMA issue order k-step outer, sub-tile inner
   int helpers;      // warps 6-9 help drain the last whole tile
+  int qkv_staged;   // EPI_QKV through final_block (rotary pairs inside a lane's 4 features)
   RopeArgs rope;
   unsigned long long* dbg;   // diagnostics: per CTA [prod wait, prod total, mma wait, mma total]
 };
@@ -276,6 +277,50 @@ FL_DEV void epi_qkv(const SkParams& P, const float* v, int n, bool nok, int mbas
   }
 }
 
+// EPI_QKV through the transpose: lane holds 4 consecutive features (nn..nn+3)
+// of token cb + i*4 + jb for i = 0..7.  Rotary (GPT-J interleaved pairs sit
+// inside the 4 features; GPT-2 has none) + q to q_out + K/V straight into the
+// pool at each row's (slot, pos): what k_rope_append did, without the qkv
+// round trip.
+FL_DEV void qkv_store4(const SkParams& P, const float4* w, int jb, int nn, int m0, int cb, int ncol) {
+  const RopeArgs& rope = P.rope;
+  const int D = rope.Hl * rope.hd;
+  const int sec = nn / D, rem = nn - sec * D;
+  const int hh = rem / rope.hd, ii = rem - hh * rope.hd;
+  const bool rot = sec < 2 && ii < rope.rot;
+  float f0 = 0.f, f1 = 0.f;
+  if (rot) {   // inv_freq of the two pairs (ii, ii+1), (ii+2, ii+3)
+    f0 = exp2f(-(2.f * (ii >> 1) / rope.rot) * 13.287712379549449f);
+    f1 = exp2f(-(2.f * ((ii >> 1) + 1) / rope.rot) * 13.287712379549449f);
+  }
+#pragma unroll 2
+  for (int i = 0; i < 8; ++i) {
+    const int j = i * 4 + jb;
+    if (j >= ncol) continue;
+    const int mg = m0 + cb + j;
+    const int pos = rope.row_pos[mg];
+    float4 x = w[i];
+    if (rot) {
+      float s0, c0, s1, c1;
+      sincosf(static_cast<float>(pos) * f0, &s0, &c0);
+      sincosf(static_cast<float>(pos) * f1, &s1, &c1);
+      x = make_float4(w[i].x * c0 - w[i].y * s0, w[i].y * c0 + w[i].x * s0,
+                      w[i].z * c1 - w[i].w * s1, w[i].w * c1 + w[i].z * s1);
+    }
+    __nv_bfloat162 lo = __floats2bfloat162_rn(x.x, x.y), hi = __floats2bfloat162_rn(x.z, x.w);
+    const uint2 packed = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+    if (sec == 0) {
+      *reinterpret_cast<uint2*>(static_cast<bf16*>(rope.q_out) + static_cast<size_t>(mg) * D + rem) = packed;
+    } else {
+      const fl_row row = rope.rows[mg];
+      if (row.kind != FL_ROW_ORPHAN) {
+        const size_t o = ((((size_t)row.slot * 2 + (sec - 1)) * rope.Hl + hh) * rope.S + pos) * rope.hd + ii;
+        *reinterpret_cast<uint2*>(static_cast<bf16*>(rope.kv_layer) + o) = packed;
+      }
+    }
+  }
+}
+
 // Final epilogue of one 32-token block of a whole tile through the per-warp
 // smem transpose (lane -> 4 weight rows of one token, 16-byte accesses).
 template <int EPI>
@@ -290,7 +335,9 @@ FL_DEV void final_block(const SkParams& P, const uint32_t* r, float bv, float* w
 #pragma unroll
   for (int i = 0; i < 8; ++i) w[i] = *reinterpret_cast<const float4*>(ws_ + (i * 4 + jb) * SK_STG_LD + c4);
   const size_t o0 = static_cast<size_t>(m0 + cb) * P.ldo + nn;
-  if (EPI == EPI_STORE || EPI == EPI_GELU) {
+  if (EPI == EPI_QKV) {
+    qkv_store4(P, w, jb, nn, m0, cb, ncol);
+  } else if (EPI == EPI_STORE || EPI == EPI_GELU) {
     bf16* dst = static_cast<bf16*>(P.out) + o0;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -738,7 +785,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         tmem_ld32(tacc + cb, r);
         const int ncol = min(32, mcount - cb);
         if (P.dbg) e_ld += clock64() - tl0;
-        if ((EPI == EPI_QKV || EPI == EPI_ARGMAX || !vec) && mode == FINAL) {
+        if (((EPI == EPI_QKV && !P.qkv_staged) || EPI == EPI_ARGMAX || !vec) && mode == FINAL) {
           // lane-per-weight-row epilogues (rotary partner / argmax reduce are lanes)
           float v[32];
 #pragma unroll
@@ -843,7 +890,9 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
               w[i].x += q[i].x; w[i].y += q[i].y; w[i].z += q[i].z; w[i].w += q[i].w;
             }
           }
-          if (EPI == EPI_STORE || EPI == EPI_GELU) {
+          if (EPI == EPI_QKV) {
+            qkv_store4(P, w, jb, nn, m0, cb, ncol);
+          } else if (EPI == EPI_STORE || EPI == EPI_GELU) {
             bf16* dst = static_cast<bf16*>(P.out) + static_cast<size_t>(m0 + cb) * P.ldo + nn;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
@@ -1068,8 +1117,10 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   static const int aorder = getenv("FL_SK_AORDER") ? atoi(getenv("FL_SK_AORDER")) : 1;
   P.aorder = aorder;
   static const int helpers = getenv("FL_SK_HELPERS") ? atoi(getenv("FL_SK_HELPERS")) : 1;
+  // staged QKV epilogue: GPT-J (interleaved rotary) and GPT-2 (no rotary)
+  P.qkv_staged = (a.epi == EPI_QKV && a.rope.family != FL_FAMILY_NEOX && a.rope.hd % 32 == 0) ? 1 : 0;
   P.helpers = (helpers && CN == 1 && (a.epi == EPI_STORE || a.epi == EPI_GELU || a.epi == EPI_ACC_F32 ||
-                                      a.epi == EPI_STORE_F32)) ? 1 : 0;
+                                      a.epi == EPI_STORE_F32 || P.qkv_staged)) ? 1 : 0;
   void (*kern)(const CUtensorMap, const CUtensorMap, const SkParams) = nullptr;
   switch (a.epi) {
     case EPI_STORE: kern = k_gemm_sk<EPI_STORE>; break;
