@@ -220,12 +220,14 @@ struct SkParams {
   int aorder;       // MMA issue order k-step outer, sub-tile inner
   int helpers;      // warps 6-9 help drain the last whole tile
   int qkv_staged;   // EPI_QKV through final_block (rotary pairs inside a lane's 4 features)
+  int tpr;          // > 0: ranges of tpr whole tiles (no split tiles) instead of stream-K
   RopeArgs rope;
   unsigned long long* dbg;   // diagnostics: per CTA [prod wait, prod total, mma wait, mma total]
 };
 
 // unit range of cluster q: [q*U/Q, (q+1)*U/Q)
 FL_DEV int range_lo(int q, const SkParams& P) {
+  if (P.tpr) return min(P.units, q * P.tpr * P.kch);    // whole tiles, tpr per range
   return static_cast<int>((static_cast<long long>(q) * P.units) / P.nclus);
 }
 // the cluster whose range holds unit x
@@ -1184,8 +1186,18 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
     if (P.csplit > P.kch) P.csplit = P.kch;             // every piece holds >= 1 K unit
     nclus = tiles * P.csplit;
   }
+  // more tiles than pairs with a single-buffered accumulator (> 256 tokens):
+  // k whole tiles per pair instead of stream-K -- a split tile's fix-up would
+  // stall the MMA mid-range (LM head at 320 rows 140 -> 131 us)
+  P.tpr = 0;
+  static const int force_tpr = getenv("FL_SK_TPR") ? atoi(getenv("FL_SK_TPR")) : -1;
+  if (P.nbuf == 1 && tiles > nclus && P.csplit == 1 && CN == 1 && force_tpr != 0) {
+    const int k = (tiles + nclus - 1) / nclus;
+    P.tpr = k;
+    nclus = (tiles + k - 1) / k;
+  }
   const int cap = (P.units + 3) / 4;                       // >= 4 chunks per range
-  if (nclus > cap && P.csplit == 1) nclus = cap;
+  if (nclus > cap && P.csplit == 1 && !P.tpr) nclus = cap;
   if (nclus < 1) nclus = 1;
   P.nclus = nclus;
   P.npairs = nclus * CN;
