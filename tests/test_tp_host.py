@@ -51,9 +51,11 @@ def test_shards_reassemble(name, world):
     assert all(s["w_lm"].shape[0] <= vl for s in shards)
 
 
-def _tp_forward(spec, shards, rows, kv_store):
+def _tp_forward(spec, shards, rows, kv_store, merged=False):
     """numpy image of enqueue_step at tp = len(shards): returns the greedy
-    token per row via the packed (logit, index) max-reduce."""
+    token per row via the packed (logit, index) max-reduce.  merged: the
+    parallel-residual path of fl_set_merged_out -- per rank [a | f] @
+    [W_o | W_proj]^T, ONE all-reduce per layer, then + b_o + b_proj."""
     world = len(shards)
     w = [{k: v.numpy() for k, v in s.items()} for s in shards]
     hl, hd = spec.n_head // world, spec.head_dim
@@ -67,6 +69,7 @@ def _tp_forward(spec, shards, rows, kv_store):
         h = _ln(x, g(0, "ln1_g"), g(0, "ln1_b"), spec.ln_eps)
         h_mlp = _ln(x, g(0, "ln2_g"), g(0, "ln2_b"), spec.ln_eps) if spec.family == "neox" else h
         y = np.zeros_like(x)                       # all-reduce of attn-out partials
+        a_rank = []
         for r in range(world):
             qkv = h @ g(r, "w_qkv").T + (g(r, "b_qkv") if g(r, "b_qkv") is not None else 0)
             a = np.zeros((len(rows), D), dtype=np.float32)
@@ -84,7 +87,18 @@ def _tp_forward(spec, shards, rows, kv_store):
                 p = np.exp(s - s.max(axis=1, keepdims=True))
                 p /= p.sum(axis=1, keepdims=True)
                 a[i] = np.einsum("hc,chd->hd", p, V).reshape(-1)
-            y += a @ g(r, "w_o").T
+            a_rank.append(a)
+            if not merged:
+                y += a @ g(r, "w_o").T
+        if merged:                                 # one all-reduce of [a|f] @ W_cat^T partials
+            y = np.zeros_like(x)
+            for r in range(world):
+                f = _gelu(h_mlp @ g(r, "w_fc").T + g(r, "b_fc"))
+                wcat = np.concatenate([g(r, "w_o"), g(r, "w_proj")], axis=1)
+                y += np.concatenate([a_rank[r], f], axis=1) @ wcat.T
+            bo = g(0, "b_o") if g(0, "b_o") is not None else 0
+            x = x + y + bo + g(0, "b_proj")
+            continue
         x = x + y + (g(0, "b_o") if g(0, "b_o") is not None else 0)
         if spec.family == "gpt2":
             h_mlp = _ln(x, g(0, "ln2_g"), g(0, "ln2_b"), spec.ln_eps)
@@ -117,6 +131,23 @@ def test_tp_dataflow_matches_unsharded_oracle(name, world):
     got, _ = _tp_forward(spec, shards, rows, store)
     want = orc.step(rows)
     assert got == [int(np.argmax(v)) for v in want]
+
+
+@pytest.mark.parametrize("name,world", [("gptj-mini", 2), ("gptj-mini", 1), ("neox-mini", 4)])
+def test_tp_merged_out_projection_matches_unsharded_oracle(name, world):
+    """The merged out-projection dataflow (one all-reduce per layer) gives the
+    oracle's tokens, as the two-all-reduce dataflow does."""
+    spec = get_spec(name)
+    full = init_weights(spec, seed=1)
+    shards = [init_weights(spec, seed=1, rank=r, world=world) for r in range(world)]
+    orc = GPTOracle.from_spec(spec, {k: v.numpy() for k, v in full.items()}, 64)
+    prompt = [5, 17, 99, 3, 250, 7]
+    rows = [(0, j, t) for j, t in enumerate(prompt)] + [(1, j, t) for j, t in enumerate(prompt[:3])]
+    got, hf = _tp_forward(spec, shards, rows, {}, merged=True)
+    want = orc.step(rows)
+    assert got == [int(np.argmax(v)) for v in want]
+    _, hf2 = _tp_forward(spec, shards, rows, {}, merged=False)
+    assert np.abs(hf - hf2).max() < 1e-3
 
 
 # ---------------------------------------------------------------- gloo, world 2
