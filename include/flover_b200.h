@@ -206,6 +206,17 @@ int fl_gemm(const void* x, int ldx, const void* w, const void* bias, void* out, 
  * pointers are then unused. */
 int fl_set_merged_out(fl_handle* h, const void* const* w_cat, const void* const* b_cat);
 
+/* Parallel-residual families (gptj, neox), tensor-core pools: run the QKV
+ * projection and the FFN up projection as ONE GEMM over the stacked weight
+ * [W_qkv; W_fc] ([3Dl + Fl][d_model], the pool's layout), bias [b_qkv | b_fc]
+ * (zeros where a model has none; b_in may be NULL).  Rows < 3Dl read LN1(x)
+ * and store q|k|v; rows >= 3Dl read the MLP input (GPT-J: LN1(x), NeoX:
+ * LN2(x)) and store GELU(FFN-up): one persistent launch balances both weight
+ * streams over all SMs (QKV alone has fewer 256-row tiles than SM pairs).
+ * Needs 3Dl % 256 == 0.  Call after fl_create, before the first
+ * fl_step; the per-layer W_QKV / W_FC pointers are then unused. */
+int fl_set_merged_in(fl_handle* h, const void* const* w_in, const void* const* b_in);
+
 /* Tensor-core weight layout: bytes of the tiled copy of a bf16 W [N][K]
  * (K % 64 == 0) and the stream-ordered re-layout into `out`.  A pool created
  * with use_tensor_cores = 2 expects every projection weight (w_qkv, w_o, w_fc,

@@ -23,7 +23,7 @@ EXPORTS = ("fl_abi_version", "fl_last_error", "fl_workspace_bytes", "fl_create",
            "fl_gemm_workspace_bytes", "fl_gemm", "fl_profile", "fl_profile_read", "fl_configure",
            "fl_last_duration_ms", "fl_attention_workspace_bytes", "fl_attention",
            "fl_gemm_debug", "fl_plan_shuffle", "fl_tiled_weight_bytes", "fl_tile_weight",
-           "fl_set_merged_out")
+           "fl_set_merged_out", "fl_set_merged_in")
 PROF_ATTENTION, PROF_GEMM, PROF_SHUFFLE, PROF_STEP = 0, 1, 2, 3
 
 
@@ -96,6 +96,7 @@ def load() -> C.CDLL:
                                  C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int,
                                  C.c_void_p]
     lib.fl_set_merged_out.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.fl_set_merged_in.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
     lib.fl_tiled_weight_bytes.restype = C.c_size_t
     lib.fl_tiled_weight_bytes.argtypes = [C.c_int, C.c_int]
     lib.fl_tile_weight.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p]

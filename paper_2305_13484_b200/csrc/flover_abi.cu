@@ -95,11 +95,16 @@ struct fl_handle {
   void *h, *h2, *qkv, *q, *a, *f;
   unsigned long long* keys;
   fl::TcWorkspace tcws;
-  int ldaf = 0;                           // row stride (elements) of a and f
+  int ldaf = 0;                           // row stride (elements) of qkv, a and f (one buffer)
   // merged out-projection (parallel residual): per layer [d][Dl + Fl] weight
   // [W_o | W_proj] and bias b_o + b_proj (fl_set_merged_out)
   std::vector<const void*> wcat, bcat;
   bool merged = false;
+  // merged in-projection (parallel residual): per layer [3Dl + Fl][d] weight
+  // [W_qkv; W_fc] and bias [b_qkv | b_fc] (fl_set_merged_in)
+  std::vector<const void*> win, bin;
+  bool merged_in = false;
+  int merged_in_max_rows = 0;             // windows wider than this run QKV and FFN-up apart
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;
   // live profiling
@@ -228,12 +233,14 @@ Layout plan(const fl_model_desc* m, const fl_pool_desc* p) {
   L.att_ml = c.take(Mr * Hl * ms * 2 * 4);
   L.h = c.take(Mr * d * es);
   L.h2 = c.take(m->family == FL_FAMILY_NEOX ? Mr * d * es : 0);
-  L.qkv = c.take(Mr * 3 * Dl * es);
-  L.q = c.take(Mr * Dl * es);
-  // attention output a and FFN activation f share rows: [Mr][Dl + Fl], so the
-  // parallel-residual families can run attn-out and FFN-down as ONE GEMM over
+  // q|k|v, the attention output a and the FFN activation f share rows:
+  // [Mr][3Dl | Dl | Fl], so the parallel-residual families can run QKV and
+  // FFN-up as ONE GEMM over [W_qkv; W_fc] (fl_set_merged_in; its FFN half
+  // lands after a's columns) and attn-out and FFN-down as ONE GEMM over
   // K = Dl + Fl (fl_set_merged_out)
-  L.a = c.take(Mr * (Dl + Fl) * es);
+  L.qkv = c.take(Mr * (4 * Dl + Fl) * es);
+  L.q = c.take(Mr * Dl * es);
+  L.a = 0;
   L.f = 0;
   L.keys = c.take(Md * 8);
   const int nmax = (3 * Dl > Fl ? 3 * Dl : Fl) > Vl ? (3 * Dl > Fl ? 3 * Dl : Fl) : Vl;
@@ -295,9 +302,9 @@ int fl_create(const fl_model_desc* m, const fl_pool_desc* p, fl_handle** out) {
   h->h2 = w + L.h2;
   h->qkv = w + L.qkv;
   h->q = w + L.q;
-  h->a = w + L.a;
-  h->f = w + L.a + (size_t)h->Dl * h->es;    // same rows, after a's Dl columns
-  h->ldaf = h->Dl + h->Fl;
+  h->a = w + L.qkv + (size_t)3 * h->Dl * h->es;    // same rows, after q|k|v
+  h->f = w + L.qkv + (size_t)4 * h->Dl * h->es;    // after a's Dl columns
+  h->ldaf = 4 * h->Dl + h->Fl;
   h->keys = (unsigned long long*)(w + L.keys);
   if (p->use_tensor_cores) {
     int e = fl::tc_init(&h->tcws, w + L.tc, fl::tc_workspace_bytes(p->max_rows, 0));
@@ -428,9 +435,14 @@ using fl::GemmArgs;
 
 int gemm(fl_handle* h, const void* x, int ldx, const void* w, const void* bias, void* out,
           int ldo, int M, int N, int K, int epi, cudaStream_t s,
-          const fl::RopeArgs* rope = nullptr, bool* fused = nullptr) {
+          const fl::RopeArgs* rope = nullptr, bool* fused = nullptr, const void* x2 = nullptr,
+          int nsplit = 0, int ogap = 0) {
   GemmArgs a{x, w, bias, out, M, N, K, ldx, ldo, epi, h->m.dtype, h->p.max_rows};
   a.w_tiled = h->p.use_tensor_cores == 2 ? 1 : 0;
+  a.x2 = x2;
+  a.nsplit = nsplit;
+  a.ogap = ogap;
+  if (nsplit && !h->p.use_tensor_cores) return FL_EINVAL;
   if (epi == fl::EPI_ARGMAX) {
     a.keys = h->keys;
     a.index_base = h->m.tp_rank * h->Vl;
@@ -505,6 +517,13 @@ int enqueue_step(fl_handle* h, int n_rows, int n_dec, bool want_logits, cudaStre
     void* kvl = kv + kv_layer_elems * es * l;
     // K2 + K3
     fl::launch_layernorm(h->x, W[FL_W_LN1_G], W[FL_W_LN1_B], h->h, n_rows, d, m.ln_eps, dt, s);
+    // MLP input: GPT-2 = LN2 of the updated residual; GPT-J = LN1 output;
+    // NeoX = LN2 of the residual *before* the attention update.
+    if (m.family == FL_FAMILY_NEOX) {
+      fl::launch_layernorm(h->x, W[FL_W_LN2_G], W[FL_W_LN2_B], h->h2, n_rows, d, m.ln_eps, dt, s);
+      fl::g_launches += 1;
+    }
+    const void* mlp_in = m.family == FL_FAMILY_NEOX ? h->h2 : h->h;
     // QKV projection; on the tcgen05 path its epilogue applies the rotary and
     // appends K/V at each row's (slot, pos) itself (EPI_QKV)
     fl::RopeArgs ra;
@@ -518,11 +537,19 @@ int enqueue_step(fl_handle* h, int n_rows, int n_dec, bool want_logits, cudaStre
     ra.family = m.family;
     ra.S = p.max_seq;
     bool qkv_fused = false;
-    FL_GEMM(h->h, d, W[FL_W_QKV], W[FL_W_QKV_B], h->qkv, 3 * Dl, n_rows, 3 * Dl, d, fl::EPI_STORE, s,
-            &ra, &qkv_fused);
+    const bool merged_in = h->merged_in && n_rows <= h->merged_in_max_rows;
+    if (merged_in) {
+      // K3 + K6 as one GEMM over [W_qkv; W_fc]: q|k|v to columns [0, 3Dl),
+      // GELU(FFN-up) to [4Dl, 4Dl + Fl) (the FFN half reads mlp_in)
+      FL_GEMM(h->h, d, h->win[l], h->bin[l], h->qkv, h->ldaf, n_rows, 3 * Dl + Fl, d, fl::EPI_GELU, s,
+              nullptr, nullptr, mlp_in, 3 * Dl, Dl);
+    } else {
+      FL_GEMM(h->h, d, W[FL_W_QKV], W[FL_W_QKV_B], h->qkv, h->ldaf, n_rows, 3 * Dl, d, fl::EPI_STORE, s,
+              &ra, &qkv_fused);
+    }
     if (!qkv_fused) {
       fl::launch_rope_append(h->qkv, h->rows, h->row_pos, n_rows, Hl, hd, m.rotary_dim, m.family,
-                             kvl, p.pool_slots, p.max_seq, h->q, dt, s);
+                             kvl, p.pool_slots, p.max_seq, h->q, dt, s, h->ldaf);
       fl::g_launches += 1;
     }
     // K4
@@ -533,12 +560,6 @@ int enqueue_step(fl_handle* h, int n_rows, int n_dec, bool want_logits, cudaStre
                                              h->att_ml, dt, s, ordered ? h->row_order : nullptr, h->ldaf);
     }
     fl::g_launches += 1;
-    // MLP input: GPT-2 = LN2 of the updated residual; GPT-J = LN1 output;
-    // NeoX = LN2 of the residual *before* the attention update.
-    if (m.family == FL_FAMILY_NEOX) {
-      fl::launch_layernorm(h->x, W[FL_W_LN2_G], W[FL_W_LN2_B], h->h2, n_rows, d, m.ln_eps, dt, s);
-      fl::g_launches += 1;
-    }
     // K5 attn-out (+ all-reduce); merged into K7 for parallel-residual models
     if (h->merged) {
     } else if (tp) {
@@ -549,15 +570,13 @@ int enqueue_step(fl_handle* h, int n_rows, int n_dec, bool want_logits, cudaStre
     } else {
       FL_GEMM(h->a, h->ldaf, W[FL_W_O], W[FL_W_O_B], h->x, d, n_rows, d, Dl, fl::EPI_ACC_F32, s);
     }
-    const void* mlp_in = h->h;  // GPT-J: LN1 output
     if (m.family == FL_FAMILY_GPT2) {
       fl::launch_layernorm(h->x, W[FL_W_LN2_G], W[FL_W_LN2_B], h->h, n_rows, d, m.ln_eps, dt, s);
       fl::g_launches += 1;
-    } else if (m.family == FL_FAMILY_NEOX) {
-      mlp_in = h->h2;
     }
     // K6 + K7 (+ all-reduce)
-    FL_GEMM(mlp_in, d, W[FL_W_FC], W[FL_W_FC_B], h->f, h->ldaf, n_rows, Fl, d, fl::EPI_GELU, s);
+    if (!merged_in)
+      FL_GEMM(mlp_in, d, W[FL_W_FC], W[FL_W_FC_B], h->f, h->ldaf, n_rows, Fl, d, fl::EPI_GELU, s);
     if (h->merged) {
       // x += [a | f] . [W_o | W_proj]^T + b_o + b_proj: one GEMM, one reduction
       // (and one all-reduce under TP instead of two)
@@ -801,6 +820,23 @@ extern "C" int fl_tile_weight(const void* w, int N, int K, void* out, void* stre
   if (!w || !out || N <= 0 || K <= 0 || K % 64) return fail(FL_EINVAL, "bad tile_weight arguments");
   if (fl::launch_tile_weight(w, N, K, out, static_cast<cudaStream_t>(stream)))
     return fail(FL_ECUDA, "tile_weight launch: %s", cudaGetErrorString(cudaGetLastError()));
+  return FL_OK;
+}
+
+extern "C" int fl_set_merged_in(fl_handle* h, const void* const* w_in, const void* const* b_in) {
+  if (!h || !w_in) return fail(FL_EINVAL, "null merged-in argument");
+  if (h->m.family == FL_FAMILY_GPT2)
+    return fail(FL_EINVAL, "merged in-projection needs a parallel-residual family (gptj, neox)");
+  if (!h->p.use_tensor_cores) return fail(FL_EINVAL, "merged in-projection needs the tensor-core path");
+  if (!h->graphs.empty()) return fail(FL_EINVAL, "fl_set_merged_in after the first step");
+  if ((3 * h->Dl) % 256) return fail(FL_EINVAL, "3 * Dl (%d) must be a multiple of 256", 3 * h->Dl);
+  h->win.assign(w_in, w_in + h->m.n_layer);
+  h->bin.assign(h->m.n_layer, nullptr);
+  if (b_in) h->bin.assign(b_in, b_in + h->m.n_layer);
+  for (auto p : h->win)
+    if (!p) return fail(FL_EINVAL, "null merged weight");
+  h->merged_in = true;
+  h->merged_in_max_rows = getenv("FL_MERGED_IN_MAX_ROWS") ? atoi(getenv("FL_MERGED_IN_MAX_ROWS")) : 192;
   return FL_OK;
 }
 

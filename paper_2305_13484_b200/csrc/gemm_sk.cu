@@ -221,9 +221,15 @@ struct SkParams {
   int helpers;      // warps 6-9 help drain the last whole tile
   int qkv_staged;   // EPI_QKV through final_block (rotary pairs inside a lane's 4 features)
   int tpr;          // > 0: ranges of tpr whole tiles (no split tiles) instead of stream-K
+  int nsplit, ogap; // dual GEMM (GemmArgs::nsplit): rows >= nsplit read x2, GELU, column + ogap
   RopeArgs rope;
   unsigned long long* dbg;   // diagnostics: per CTA [prod wait, prod total, mma wait, mma total]
 };
+
+// dual GEMM: output column and activation of weight row n (identity / on
+// for a single GEMM)
+FL_DEV int ocol(const SkParams& P, int n) { return P.nsplit && n >= P.nsplit ? n + P.ogap : n; }
+FL_DEV bool act_on(const SkParams& P, int n) { return !P.nsplit || n >= P.nsplit; }
 
 // unit range of cluster q: [q*U/Q, (q+1)*U/Q)
 FL_DEV int range_lo(int q, const SkParams& P) {
@@ -336,7 +342,8 @@ FL_DEV void final_block(const SkParams& P, const uint32_t* r, float bv, float* w
   float4 w[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) w[i] = *reinterpret_cast<const float4*>(ws_ + (i * 4 + jb) * SK_STG_LD + c4);
-  const size_t o0 = static_cast<size_t>(m0 + cb) * P.ldo + nn;
+  const size_t o0 = static_cast<size_t>(m0 + cb) * P.ldo + ocol(P, nn);
+  const bool act = EPI == EPI_GELU && act_on(P, nn);
   if (EPI == EPI_QKV) {
     qkv_store4(P, w, jb, nn, m0, cb, ncol);
   } else if (EPI == EPI_STORE || EPI == EPI_GELU) {
@@ -346,7 +353,7 @@ FL_DEV void final_block(const SkParams& P, const uint32_t* r, float bv, float* w
       const int j = i * 4 + jb;
       if (j >= ncol) continue;
       float4 x = w[i];
-      if (EPI == EPI_GELU) { x.x = gelu_tanh(x.x); x.y = gelu_tanh(x.y); x.z = gelu_tanh(x.z); x.w = gelu_tanh(x.w); }
+      if (act) { x.x = gelu_tanh(x.x); x.y = gelu_tanh(x.y); x.z = gelu_tanh(x.z); x.w = gelu_tanh(x.w); }
       __nv_bfloat162 lo = __floats2bfloat162_rn(x.x, x.y), hi = __floats2bfloat162_rn(x.z, x.w);
       *reinterpret_cast<uint2*>(dst + static_cast<size_t>(j) * P.ldo) =
           make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
@@ -376,7 +383,7 @@ FL_DEV void final_block(const SkParams& P, const uint32_t* r, float bv, float* w
 template <int EPI>
 __global__ void __launch_bounds__(SK_THREADS, 1)
     k_gemm_sk(const __grid_constant__ CUtensorMap tma_w, const __grid_constant__ CUtensorMap tma_x,
-              const __grid_constant__ SkParams P) {
+              const __grid_constant__ CUtensorMap tma_x2, const __grid_constant__ SkParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[SK_MAXST];
   __shared__ __align__(8) uint64_t empty_bar[SK_MAXST];
@@ -414,6 +421,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_w)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_x)) : "memory");
+    if (P.nsplit) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_x2)) : "memory");
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full_bar[s], 1 + P.mt);   // weight producer + one per token sub-tile
       mbar_init(&empty_bar[s], CN);          // every pair's MMAs consumed the stage
@@ -469,6 +477,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
           }
         }
         const int m0 = cur_m0, n0 = cur_n0, k = cur_k;
+        const CUtensorMap* xm = P.nsplit && n0 >= P.nsplit ? &tma_x2 : &tma_x;   // dual GEMM: 2nd operand
         // weight coordinates: row-major W -> (k, n0); tiled W -> the first
         // row of the contiguous 128 x 64 chunk (tile n0/128, K chunk k/64)
         const int wcol = P.w_tiled ? 0 : k;
@@ -480,14 +489,14 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         else if (role < 0 && KPB > 1)
           tma_load_pair3(&tma_w, &full_bar[st], smem + st * STAGE, n0, k / SK_BK);
         else if (role >= 0 && KPB > 1)
-          tma_load_pair3(&tma_x, &full_bar[st], smem + st * STAGE + AB + role * KPB * XB,
+          tma_load_pair3(xm, &full_bar[st], smem + st * STAGE + AB + role * KPB * XB,
                          m0 + role * P.bn + xi * (P.bn / 2), k / SK_BK);
         else if (role < 0 && CN == 1)
           tma_load_pair(&tma_w, &full_bar[st], smem + st * STAGE, wcol, wrow);
         else if (role < 0)
           tma_load_pair_mc(&tma_w, &full_bar[st], smem + st * STAGE + c * wrows * 128, wcol, wrow + c * wrows, wmask);
         else
-          tma_load_pair(&tma_x, &full_bar[st], smem + st * STAGE + AB + role * XB, k,
+          tma_load_pair(xm, &full_bar[st], smem + st * STAGE + AB + role * XB, k,
                         m0 + role * P.bn + xi * (P.bn / 2));
       };
       const int pre = min(u1 - u0, stages);
@@ -678,7 +687,8 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
 #pragma unroll
         for (int p = 0; p < 4; ++p)
           if (p < S) { acc.x += q[p].x; acc.y += q[p].y; acc.z += q[p].z; acc.w += q[p].w; }
-        const size_t o = static_cast<size_t>(m0 + tok) * P.ldo + nn;
+        const size_t o = static_cast<size_t>(m0 + tok) * P.ldo + ocol(P, nn);
+        const bool act = EPI == EPI_GELU && act_on(P, nn);
         if (nn + 3 < P.N && P.vec) {
           if (EPI == EPI_ACC_F32) {
             float4* d = reinterpret_cast<float4*>(static_cast<float*>(P.out) + o);
@@ -687,7 +697,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
           } else if (EPI == EPI_STORE_F32) {
             *reinterpret_cast<float4*>(static_cast<float*>(P.out) + o) = acc;
           } else {
-            if (EPI == EPI_GELU) {
+            if (act) {
               acc.x = gelu_tanh(acc.x); acc.y = gelu_tanh(acc.y); acc.z = gelu_tanh(acc.z); acc.w = gelu_tanh(acc.w);
             }
             __nv_bfloat162 l2 = __floats2bfloat162_rn(acc.x, acc.y), h2 = __floats2bfloat162_rn(acc.z, acc.w);
@@ -699,7 +709,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
           for (int qq = 0; qq < 4 && nn + qq < P.N; ++qq) {
             if (EPI == EPI_ACC_F32) static_cast<float*>(P.out)[o + qq] += a4[qq];
             else if (EPI == EPI_STORE_F32) static_cast<float*>(P.out)[o + qq] = a4[qq];
-            else static_cast<bf16*>(P.out)[o + qq] = __float2bfloat16_rn(EPI == EPI_GELU ? gelu_tanh(a4[qq]) : a4[qq]);
+            else static_cast<bf16*>(P.out)[o + qq] = __float2bfloat16_rn(act ? gelu_tanh(a4[qq]) : a4[qq]);
           }
         }
       }
@@ -823,13 +833,14 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
             __syncwarp();
             if (lane < ncol && key) atomicMax(&P.keys[m0 + cb + lane], key);
           } else if (nok) {
-            const size_t o0 = static_cast<size_t>(m0 + cb) * P.ldo + n;
+            const size_t o0 = static_cast<size_t>(m0 + cb) * P.ldo + ocol(P, n);
+            const bool act = EPI == EPI_GELU && act_on(P, n);
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
               if (j >= ncol) continue;
               const size_t o = o0 + static_cast<size_t>(j) * P.ldo;
               if (EPI == EPI_STORE || EPI == EPI_GELU)
-                static_cast<bf16*>(P.out)[o] = __float2bfloat16_rn(EPI == EPI_GELU ? gelu_tanh(v[j]) : v[j]);
+                static_cast<bf16*>(P.out)[o] = __float2bfloat16_rn(act ? gelu_tanh(v[j]) : v[j]);
               else if (EPI == EPI_ACC_F32)
                 static_cast<float*>(P.out)[o] += v[j];
               else
@@ -895,13 +906,14 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
           if (EPI == EPI_QKV) {
             qkv_store4(P, w, jb, nn, m0, cb, ncol);
           } else if (EPI == EPI_STORE || EPI == EPI_GELU) {
-            bf16* dst = static_cast<bf16*>(P.out) + static_cast<size_t>(m0 + cb) * P.ldo + nn;
+            bf16* dst = static_cast<bf16*>(P.out) + static_cast<size_t>(m0 + cb) * P.ldo + ocol(P, nn);
+            const bool act = EPI == EPI_GELU && act_on(P, nn);
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
               const int j = i * 4 + jb;
               if (j >= ncol) continue;
               float4 x = w[i];
-              if (EPI == EPI_GELU) { x.x = gelu_tanh(x.x); x.y = gelu_tanh(x.y); x.z = gelu_tanh(x.z); x.w = gelu_tanh(x.w); }
+              if (act) { x.x = gelu_tanh(x.x); x.y = gelu_tanh(x.y); x.z = gelu_tanh(x.z); x.w = gelu_tanh(x.w); }
               __nv_bfloat162 lo = __floats2bfloat162_rn(x.x, x.y), hi = __floats2bfloat162_rn(x.z, x.w);
               *reinterpret_cast<uint2*>(dst + static_cast<size_t>(j) * P.ldo) =
                   make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
@@ -1065,6 +1077,10 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
     g_sk_err = "tensor-core GEMM needs bf16, K % 64 == 0 and 16-byte aligned rows";
     return -1;
   }
+  if (a.nsplit && (a.epi != EPI_GELU || a.nsplit % (2 * SK_BM) || a.nsplit >= a.N || a.ogap < 0)) {
+    g_sk_err = "dual GEMM needs EPI_GELU and a split at a multiple of 256 weight rows";
+    return -1;
+  }
   static bool configured = false;
   if (!configured) {
     for (auto k : {k_gemm_sk<EPI_STORE>, k_gemm_sk<EPI_GELU>, k_gemm_sk<EPI_ACC_F32>, k_gemm_sk<EPI_STORE_F32>,
@@ -1123,7 +1139,7 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   P.qkv_staged = (a.epi == EPI_QKV && a.rope.family != FL_FAMILY_NEOX && a.rope.hd % 32 == 0) ? 1 : 0;
   P.helpers = (helpers && CN == 1 && (a.epi == EPI_STORE || a.epi == EPI_GELU || a.epi == EPI_ACC_F32 ||
                                       a.epi == EPI_STORE_F32 || P.qkv_staged)) ? 1 : 0;
-  void (*kern)(const CUtensorMap, const CUtensorMap, const SkParams) = nullptr;
+  void (*kern)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const SkParams) = nullptr;
   switch (a.epi) {
     case EPI_STORE: kern = k_gemm_sk<EPI_STORE>; break;
     case EPI_GELU: kern = k_gemm_sk<EPI_GELU>; break;
@@ -1210,6 +1226,8 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   P.flags = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + (size_t)SK_MAX_PAIRS * 2 * SK_MAX_SPAN * SK_BM * 4);
   P.rope = a.rope;
   P.dbg = g_sk_dbg;
+  P.nsplit = a.nsplit;
+  P.ogap = a.ogap;
   static const int use_red = getenv("FL_SK_RED") ? atoi(getenv("FL_SK_RED")) : 0;
   P.red = use_red;
   P.vec = (a.ldo % 4 == 0 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0) ? 1 : 0;
@@ -1228,7 +1246,13 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   if (!sk_map({a.x, 0, (uint64_t)(a.mcap > a.M ? a.mcap : a.M), (uint64_t)a.K, (uint64_t)a.ldx * 2, SK_BK,
                (uint32_t)(P.bn / 2), 1, P.kpb}, &mx))
     return -1;
-  cudaError_t e = launch_k(kern, dim3(2 * P.npairs), dim3(SK_THREADS), smem, s, dim3(2 * CN, 1, 1), *mw, *mx, P);
+  CUtensorMap* mx2 = mx;
+  if (a.x2 && a.x2 != a.x &&
+      !sk_map({a.x2, 0, (uint64_t)(a.mcap > a.M ? a.mcap : a.M), (uint64_t)a.K, (uint64_t)a.ldx * 2, SK_BK,
+               (uint32_t)(P.bn / 2), 1, P.kpb}, &mx2))
+    return -1;
+  cudaError_t e = launch_k(kern, dim3(2 * P.npairs), dim3(SK_THREADS), smem, s, dim3(2 * CN, 1, 1), *mw, *mx,
+                           *mx2, P);
   if (e != cudaSuccess) {
     char buf[256];
     snprintf(buf, sizeof buf, "k_gemm_sk launch (pairs %d smem %d stages %d bn %d mt %d): %s", P.npairs, smem,

@@ -753,8 +753,8 @@ int gemm_tc(TcWorkspace* ws, const GemmArgs& a, cudaStream_t s) {
   // selects the per-tile cluster-split kernel below (kept for comparison)
   static const bool legacy = getenv("FL_GEMM_LEGACY") != nullptr;
   if (!legacy) return gemm_sk(ws->base, ws->num_sms, a, s);
-  if (a.w_tiled) {
-    g_tc_err = "tiled weights need the stream-K GEMM (unset FL_GEMM_LEGACY)";
+  if (a.w_tiled || a.nsplit) {
+    g_tc_err = "tiled weights and dual GEMMs need the stream-K GEMM (unset FL_GEMM_LEGACY)";
     return -1;
   }
   MapCache& cache = *static_cast<MapCache*>(ws->maps);

@@ -39,6 +39,12 @@ struct GemmArgs {
   int index_base = 0;                   // EPI_ARGMAX: global index of weight row 0
   RopeArgs rope;                        // EPI_QKV
   int w_tiled = 0;                      // w in the fl_tile_weight layout
+  // two GEMMs over one weight stream [W1; W2] (EPI_GELU only, tcgen05 path):
+  // weight rows n < nsplit read x and store plainly to out column n; rows
+  // n >= nsplit read x2 (null: x) and get GELU, stored to column n + ogap.
+  // nsplit is a multiple of 256 (whole pair tiles on either side).
+  const void* x2 = nullptr;
+  int nsplit = 0, ogap = 0;
 };
 
 // SIMT FFMA GEMM (fp32 path and the reference path for the tensor-core GEMM).
@@ -60,9 +66,10 @@ void launch_add_partial(float* x, const float* y, const void* b1, const void* b2
                         int dtype, cudaStream_t s);
 
 // rotary on q/k, q -> qout [M, Hl*hd]; k/v -> KV pool of this layer at (slot, pos).
+// qkv rows are ldq elements apart (0: 3 * Hl * hd).
 void launch_rope_append(const void* qkv, const fl_row* rows, const int32_t* row_pos, int M,
                         int Hl, int hd, int rot, int family, void* kv_layer, int C, int S,
-                        void* qout, int dtype, cudaStream_t s);
+                        void* qout, int dtype, cudaStream_t s, int ldq = 0);
 
 // split-K masked decode attention over each row's own context.
 int attn_max_splits(int S);

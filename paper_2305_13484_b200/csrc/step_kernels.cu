@@ -110,9 +110,24 @@ __global__ void __launch_bounds__(256) k_layernorm(const float* __restrict__ x,
   for (int c = 0; c < PER; ++c) {
     const int i = (c * blockDim.x + threadIdx.x) * 4;
     if (i < d) {
+      if constexpr (sizeof(T) == 2) {
+        // 8-byte gamma / beta loads and output stores (4 bf16 per thread)
+        const uint2 gr = *reinterpret_cast<const uint2*>(g + i), br = *reinterpret_cast<const uint2*>(b + i);
+        const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gr);
+        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&br);
+        __nv_bfloat162 y[2];
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        o[i + j] = from_f<T>((v[4 * c + j] - mean) * rstd * to_f(g[i + j]) + to_f(b[i + j]));
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const float2 gf = __bfloat1622float2(g2[h2]), bf = __bfloat1622float2(b2[h2]);
+          y[h2] = __floats2bfloat162_rn((v[4 * c + 2 * h2] - mean) * rstd * gf.x + bf.x,
+                                        (v[4 * c + 2 * h2 + 1] - mean) * rstd * gf.y + bf.y);
+        }
+        *reinterpret_cast<uint2*>(o + i) = *reinterpret_cast<const uint2*>(y);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          o[i + j] = from_f<T>((v[4 * c + j] - mean) * rstd * to_f(g[i + j]) + to_f(b[i + j]));
+      }
     }
   }
 }
@@ -175,12 +190,12 @@ template <typename T>
 __global__ void k_rope_append(const T* __restrict__ qkv, const fl_row* __restrict__ rows,
                               const int32_t* __restrict__ row_pos, int Hl, int hd, int rot,
                               int family, T* __restrict__ kv_layer, int C, int S,
-                              T* __restrict__ qout) {
+                              T* __restrict__ qout, int ldq) {
   pdl_trigger();
   pdl_wait();
   const int r = blockIdx.x, h = blockIdx.y, i = threadIdx.x;
   const int D = Hl * hd;
-  const T* base = qkv + static_cast<size_t>(r) * 3 * D + h * hd;
+  const T* base = qkv + static_cast<size_t>(r) * ldq + h * hd;
   float q = to_f(base[i]);
   float k = to_f(base[D + i]);
   const float v = to_f(base[2 * D + i]);
@@ -218,6 +233,18 @@ __global__ void k_rope_append(const T* __restrict__ qkv, const fl_row* __restric
   }
 }
 
+// sin/cos of the rotary angle pos * 10000^(-2j/rot): the fp32 angle (as the
+// precise path forms it) reduced to [-pi, pi] with a two-constant Cody-Waite
+// step, then the SFU sincos -- |error| ~1e-6 against sincosf, which spends
+// hundreds of instructions per call on its general range reduction
+FL_DEV void rope_sincos(float pos, int j, int rot, float* sn, float* cs) {
+  const float x = pos * exp2f(-(2.f * j / rot) * 13.287712379549449f);   // log2(10000)
+  const float kq = rintf(x * 0.15915494309189535f);
+  float rr = fmaf(-kq, 6.28318548202514648f, x);       // 2pi, fp32 head
+  rr = fmaf(-kq, -1.7484556e-07f, rr);                  // 2pi - head
+  __sincosf(rr, sn, cs);
+}
+
 // bf16 variant: one thread per 16-byte vector (8 elements) of q, k and v --
 // 16-byte loads and stores instead of 2-byte ones.  GPT-J's interleaved pairs
 // (2j, 2j+1) sit inside one vector; NeoX's rotate-half partner (i +- rot/2) is
@@ -227,7 +254,7 @@ __global__ void __launch_bounds__(256) k_rope_append_v(const bf16* __restrict__ 
                                                       const int32_t* __restrict__ row_pos, int Hl,
                                                       int hd, int rot, int family,
                                                       bf16* __restrict__ kv_layer, int S,
-                                                      bf16* __restrict__ qout) {
+                                                      bf16* __restrict__ qout, int ldq) {
   pdl_trigger();
   pdl_wait();
   const int r = blockIdx.x;
@@ -236,41 +263,48 @@ __global__ void __launch_bounds__(256) k_rope_append_v(const bf16* __restrict__ 
   if (vec * 8 >= D) return;
   const int e0 = vec * 8;
   const int h = e0 / hd, i0 = e0 - h * hd;
-  const bf16* base = qkv + static_cast<size_t>(r) * 3 * D;
+  const bf16* base = qkv + static_cast<size_t>(r) * ldq;
   float q[8], k[8], v[8];
   load16(base + e0, q);
   load16(base + D + e0, k);
   load16(base + 2 * D + e0, v);
   const int pos = row_pos[r];
   if (rot > 0 && i0 < rot) {
-    float qo[8], ko[8];
+    const float fpos = static_cast<float>(pos);
+    if (family == FL_FAMILY_GPTJ) {
+      // interleaved pairs (2j, 2j+1) sit inside the vector: one sincos per pair
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const int i = i0 + t;
-      if (i >= rot) { qo[t] = q[t]; ko[t] = k[t]; continue; }
-      int j;
-      float sign, qp, kp;
-      if (family == FL_FAMILY_GPTJ) {
-        j = i >> 1;
-        sign = (i & 1) ? 1.f : -1.f;
-        qp = q[t ^ 1];
-        kp = k[t ^ 1];
-      } else {
-        const int half = rot >> 1;
-        j = i < half ? i : i - half;
-        const int partner = i < half ? i + half : i - half;
-        sign = i < half ? -1.f : 1.f;
-        qp = __bfloat162float(base[h * hd + partner]);
-        kp = __bfloat162float(base[D + h * hd + partner]);
+      for (int t = 0; t < 8; t += 2) {
+        if (i0 + t >= rot) break;
+        float sn, cs;
+        rope_sincos(fpos, (i0 + t) >> 1, rot, &sn, &cs);
+        const float q0 = q[t], q1 = q[t + 1], k0 = k[t], k1 = k[t + 1];
+        q[t] = q0 * cs - q1 * sn;
+        q[t + 1] = q1 * cs + q0 * sn;
+        k[t] = k0 * cs - k1 * sn;
+        k[t + 1] = k1 * cs + k0 * sn;
       }
-      const float inv_freq = exp2f(-(2.f * j / rot) * 13.287712379549449f);
-      float sn, cs;
-      sincosf(static_cast<float>(pos) * inv_freq, &sn, &cs);
-      qo[t] = q[t] * cs + sign * qp * sn;
-      ko[t] = k[t] * cs + sign * kp * sn;
-    }
+    } else {
+      // NeoX rotate-half: partner i +- rot/2 read element-wise from the row
+      const int half = rot >> 1;
+      float qo[8], ko[8];
 #pragma unroll
-    for (int t = 0; t < 8; ++t) { q[t] = qo[t]; k[t] = ko[t]; }
+      for (int t = 0; t < 8; ++t) {
+        const int i = i0 + t;
+        if (i >= rot) { qo[t] = q[t]; ko[t] = k[t]; continue; }
+        const int j = i < half ? i : i - half;
+        const int partner = i < half ? i + half : i - half;
+        const float sign = i < half ? -1.f : 1.f;
+        const float qp = __bfloat162float(base[h * hd + partner]);
+        const float kp = __bfloat162float(base[D + h * hd + partner]);
+        float sn, cs;
+        rope_sincos(fpos, j, rot, &sn, &cs);
+        qo[t] = q[t] * cs + sign * qp * sn;
+        ko[t] = k[t] * cs + sign * kp * sn;
+      }
+#pragma unroll
+      for (int t = 0; t < 8; ++t) { q[t] = qo[t]; k[t] = ko[t]; }
+    }
   }
   store16(qout + static_cast<size_t>(r) * D + e0, q);
   const fl_row row = rows[r];
@@ -284,23 +318,24 @@ __global__ void __launch_bounds__(256) k_rope_append_v(const bf16* __restrict__ 
 
 void launch_rope_append(const void* qkv, const fl_row* rows, const int32_t* row_pos, int M,
                         int Hl, int hd, int rot, int family, void* kv_layer, int C, int S,
-                        void* qout, int dtype, cudaStream_t s) {
+                        void* qout, int dtype, cudaStream_t s, int ldq) {
   if (M <= 0) return;
+  if (ldq <= 0) ldq = 3 * Hl * hd;
   dim3 grid(M, Hl);
   if (family == FL_FAMILY_GPT2) rot = 0;
   if (dtype == FL_DTYPE_BF16 && hd % 8 == 0) {
     const int vecs = Hl * hd / 8;
     const int bs = vecs < 256 ? (vecs + 31) / 32 * 32 : 256;
     launch_k(k_rope_append_v, dim3(M, (vecs + bs - 1) / bs), dim3(bs), 0, s, 1, (const bf16*)qkv, rows, row_pos,
-             Hl, hd, rot, family, (bf16*)kv_layer, S, (bf16*)qout);
+             Hl, hd, rot, family, (bf16*)kv_layer, S, (bf16*)qout, ldq);
     return;
   }
   if (dtype == FL_DTYPE_BF16)
     launch_k(k_rope_append<bf16>, dim3(grid), dim3(hd), 0, s, 1, (const bf16*)qkv, rows, row_pos, Hl, hd, rot, family,
-                                            (bf16*)kv_layer, C, S, (bf16*)qout);
+                                            (bf16*)kv_layer, C, S, (bf16*)qout, ldq);
   else
     launch_k(k_rope_append<float>, dim3(grid), dim3(hd), 0, s, 1, (const float*)qkv, rows, row_pos, Hl, hd, rot,
-                                             family, (float*)kv_layer, C, S, (float*)qout);
+                                             family, (float*)kv_layer, C, S, (float*)qout, ldq);
 }
 
 // ---------------------------------------------------------------- K8 greedy argmax

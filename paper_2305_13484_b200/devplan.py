@@ -46,14 +46,17 @@ def device_plan_shuffle(layout: BufferLayout, device="cuda", stream=None) -> Shu
     n = len(occ)
     if n > MAX_WINDOW:
         raise ValueError(f"window of {n} slots > {MAX_WINDOW}")
-    occ_d = torch.tensor(occ or [0], dtype=torch.int32, device=device)
-    size_d = torch.tensor(size or [0], dtype=torch.int64, device=device)
-    out_d = torch.zeros(3 + 2 * max(n, 1), dtype=torch.int32, device=device)
-    bytes_d = torch.zeros(1, dtype=torch.int64, device=device)
-    s = stream if stream is not None else torch.cuda.current_stream()
-    launch_plan(occ_d, size_d, n, layout.buffer_offset, out_d, bytes_d, s.cuda_stream)
-    out = out_d.cpu().tolist()
-    nbytes = int(bytes_d.item())
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    # inputs, kernel and read-back all ordered on one stream (the serving
+    # stream is not torch's current one)
+    with torch.cuda.stream(s):
+        occ_d = torch.tensor(occ or [0], dtype=torch.int32, device=device)
+        size_d = torch.tensor(size or [0], dtype=torch.int64, device=device)
+        out_d = torch.zeros(3 + 2 * max(n, 1), dtype=torch.int32, device=device)
+        bytes_d = torch.zeros(1, dtype=torch.int64, device=device)
+        launch_plan(occ_d, size_d, n, layout.buffer_offset, out_d, bytes_d, s.cuda_stream)
+        out = out_d.cpu().tolist()
+        nbytes = int(bytes_d.item())
     offset, wlen, nm = out[0], out[1], out[2]
     slots = layout.slots
     moves = tuple(ShuffleMove(slots[out[3 + 2 * r]].occupant, out[3 + 2 * r], out[4 + 2 * r],

@@ -102,6 +102,21 @@ class CudaExecutor:
         self.merged = (self.use_tc and spec.family in ("gptj", "neox")
                        and not os.environ.get("FL_NO_MERGED_OUT"))
         self._wcat, self._bcat = [], []
+        # ... and QKV and FFN-up as one GEMM over [W_qkv; W_fc] (rows 3*Dl..
+        # read the MLP input, get GELU, land after the attention output)
+        self.merged_in = (self.use_tc and spec.family in ("gptj", "neox") and (3 * hl * spec.head_dim) % 256 == 0
+                          and not os.environ.get("FL_NO_MERGED_IN"))
+        self._win, self._bin = [], []
+        if self.merged_in:
+            for l in range(spec.n_layer):
+                wq, wf = self.w.pop(f"layers.{l}.w_qkv"), self.w.pop(f"layers.{l}.w_fc")
+                self.w[f"layers.{l}.w_in"] = torch.cat([wq, wf], dim=0).contiguous()
+                bq, bf = self.w.pop(f"layers.{l}.b_qkv", None), self.w.pop(f"layers.{l}.b_fc", None)
+                if bq is not None or bf is not None:
+                    bq = bq if bq is not None else torch.zeros(wq.shape[0], dtype=tdt, device=self.device)
+                    bf = bf if bf is not None else torch.zeros(wf.shape[0], dtype=tdt, device=self.device)
+                    self.w[f"layers.{l}.b_in"] = torch.cat([bq, bf]).contiguous()
+                del wq, wf, bq, bf
         if self.merged:
             for l in range(spec.n_layer):
                 wo, wp = self.w.pop(f"layers.{l}.w_o"), self.w.pop(f"layers.{l}.w_proj")
@@ -112,7 +127,7 @@ class CudaExecutor:
                 if bs:
                     self.w[f"layers.{l}.b_cat"] = sum(bs).to(tdt)
         if self.tiled:
-            names = [f"layers.{l}.{k}" for l in range(spec.n_layer) for k in GEMM_KEYS + ("w_cat",)] + ["w_lm"]
+            names = [f"layers.{l}.{k}" for l in range(spec.n_layer) for k in GEMM_KEYS + ("w_cat", "w_in")] + ["w_lm"]
             for name in names:
                 t = self.w.get(name)
                 if t is None:
@@ -123,6 +138,18 @@ class CudaExecutor:
                                                    C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)))
                 self.w[name] = tt
                 del t
+        if self.merged_in:
+            # windows wider than the library's merged_in_max_rows run QKV and
+            # FFN-up apart over views of the stacked weight (rows 3*Dl.. start
+            # at element 3*Dl*d in both the row-major and the tiled layout)
+            q3 = 3 * hl * spec.head_dim
+            for l in range(spec.n_layer):
+                wi = self.w[f"layers.{l}.w_in"].view(-1)
+                self.w[f"layers.{l}.w_qkv"] = wi[:q3 * spec.d_model]
+                self.w[f"layers.{l}.w_fc"] = wi[q3 * spec.d_model:]
+                bi = self.w.get(f"layers.{l}.b_in")
+                if bi is not None:
+                    self.w[f"layers.{l}.b_qkv"], self.w[f"layers.{l}.b_fc"] = bi[:q3], bi[q3:]
         del weights       # our own row-major copies are freed before the KV pool is sized
         ptrs = []
         for layer in range(spec.n_layer):
@@ -180,6 +207,13 @@ class CudaExecutor:
             self._wcat = (C.c_void_p * len(wc))(*wc)
             self._bcat = (C.c_void_p * len(bc))(*bc)
             _lib.check(self.lib.fl_set_merged_out(self.handle, self._wcat, self._bcat))
+        if self.merged_in:
+            wi = [self.w[f"layers.{l}.w_in"].data_ptr() for l in range(spec.n_layer)]
+            bi = [self.w[f"layers.{l}.b_in"].data_ptr() if f"layers.{l}.b_in" in self.w else None
+                  for l in range(spec.n_layer)]
+            self._win = (C.c_void_p * len(wi))(*wi)
+            self._bin = (C.c_void_p * len(bi))(*bi)
+            _lib.check(self.lib.fl_set_merged_in(self.handle, self._win, self._bin))
         self.use_graphs = use_graphs
         self._lib_timing = False
         _lib.check(self.lib.fl_configure(self.handle, int(use_graphs), 8, 0))

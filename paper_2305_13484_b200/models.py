@@ -71,6 +71,9 @@ SPECS = {
                            lm_std=0.05),
     "neox-mini": ModelSpec("neox-mini", "neox", 2, 384, 4, 96, 768, 2048, rotary_dim=24,
                            lm_std=0.05),
+    # 3 * d_model a multiple of 256: exercises the merged QKV / FFN-up GEMM
+    "neox-mini-w": ModelSpec("neox-mini-w", "neox", 2, 768, 8, 96, 1536, 2048, rotary_dim=24,
+                             lm_std=0.05),
     "gpt2-mini": ModelSpec("gpt2-mini", "gpt2", 2, 256, 4, 64, 1024, 4096, max_pos=1024),
 }
 

@@ -32,6 +32,11 @@ if TILED:
         return t
     WT = [[_tile(w) for w in lw] for lw in W]
     torch.cuda.synchronize()
+QF = "qf" in (os.environ.get("ONLY") or "")     # QKV and FFN-up as one GEMM over [W_qkv; W_fc]
+if QF:
+    WQF = [torch.cat([lw[0], lw[2]], 0) for lw in W]
+    WQFT = [_tile(w) for w in WQF] if TILED else None
+    torch.cuda.synchronize()
 s = torch.cuda.Stream()
 Ms = [int(a) for a in sys.argv[1:]] or [8, 64, 128, 192, 256, 320]
 ONLY = os.environ.get("ONLY")      # e.g. "qkv" or "qkv,o": only these projections (28 cold layers)
@@ -40,6 +45,7 @@ for M in Ms:
     h = torch.randn(M, d, device="cuda").bfloat16()
     qkv = torch.empty(M, 3 * d, device="cuda", dtype=torch.bfloat16)
     f = torch.empty(M, F, device="cuda", dtype=torch.bfloat16)
+    qf = torch.empty(M, 3 * d + F, device="cuda", dtype=torch.bfloat16)
     a = torch.randn(M, d, device="cuda").bfloat16()
     x = torch.zeros(M, d, device="cuda")
     keys = torch.zeros(M, device="cuda", dtype=torch.int64)
@@ -56,12 +62,14 @@ for M in Ms:
             if "qkv" in SEL: gemm(h, W[l][0], qkv, 0, 3 * d, WT[l][0] if WT else None)
             if "o" in SEL: gemm(a, W[l][1], x, 2, d, WT[l][1] if WT else None)
             if "fc" in SEL: gemm(h, W[l][2], f, 1, F, WT[l][2] if WT else None)
+            if "qf" in SEL: gemm(h, WQF[l], qf, 0, 3 * d + F, WQFT[l] if WQFT else None)
             if "proj" in SEL: gemm(f, W[l][3], x, 2, d, WT[l][3] if WT else None)
     def ref():
         for l in range(L):
             if "qkv" in SEL: torch.matmul(h, W[l][0].T, out=qkv)
             if "o" in SEL: torch.matmul(a, W[l][1].T)
             if "fc" in SEL: torch.matmul(h, W[l][2].T, out=f)
+            if "qf" in SEL: torch.matmul(h, WQF[l].T, out=qf)
             if "proj" in SEL: torch.matmul(f, W[l][3].T)
     res = []
     for name, fn in (("ours", ours), ("cublas", ref)):
@@ -77,7 +85,7 @@ for M in Ms:
                 gr.replay()
             e1.record(s); torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / 5
-        wel = sum({"qkv": 3 * d * d, "o": d * d, "fc": d * F, "proj": d * F}[k] for k in SEL)
+        wel = sum({"qkv": 3 * d * d, "o": d * d, "fc": d * F, "proj": d * F, "qf": 3 * d * d + d * F}[k] for k in SEL)
         tf = 2 * M * L * wel / (ms * 1e-3) / 1e12
         gb = L * wel * 2 / (ms * 1e-3) / 1e9
         res.append(f"{name} {1e3 * ms / L:7.1f} us/layer ({tf:5.0f} TF/s, {gb:5.0f} GB/s weights)")
