@@ -836,7 +836,7 @@ extern "C" int fl_set_merged_in(fl_handle* h, const void* const* w_in, const voi
   for (auto p : h->win)
     if (!p) return fail(FL_EINVAL, "null merged weight");
   h->merged_in = true;
-  h->merged_in_max_rows = getenv("FL_MERGED_IN_MAX_ROWS") ? atoi(getenv("FL_MERGED_IN_MAX_ROWS")) : 192;
+  h->merged_in_max_rows = getenv("FL_MERGED_IN_MAX_ROWS") ? atoi(getenv("FL_MERGED_IN_MAX_ROWS")) : 256;
   return FL_OK;
 }
 

@@ -1207,7 +1207,14 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   // stall the MMA mid-range (LM head at 320 rows 140 -> 131 us)
   P.tpr = 0;
   static const int force_tpr = getenv("FL_SK_TPR") ? atoi(getenv("FL_SK_TPR")) : -1;
-  if (P.nbuf == 1 && tiles > nclus && P.csplit == 1 && CN == 1 && force_tpr != 0) {
+  // ... and, from 128 tokens on, also with a double-buffered accumulator: whole
+  // tiles keep the first tile's epilogue under the second tile's MMAs and need
+  // no fix-up (merged QKV + FFN-up, GPT-J step at 128 / 192 / 256 rows -2.8 /
+  // -3.4 / -5 % against stream-K; at 64 / 96 rows, still HBM-bound, stream-K's
+  // balance wins by 8.5 / 0.6 %; tools/host_gap.py)
+  static const int tpr_wide = getenv("FL_SK_TPR_WIDE") ? atoi(getenv("FL_SK_TPR_WIDE")) : 128;
+  if ((P.nbuf == 1 || (tpr_wide > 0 && a.M >= tpr_wide)) && tiles > nclus && P.csplit == 1 && CN == 1 &&
+      force_tpr != 0) {
     const int k = (tiles + nclus - 1) / nclus;
     P.tpr = k;
     nclus = (tiles + k - 1) / k;
