@@ -54,7 +54,10 @@ struct AttnCfg {
   // 8 lanes per key: 3-level shuffle reductions and 4 independent keys per
   // warp-step; a warp-wide 16-byte load then spans 4 K rows (4 wavefronts,
   // the minimum for 512 bytes) so the layout costs no extra bank conflicts
-  static constexpr int G = NextPow2<NV>::v < 8 ? NextPow2<NV>::v : 8;   // lanes per key
+  // (hd 96, bf16: 12 vectors -> 4 lanes x 3 instead of 8 lanes x 2 with a
+  // quarter of the lanes idle, and 2 shuffle levels for 8 keys per warp-step)
+  static constexpr int G0 = NextPow2<NV>::v < 8 ? NextPow2<NV>::v : 8;
+  static constexpr int G = (NV % G0 == 0 || NV % 4 != 0) ? G0 : 4;   // lanes per key
   static constexpr int PER = (NV + G - 1) / G;            // vectors per lane
   static constexpr int KPW = 32 / G;                      // keys per warp-step
   static constexpr int CW = 4;                            // consumer warps

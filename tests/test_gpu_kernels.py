@@ -141,3 +141,43 @@ def test_tcgen05_gemm_tiled_weights(M, N, K, epi):
         assert torch.equal(o1, o2)
     else:
         assert (o1 - o2).abs().max().item() <= 1e-4 * o1.abs().max().item()
+
+
+@pytest.mark.parametrize("hd", [64, 96, 128, 256])
+@pytest.mark.parametrize("M,Hl", [(3, 4), (40, 8), (150, 2)])
+def test_attention_kernel_matches_fp32_reference(hd, M, Hl):
+    """K4 through the C-ABI (fl_attention) against a plain torch fp32 softmax
+    attention over each row's own slot and context (1 <= ctx <= S, ragged;
+    split-K + combine at small M * Hl, single pass at large)."""
+    import ctypes as C
+    from paper_2305_13484_b200 import _lib
+    lib = _lib.load()
+    S = 700
+    Cs = M + 3
+    g = torch.Generator(device="cuda").manual_seed(hd * 1000 + M)
+    kv = torch.randn(Cs, 2, Hl, S, hd, device="cuda", generator=g).bfloat16()
+    q = torch.randn(M, Hl * hd, device="cuda", generator=g).bfloat16()
+    ctx = torch.randint(1, S + 1, (M,), device="cuda", generator=g, dtype=torch.int32)
+    ctx[0] = 1
+    ctx[-1] = S
+    slots = torch.randperm(Cs, device="cuda", generator=g)[:M].to(torch.int32)
+    rows = torch.zeros(M, 6, dtype=torch.int32, device="cuda")
+    rows[:, 0] = slots
+    rows[:, 1] = torch.arange(M, dtype=torch.int32, device="cuda")
+    rows[:, 2] = ctx - 1
+    rows[:, 4] = _lib.ROW_DECODE
+    ws = torch.empty(lib.fl_attention_workspace_bytes(M, Hl, hd, S), dtype=torch.uint8, device="cuda")
+    out = torch.empty(M, Hl * hd, dtype=torch.bfloat16, device="cuda")
+    _lib.check(lib.fl_attention(q.data_ptr(), rows.data_ptr(), ctx.data_ptr(), M, Hl, hd, kv.data_ptr(), Cs, S,
+                                out.data_ptr(), ws.data_ptr(), _lib.FL_DTYPE["bf16"],
+                                C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    ref = torch.empty(M, Hl, hd, device="cuda")
+    qf = q.float().view(M, Hl, hd)
+    for r in range(M):
+        n = int(ctx[r])
+        k = kv[int(slots[r]), 0, :, :n].float()          # [Hl, n, hd]
+        v = kv[int(slots[r]), 1, :, :n].float()
+        p = torch.softmax(torch.einsum("hd,hnd->hn", qf[r], k) / hd ** 0.5, dim=-1)
+        ref[r] = torch.einsum("hn,hnd->hd", p, v)
+    torch.testing.assert_close(out.float().view(M, Hl, hd), ref, atol=2e-2, rtol=2e-2)
