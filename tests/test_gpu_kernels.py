@@ -49,7 +49,10 @@ SHAPES = [(1, 768, 768), (7, 2304, 768), (16, 512, 1024), (55, 3072, 768), (64, 
           (100, 50257, 768), (129, 1536, 4096), (256, 4096, 512), (300, 1000, 256), (17, 128, 64),
           (350, 1536, 4096), (512, 768, 768), (700, 1024, 512), (1000, 384, 256),
           # GPT-J 6B projection shapes at a saturated window (stream-K splits tiles)
-          (320, 12288, 4096), (262, 4096, 16384), (96, 16384, 4096), (5, 4096, 4096)]
+          (320, 12288, 4096), (262, 4096, 16384), (96, 16384, 4096), (5, 4096, 4096),
+          # more 256-row tiles than SM pairs at >= 128 rows: ranges of tpr >= 2
+          # whole tiles (GPT-J merged QKV + FFN-up, NeoX merged, LM head)
+          (192, 28672, 4096), (136, 30720, 6144), (320, 50400, 4096)]
 
 
 @pytest.mark.parametrize("M,N,K", SHAPES)
@@ -118,7 +121,8 @@ def test_shuffle_kernel_bit_exact():
 
 
 @pytest.mark.parametrize("M,N,K", [(8, 12288, 4096), (320, 12288, 4096), (262, 4096, 16384), (100, 50257, 768),
-                                   (300, 1000, 256), (700, 1024, 512), (129, 1536, 4096)])
+                                   (300, 1000, 256), (700, 1024, 512), (129, 1536, 4096),
+                                   (192, 28672, 4096), (136, 30720, 6144)])
 @pytest.mark.parametrize("epi", [EPI_STORE, EPI_ACC])
 def test_tcgen05_gemm_tiled_weights(M, N, K, epi):
     """fl_tile_weight layout ([N/128][K/64][128][64]) + use_tc = 2 gives the
