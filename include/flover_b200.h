@@ -195,6 +195,24 @@ int fl_attention(const void* q, const fl_row* rows, const int32_t* row_ctx, int 
                  void* cuda_stream);
 int fl_gemm(const void* x, int ldx, const void* w, const void* bias, void* out, int ldo, int M,
             int N, int K, int epi, int dtype, int use_tc, void* workspace, void* cuda_stream);
+/* Diagnostic entry, every epilogue: as fl_gemm, plus epi 4 = greedy argmax
+ * (keys[m] = max(keys[m], packed(logit, index_base + n)); keys zeroed by the
+ * caller, out unused) and the dual GEMM of fl_set_merged_in (nsplit > 0,
+ * epi 1: weight rows >= nsplit read x2 and store GELU(.) at column n + ogap;
+ * rows < nsplit read x and store plainly).  use_tc 2: W in fl_tile_weight
+ * layout. */
+int fl_gemm2(const void* x, const void* x2, int ldx, const void* w, const void* bias, void* out,
+             int ldo, int M, int N, int K, int epi, int dtype, int use_tc, int nsplit, int ogap,
+             unsigned long long* keys, int index_base, void* workspace, void* cuda_stream);
+/* fl_gemm / fl_gemm2 re-arm the split-K flags of the caller's workspace on the
+ * stream before every tensor-core call (default 1); timing loops over one
+ * workspace may switch it off (the flags self-reset after each launch). */
+void fl_gemm_set_rearm(int on);
+/* Tuning studies only (tools/): key 0 = programmatic dependent launch (1 on,
+ * 0 off) for every kernel launched afterwards; keys 1-4 override the GEMM's
+ * work decomposition (max pairs, ring stages, K sub-chunks per unit, minimum
+ * units per stream-K range); -1 restores the built-in choice. */
+void fl_gemm_tune(int key, int value);
 
 /* Parallel-residual families (gptj, neox): run the attention output projection
  * and the FFN down projection as ONE GEMM over K = Dl + Fl,
@@ -213,9 +231,11 @@ int fl_set_merged_out(fl_handle* h, const void* const* w_cat, const void* const*
  * and store q|k|v; rows >= 3Dl read the MLP input (GPT-J: LN1(x), NeoX:
  * LN2(x)) and store GELU(FFN-up): one persistent launch balances both weight
  * streams over all SMs (QKV alone has fewer 256-row tiles than SM pairs).
- * Needs 3Dl % 256 == 0.  Call after fl_create, before the first
- * fl_step; the per-layer W_QKV / W_FC pointers are then unused. */
-int fl_set_merged_in(fl_handle* h, const void* const* w_in, const void* const* b_in);
+ * Needs 3Dl % 256 == 0.  Windows of more than max_rows rows (< 0: the
+ * default, 256) run QKV and FFN-up as two GEMMs over views of the stacked
+ * weight (rows [0, 3Dl) and [3Dl, 3Dl + Fl)).  Call after fl_create, before
+ * the first fl_step. */
+int fl_set_merged_in(fl_handle* h, const void* const* w_in, const void* const* b_in, int max_rows);
 
 /* Tensor-core weight layout: bytes of the tiled copy of a bf16 W [N][K]
  * (K % 64 == 0) and the stream-ordered re-layout into `out`.  A pool created

@@ -23,7 +23,7 @@ EXPORTS = ("fl_abi_version", "fl_last_error", "fl_workspace_bytes", "fl_create",
            "fl_gemm_workspace_bytes", "fl_gemm", "fl_profile", "fl_profile_read", "fl_configure",
            "fl_last_duration_ms", "fl_attention_workspace_bytes", "fl_attention",
            "fl_gemm_debug", "fl_plan_shuffle", "fl_tiled_weight_bytes", "fl_tile_weight",
-           "fl_set_merged_out", "fl_set_merged_in")
+           "fl_set_merged_out", "fl_set_merged_in", "fl_gemm2", "fl_gemm_set_rearm", "fl_gemm_tune")
 PROF_ATTENTION, PROF_GEMM, PROF_SHUFFLE, PROF_STEP = 0, 1, 2, 3
 
 
@@ -82,6 +82,13 @@ def load() -> C.CDLL:
     lib.fl_gemm.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
                             C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p,
                             C.c_void_p]
+    lib.fl_gemm2.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                             C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                             C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+    lib.fl_gemm_set_rearm.argtypes = [C.c_int]
+    lib.fl_gemm_set_rearm.restype = None
+    lib.fl_gemm_tune.argtypes = [C.c_int, C.c_int]
+    lib.fl_gemm_tune.restype = None
     lib.fl_profile.argtypes = [C.c_void_p, C.c_int]
     lib.fl_configure.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int]
     lib.fl_last_duration_ms.argtypes = [C.c_void_p, C.POINTER(C.c_float)]
@@ -96,7 +103,7 @@ def load() -> C.CDLL:
                                  C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int,
                                  C.c_void_p]
     lib.fl_set_merged_out.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
-    lib.fl_set_merged_in.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.fl_set_merged_in.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
     lib.fl_tiled_weight_bytes.restype = C.c_size_t
     lib.fl_tiled_weight_bytes.argtypes = [C.c_int, C.c_int]
     lib.fl_tile_weight.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p]

@@ -24,7 +24,7 @@ from dataclasses import dataclass
 from .buffer import BufferLayout, Slot
 from .core import Request
 from .cost import CostParams, TPConfig, iteration_time
-from .errors import InvalidParam
+from .errors import CapacityExceeded, InvalidParam
 from .trace import EventKind, Trace, TraceEvent
 
 
@@ -78,7 +78,11 @@ def run_dynamic_batching(requests, cfg: BatchWindowConfig, params: CostParams,
         raise InvalidParam(f"clock must be 'cost' or 'device', got {clock!r}")
     if clock == "device" and executor is None:
         raise InvalidParam("clock='device' needs an executor")
+    from .engine import check_tp
+    check_tp(tp or TPConfig(), executor, clock)
     tp = tp or TPConfig()
+    from .engine import check_tp
+    check_tp(tp, executor, "cost")
     ordered = sorted(requests, key=lambda r: (r.arrival_time, r.request_id))
     ev = []
     for r in ordered:
@@ -154,6 +158,8 @@ def run_dynamic_batching(requests, cfg: BatchWindowConfig, params: CostParams,
 def run_concurrent_instances(requests, params: CostParams, tp: TPConfig | None = None,
                              record_tokens: bool = True, *, executor=None) -> Trace:
     tp = tp or TPConfig()
+    from .engine import check_tp
+    check_tp(tp, executor, "cost")
     ordered = sorted(requests, key=lambda r: (r.arrival_time, r.request_id))
     ev = []
     for r in ordered:
@@ -230,6 +236,9 @@ def _replay_instances(executor, ordered, token_log) -> None:
         if bs is None:
             slot = free.pop() if free else next_slot
             if slot == next_slot:
+                if next_slot >= executor.C:
+                    # a second live instance would share physical slot s % C
+                    raise CapacityExceeded(f"{next_slot + 1} live instances > KV pool of {executor.C} slots")
                 next_slot += 1
             bs = _BatchStream("cost")
             bs.layout.slots = [Slot(None, 0)] * slot   # this instance's own KV slot

@@ -23,7 +23,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-v", "-I", os.path.join(ROOT, "include")]
 SOURCES = ["flover_abi.cu", "step_kernels.cu", "attention.cu", "shuffle.cu", "gemm_simt.cu",
-           "gemm_tc.cu", "gemm_sk.cu", "planner.cu"]
+           "gemm_sk.cu", "planner.cu"]
 
 
 def _compile(src: str) -> tuple:

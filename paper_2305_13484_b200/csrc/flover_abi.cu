@@ -80,7 +80,7 @@ size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
 namespace fl {
 std::atomic<int64_t> g_launches{0};
-bool g_use_pdl = getenv("FL_NO_PDL") == nullptr;
+bool g_use_pdl = true;
 }
 
 struct fl_handle {
@@ -285,7 +285,6 @@ int fl_create(const fl_model_desc* m, const fl_pool_desc* p, fl_handle** out) {
   h->Vl = (m->vocab + m->tp_size - 1) / m->tp_size;
   h->Vloc = m->vocab - m->tp_rank * h->Vl < h->Vl ? m->vocab - m->tp_rank * h->Vl : h->Vl;
   h->ms = fl::attn_max_splits(p->max_seq);
-  h->use_graphs = getenv("FL_NO_GRAPH") == nullptr;
   char* w = static_cast<char*>(p->workspace);
   h->rows = (fl_row*)(w + L.rows);
   h->row_tok = (int32_t*)(w + L.row_tok);
@@ -434,8 +433,7 @@ namespace {
 using fl::GemmArgs;
 
 int gemm(fl_handle* h, const void* x, int ldx, const void* w, const void* bias, void* out,
-          int ldo, int M, int N, int K, int epi, cudaStream_t s,
-          const fl::RopeArgs* rope = nullptr, bool* fused = nullptr, const void* x2 = nullptr,
+          int ldo, int M, int N, int K, int epi, cudaStream_t s, const void* x2 = nullptr,
           int nsplit = 0, int ogap = 0) {
   GemmArgs a{x, w, bias, out, M, N, K, ldx, ldo, epi, h->m.dtype, h->p.max_rows};
   a.w_tiled = h->p.use_tensor_cores == 2 ? 1 : 0;
@@ -454,23 +452,7 @@ int gemm(fl_handle* h, const void* x, int ldx, const void* w, const void* bias, 
   ps.flops = 2.0 * M * N * K;
   ps.bytes = (double)N * K * h->es + (double)M * K * h->es + (double)M * N * oes *
              (epi == fl::EPI_ACC_F32 ? 2.0 : 1.0);
-  if (fused) *fused = false;
-  // rotary + KV append in the QKV GEMM's epilogue (EPI_QKV; staged through
-  // the smem transpose for GPT-J / GPT-2) is opt-in: it lengthens the QKV
-  // GEMM's exposed epilogue by more than k_rope_append costs (C3 step at 320
-  // rows 7.72 -> 8.10 ms), scattered 8-byte KV stores + sincos per pair
-  static const bool fuse = getenv("FL_QKV_FUSE") != nullptr;
-  if (!fuse || !h->p.use_tensor_cores) rope = nullptr;
-  if (rope) {
-    a.epi = h->p.use_tensor_cores ? fl::EPI_QKV : fl::EPI_STORE;
-    a.rope = *rope;
-  }
-  if (h->p.use_tensor_cores) {
-    const int r = fl::gemm_tc(&h->tcws, a, s);
-    if (r < 0) return FL_ECUDA;
-    if (fused) *fused = rope && r == 0;
-    return FL_OK;
-  }
+  if (h->p.use_tensor_cores) return fl::gemm_tc(&h->tcws, a, s) < 0 ? FL_ECUDA : FL_OK;
   fl::gemm_simt(a, s);
   return FL_OK;
 }
@@ -507,7 +489,7 @@ int enqueue_step(fl_handle* h, int n_rows, int n_dec, bool want_logits, cudaStre
   fl::g_launches += 1;
   const int att_keys = fl::attn_keys_per_split(n_rows * Hl, p.max_seq);
   // rows ranked by descending context once per step (attention's schedule)
-  const bool ordered = n_rows <= 1024 && getenv("FL_ATT_NO_ORDER") == nullptr;
+  const bool ordered = n_rows <= 1024;
   if (ordered) {
     fl::launch_row_order(h->row_ctx, n_rows, h->row_order, s);
     fl::g_launches += 1;
@@ -524,34 +506,19 @@ int enqueue_step(fl_handle* h, int n_rows, int n_dec, bool want_logits, cudaStre
       fl::g_launches += 1;
     }
     const void* mlp_in = m.family == FL_FAMILY_NEOX ? h->h2 : h->h;
-    // QKV projection; on the tcgen05 path its epilogue applies the rotary and
-    // appends K/V at each row's (slot, pos) itself (EPI_QKV)
-    fl::RopeArgs ra;
-    ra.rows = h->rows;
-    ra.row_pos = h->row_pos;
-    ra.kv_layer = kvl;
-    ra.q_out = h->q;
-    ra.Hl = Hl;
-    ra.hd = hd;
-    ra.rot = m.family == FL_FAMILY_GPT2 ? 0 : m.rotary_dim;
-    ra.family = m.family;
-    ra.S = p.max_seq;
-    bool qkv_fused = false;
     const bool merged_in = h->merged_in && n_rows <= h->merged_in_max_rows;
     if (merged_in) {
       // K3 + K6 as one GEMM over [W_qkv; W_fc]: q|k|v to columns [0, 3Dl),
       // GELU(FFN-up) to [4Dl, 4Dl + Fl) (the FFN half reads mlp_in)
       FL_GEMM(h->h, d, h->win[l], h->bin[l], h->qkv, h->ldaf, n_rows, 3 * Dl + Fl, d, fl::EPI_GELU, s,
-              nullptr, nullptr, mlp_in, 3 * Dl, Dl);
+              mlp_in, 3 * Dl, Dl);
     } else {
-      FL_GEMM(h->h, d, W[FL_W_QKV], W[FL_W_QKV_B], h->qkv, h->ldaf, n_rows, 3 * Dl, d, fl::EPI_STORE, s,
-              &ra, &qkv_fused);
+      FL_GEMM(h->h, d, W[FL_W_QKV], W[FL_W_QKV_B], h->qkv, h->ldaf, n_rows, 3 * Dl, d, fl::EPI_STORE, s);
     }
-    if (!qkv_fused) {
-      fl::launch_rope_append(h->qkv, h->rows, h->row_pos, n_rows, Hl, hd, m.rotary_dim, m.family,
-                             kvl, p.pool_slots, p.max_seq, h->q, dt, s, h->ldaf);
-      fl::g_launches += 1;
-    }
+    // rotary on q/k, q -> h->q, k/v appended to the pool at each row's (slot, pos)
+    fl::launch_rope_append(h->qkv, h->rows, h->row_pos, n_rows, Hl, hd, m.rotary_dim, m.family,
+                           kvl, p.pool_slots, p.max_seq, h->q, dt, s, h->ldaf);
+    fl::g_launches += 1;
     // K4
     {
       ProfScope ps(h, FL_PROF_ATTENTION, s);
@@ -739,17 +706,36 @@ extern "C" int fl_shuffle(fl_handle* h, const int32_t* moves, int n, void* strea
 namespace {
 fl::TcWorkspace g_dbg_ws;
 void* g_dbg_base = nullptr;
+bool g_dbg_rearm = true;
+}
+
+extern "C" void fl_gemm_set_rearm(int on) { g_dbg_rearm = on != 0; }
+
+// Diagnostics for tuning studies (tools/): key 0 programmatic dependent
+// launch on/off for every kernel; keys 1-4 the GEMM's work decomposition
+// (gemm_sk.cu g_tune); value -1 restores the built-in choice.
+extern "C" void fl_gemm_tune(int key, int value) {
+  if (key == 0) fl::g_use_pdl = value != 0;
+  else fl::sk_tune(key, value);
 }
 
 extern "C" size_t fl_gemm_workspace_bytes(void) { return fl::tc_workspace_bytes(0, 0); }
 extern "C" void fl_gemm_debug(unsigned long long* dev_counters) { fl::tc_set_debug(dev_counters); }
 
-extern "C" int fl_gemm(const void* x, int ldx, const void* w, const void* bias, void* out, int ldo,
-                       int M, int N, int K, int epi, int dtype, int use_tc, void* workspace,
-                       void* stream) {
-  if (!x || !w || !out || M < 1 || N < 1 || K < 1) return fail(FL_EINVAL, "bad gemm arguments");
+extern "C" int fl_gemm2(const void* x, const void* x2, int ldx, const void* w, const void* bias, void* out,
+                        int ldo, int M, int N, int K, int epi, int dtype, int use_tc, int nsplit, int ogap,
+                        unsigned long long* keys, int index_base, void* workspace, void* stream) {
+  if (!x || !w || M < 1 || N < 1 || K < 1) return fail(FL_EINVAL, "bad gemm arguments");
+  if (epi == fl::EPI_ARGMAX ? !keys || !use_tc : !out) return fail(FL_EINVAL, "bad gemm output");
+  if (epi < fl::EPI_STORE || epi > fl::EPI_ARGMAX) return fail(FL_EINVAL, "bad epilogue %d", epi);
+  if (nsplit && !use_tc) return fail(FL_EINVAL, "dual GEMM needs the tensor-core path");
   fl::GemmArgs a{x, w, bias, out, M, N, K, ldx, ldo, epi, dtype, M};
   a.w_tiled = use_tc == 2 ? 1 : 0;
+  a.x2 = x2;
+  a.nsplit = nsplit;
+  a.ogap = ogap;
+  a.keys = keys;
+  a.index_base = index_base;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (use_tc) {
     if (g_dbg_base != workspace) {
@@ -759,15 +745,23 @@ extern "C" int fl_gemm(const void* x, int ldx, const void* w, const void* bias, 
       g_dbg_base = workspace;
     }
     // the caller's scratch may have been reused by the allocator: re-arm the
-    // stream-K flags on the stream every call (diagnostic path only)
-    static const bool no_rearm = getenv("FL_GEMM_NO_REARM") != nullptr;   // timing loops
-    if (!no_rearm) FL_CUDA(fl::sk_rearm(workspace, s));
+    // stream-K flags on the stream every call (diagnostic path only; timing
+    // loops over one workspace switch it off with fl_gemm_set_rearm)
+    if (g_dbg_rearm) FL_CUDA(fl::sk_rearm(workspace, s));
     if (fl::gemm_tc(&g_dbg_ws, a, s)) return fail(FL_EINVAL, "%s", fl::tc_last_error());
   } else {
     fl::gemm_simt(a, s);
   }
   FL_CUDA(cudaGetLastError());
   return FL_OK;
+}
+
+extern "C" int fl_gemm(const void* x, int ldx, const void* w, const void* bias, void* out, int ldo,
+                       int M, int N, int K, int epi, int dtype, int use_tc, void* workspace,
+                       void* stream) {
+  if (epi == fl::EPI_ARGMAX) return fail(FL_EINVAL, "argmax epilogue: use fl_gemm2");
+  return fl_gemm2(x, nullptr, ldx, w, bias, out, ldo, M, N, K, epi, dtype, use_tc, 0, 0, nullptr, 0,
+                  workspace, stream);
 }
 
 extern "C" size_t fl_attention_workspace_bytes(int M, int Hl, int hd, int S) {
@@ -823,7 +817,8 @@ extern "C" int fl_tile_weight(const void* w, int N, int K, void* out, void* stre
   return FL_OK;
 }
 
-extern "C" int fl_set_merged_in(fl_handle* h, const void* const* w_in, const void* const* b_in) {
+extern "C" int fl_set_merged_in(fl_handle* h, const void* const* w_in, const void* const* b_in,
+                                int max_rows) {
   if (!h || !w_in) return fail(FL_EINVAL, "null merged-in argument");
   if (h->m.family == FL_FAMILY_GPT2)
     return fail(FL_EINVAL, "merged in-projection needs a parallel-residual family (gptj, neox)");
@@ -836,7 +831,9 @@ extern "C" int fl_set_merged_in(fl_handle* h, const void* const* w_in, const voi
   for (auto p : h->win)
     if (!p) return fail(FL_EINVAL, "null merged weight");
   h->merged_in = true;
-  h->merged_in_max_rows = getenv("FL_MERGED_IN_MAX_ROWS") ? atoi(getenv("FL_MERGED_IN_MAX_ROWS")) : 256;
+  // above 256 rows the accumulator is single-buffered: QKV and FFN-up run
+  // apart over views of the stacked weight (measured)
+  h->merged_in_max_rows = max_rows < 0 ? 256 : max_rows;
   return FL_OK;
 }
 

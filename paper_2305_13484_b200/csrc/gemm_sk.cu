@@ -53,6 +53,9 @@ constexpr int SK_RING_BUDGET = 200 * 1024;
 constexpr int SK_STG_LD = 36;              // transpose row stride (floats): conflict-free
 
 thread_local std::string g_sk_err;
+// diagnostic overrides (fl_gemm_tune; -1 = the built-in choice): 1 max pairs,
+// 2 ring stages, 3 K sub-chunks per unit, 4 min units per stream-K range
+int g_tune[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
 unsigned long long* g_sk_dbg = nullptr;
 
 FL_DEV uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -114,16 +117,6 @@ FL_DEV void tma_load_pair3(const CUtensorMap* map, uint64_t* bar, void* dst, int
       "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(0), "r"(row), "r"(kc)
       : "memory");
 }
-// 2-SM load multicast to the CTAs of `mask` (same smem offset in each);
-// complete_tx lands on each destination pair's leader barrier
-FL_DEV void tma_load_pair_mc(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1, uint16_t mask) {
-  const uint32_t leader_bar = smem_u32(bar) & 0xFEFFFFFFu;
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
-      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1), "h"(mask)
-      : "memory");
-}
 FL_DEV void mma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -142,13 +135,6 @@ FL_DEV uint32_t cluster_ctarank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
   return r;
-}
-FL_DEV float4 ld_dsmem_f4(const void* local, uint32_t rank) {
-  uint32_t remote;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local)), "r"(rank));
-  float4 v;
-  asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(remote));
-  return v;
 }
 FL_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 FL_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -179,9 +165,6 @@ FL_DEV void tmem_ld32(uint32_t taddr, uint32_t* r) {
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
-FL_DEV void red_add_v4(float* p, float a, float b, float c, float d) {
-  asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
-}
 FL_DEV unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -189,6 +172,9 @@ FL_DEV unsigned ld_acquire(const unsigned* p) {
 }
 FL_DEV void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+FL_DEV void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 FL_DEV void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }   // the 4 epilogue warps
 
@@ -199,7 +185,10 @@ struct SkParams {
   int mt, bn;       // token sub-tiles per tile and their width (UMMA N)
   int span;         // tokens per token tile (mt * bn)
   int stages, ncols, nbuf;
-  int units, npairs;
+  int units;        // ntm * ntn * kch
+  int npairs;       // pairs in the grid = work ranges
+  int dpw;          // whole tiles per pair in the data-parallel prefix (see pair_ranges)
+  int nsk;          // pairs sharing the stream-K units after the prefix (<= npairs)
   const bf16* bias;
   void* out;
   unsigned long long* keys;
@@ -208,21 +197,14 @@ struct SkParams {
   unsigned* flags;  // [npairs][2]
   int slot_elems;   // floats per (pair, half) slot
   int vec;          // out rows 16-byte aligned: vector stores
-  int red;          // EPI_ACC_F32 split tiles: red.add pieces (else owner fix-up)
   int csplit;       // >1: tile K split evenly over S pairs, spread reduction
-  int cn;           // pairs per cluster: token slices sharing multicast weight tiles
-  int nclus;        // clusters (work ranges)
   int slice;        // tokens per pair (mt * bn)
   int kpb;          // 64-wide K sub-chunks per unit/stage (2: one 3-D request per operand)
   int ntm;          // token tiles
   int w_tiled;      // weights in the fl_tile_weight layout [N/128][K/64][128][64]
   int kch64;        // K / 64
-  int aorder;       // MMA issue order k-step outer, sub-tile inner
   int helpers;      // warps 6-9 help drain the last whole tile
-  int qkv_staged;   // EPI_QKV through final_block (rotary pairs inside a lane's 4 features)
-  int tpr;          // > 0: ranges of tpr whole tiles (no split tiles) instead of stream-K
   int nsplit, ogap; // dual GEMM (GemmArgs::nsplit): rows >= nsplit read x2, GELU, column + ogap
-  RopeArgs rope;
   unsigned long long* dbg;   // diagnostics: per CTA [prod wait, prod total, mma wait, mma total]
 };
 
@@ -231,102 +213,43 @@ struct SkParams {
 FL_DEV int ocol(const SkParams& P, int n) { return P.nsplit && n >= P.nsplit ? n + P.ogap : n; }
 FL_DEV bool act_on(const SkParams& P, int n) { return !P.nsplit || n >= P.nsplit; }
 
-// unit range of cluster q: [q*U/Q, (q+1)*U/Q)
-FL_DEV int range_lo(int q, const SkParams& P) {
-  if (P.tpr) return min(P.units, q * P.tpr * P.kch);    // whole tiles, tpr per range
-  return static_cast<int>((static_cast<long long>(q) * P.units) / P.nclus);
+// Work of pair q (unit index = tile * kch + K unit): a data-parallel prefix
+// of dpw whole tiles [q*dpw, (q+1)*dpw), then an equal share of the units
+// left after the npairs*dpw prefix tiles (stream-K) if q < nsk.  dpw = 0:
+// pure stream-K (or the even split of csplit); no remainder: pure whole
+// tiles.  Every pair streams the same number of weight bytes, all SMs busy
+// whatever N/256 is.  nsk <= the remaining units, so no stream-K range is
+// empty: every pair between a split tile's owner and its last piece holds a
+// piece and publishes it (an empty one would leave the owner waiting).
+struct Ranges {
+  int lo[2], hi[2];
+};
+FL_DEV Ranges pair_ranges(const SkParams& P, int q) {
+  Ranges r;
+  const int dpu = P.dpw * P.kch;
+  r.lo[0] = q * dpu;
+  r.hi[0] = r.lo[0] + dpu;
+  const int base = dpu * P.npairs, ur = P.units - base;
+  const int qs = q < P.nsk ? q : P.nsk;
+  r.lo[1] = base + static_cast<int>((static_cast<long long>(qs) * ur) / P.nsk);
+  r.hi[1] = q < P.nsk ? base + static_cast<int>((static_cast<long long>(q + 1) * ur) / P.nsk) : r.lo[1];
+  return r;
 }
-// the cluster whose range holds unit x
+// the pair whose stream-K range holds unit x (x past the whole-tile prefix)
 FL_DEV int owner_of(int x, const SkParams& P) {
-  return static_cast<int>(((static_cast<long long>(x) + 1) * P.nclus + P.units - 1) / P.units) - 1;
+  const int base = P.dpw * P.kch * P.npairs, ur = P.units - base;
+  return static_cast<int>(((static_cast<long long>(x - base) + 1) * P.nsk + ur - 1) / ur) - 1;
 }
-
-// EPI_QKV epilogue of 32 token columns [mbase, mbase+ncol) of this thread's
-// weight row n (full sums, bias included): rotary on q/k, q -> q_out, k/v ->
-// the KV pool at each row's (slot, pos) -- what k_rope_append does.
-FL_DEV void epi_qkv(const SkParams& P, const float* v, int n, bool nok, int mbase, int ncol, int lane) {
-  const RopeArgs& rope = P.rope;
-  const int D = rope.Hl * rope.hd;
-  const int sec = n / D, rem = n - sec * D;
-  const int hh = rem / rope.hd, ii = rem - hh * rope.hd;
-  const bool rot_row = sec < 2 && ii < rope.rot;
-  int src = lane, jf = 0;
-  float sgn = 0.f;
-  if (rope.family == FL_FAMILY_GPTJ) {
-    src = lane ^ 1; jf = ii >> 1; sgn = (ii & 1) ? 1.f : -1.f;
-  } else if (rope.family == FL_FAMILY_NEOX) {
-    const int half = rope.rot >> 1;
-    src = ii < half ? lane + half : lane - half;
-    jf = ii < half ? ii : ii - half;
-    sgn = ii < half ? -1.f : 1.f;
-  }
-  src = rot_row ? src : lane;
-  const float inv_freq = exp2f(-(2.f * jf / max(rope.rot, 1)) * 13.287712379549449f);
-#pragma unroll 4
-  for (int j = 0; j < 32; ++j) {
-    if (j >= ncol) break;
-    float x = v[j];
-    const float xp = __shfl_sync(0xffffffffu, x, src);
-    const int mg = mbase + j;
-    const int pos = rope.row_pos[mg];
-    if (rot_row) {
-      float sn, cs;
-      sincosf(static_cast<float>(pos) * inv_freq, &sn, &cs);
-      x = x * cs + sgn * xp * sn;
-    }
-    if (!nok) continue;
-    if (sec == 0) {
-      static_cast<bf16*>(rope.q_out)[static_cast<size_t>(mg) * D + rem] = __float2bfloat16_rn(x);
-    } else if (rope.rows[mg].kind != FL_ROW_ORPHAN) {
-      const size_t slot = rope.rows[mg].slot;
-      const size_t o = (((slot * 2 + (sec - 1)) * rope.Hl + hh) * rope.S + pos) * rope.hd + ii;
-      static_cast<bf16*>(rope.kv_layer)[o] = __float2bfloat16_rn(x);
-    }
-  }
-}
-
-// EPI_QKV through the transpose: lane holds 4 consecutive features (nn..nn+3)
-// of token cb + i*4 + jb for i = 0..7.  Rotary (GPT-J interleaved pairs sit
-// inside the 4 features; GPT-2 has none) + q to q_out + K/V straight into the
-// pool at each row's (slot, pos): what k_rope_append did, without the qkv
-// round trip.
-FL_DEV void qkv_store4(const SkParams& P, const float4* w, int jb, int nn, int m0, int cb, int ncol) {
-  const RopeArgs& rope = P.rope;
-  const int D = rope.Hl * rope.hd;
-  const int sec = nn / D, rem = nn - sec * D;
-  const int hh = rem / rope.hd, ii = rem - hh * rope.hd;
-  const bool rot = sec < 2 && ii < rope.rot;
-  float f0 = 0.f, f1 = 0.f;
-  if (rot) {   // inv_freq of the two pairs (ii, ii+1), (ii+2, ii+3)
-    f0 = exp2f(-(2.f * (ii >> 1) / rope.rot) * 13.287712379549449f);
-    f1 = exp2f(-(2.f * ((ii >> 1) + 1) / rope.rot) * 13.287712379549449f);
-  }
-#pragma unroll 2
-  for (int i = 0; i < 8; ++i) {
-    const int j = i * 4 + jb;
-    if (j >= ncol) continue;
-    const int mg = m0 + cb + j;
-    const int pos = rope.row_pos[mg];
-    float4 x = w[i];
-    if (rot) {
-      float s0, c0, s1, c1;
-      sincosf(static_cast<float>(pos) * f0, &s0, &c0);
-      sincosf(static_cast<float>(pos) * f1, &s1, &c1);
-      x = make_float4(w[i].x * c0 - w[i].y * s0, w[i].y * c0 + w[i].x * s0,
-                      w[i].z * c1 - w[i].w * s1, w[i].w * c1 + w[i].z * s1);
-    }
-    __nv_bfloat162 lo = __floats2bfloat162_rn(x.x, x.y), hi = __floats2bfloat162_rn(x.z, x.w);
-    const uint2 packed = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
-    if (sec == 0) {
-      *reinterpret_cast<uint2*>(static_cast<bf16*>(rope.q_out) + static_cast<size_t>(mg) * D + rem) = packed;
-    } else {
-      const fl_row row = rope.rows[mg];
-      if (row.kind != FL_ROW_ORPHAN) {
-        const size_t o = ((((size_t)row.slot * 2 + (sec - 1)) * rope.Hl + hh) * rope.S + pos) * rope.hd + ii;
-        *reinterpret_cast<uint2*>(static_cast<bf16*>(rope.kv_layer) + o) = packed;
-      }
-    }
-  }
+// one segment = the part of one tile inside one range
+struct Seg {
+  int t, klo, khi;
+};
+FL_DEV Seg seg_at(int u, int hi, int kch) {
+  Seg g;
+  g.t = u / kch;
+  g.klo = u - g.t * kch;
+  g.khi = min(kch, g.klo + (hi - u));
+  return g;
 }
 
 // Final epilogue of one 32-token block of a whole tile through the per-warp
@@ -344,9 +267,7 @@ FL_DEV void final_block(const SkParams& P, const uint32_t* r, float bv, float* w
   for (int i = 0; i < 8; ++i) w[i] = *reinterpret_cast<const float4*>(ws_ + (i * 4 + jb) * SK_STG_LD + c4);
   const size_t o0 = static_cast<size_t>(m0 + cb) * P.ldo + ocol(P, nn);
   const bool act = EPI == EPI_GELU && act_on(P, nn);
-  if (EPI == EPI_QKV) {
-    qkv_store4(P, w, jb, nn, m0, cb, ncol);
-  } else if (EPI == EPI_STORE || EPI == EPI_GELU) {
+  if (EPI == EPI_STORE || EPI == EPI_GELU) {
     bf16* dst = static_cast<bf16*>(P.out) + o0;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -398,25 +319,26 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
   unsigned long long g_start = 0;
   if (P.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
   const int xi = blockIdx.x & 1;                 // position in the pair (cluster rank)
-  const int pair = blockIdx.x >> 1;              // global pair id = clu * CN + c
+  const int pair = blockIdx.x >> 1;              // pair id = work range
   const bool leader = xi == 0;
-  const uint32_t crank = cluster_ctarank();
-  const uint32_t prank = crank & ~1u;            // the pair's leader in the cluster
+  const uint32_t prank = cluster_ctarank() & ~1u;   // the pair's leader in the cluster
   const uint16_t pmask = static_cast<uint16_t>(3u << prank);
-  const int CN = P.cn;
-  const int c = static_cast<int>(crank >> 1);    // token slice of this pair in the cluster
-  const int clu = pair / CN;
-  // weight rows are multicast to the same-half CTA of every pair of the cluster
-  uint16_t wmask = 0;
-  for (int q = 0; q < CN; ++q) wmask |= static_cast<uint16_t>(1u << (2 * q + xi));
-  const uint16_t allmask = static_cast<uint16_t>((1u << (2 * CN)) - 1u);
-  const int wrows = SK_BM / CN;                  // weight rows this CTA loads per chunk
   const int XB = (P.bn / 2) * SK_BK * 2;         // this CTA's half of a token sub-tile (64 K)
   const int KPB = P.kpb;                         // 64-wide K sub-chunks per unit
   const int AB = KPB * SK_A_BYTES;               // weight bytes per stage and CTA
   const int STAGE = AB + P.mt * KPB * XB;
   const int stages = P.stages, kch = P.kch;
-  const int u0 = range_lo(clu, P), u1 = range_lo(clu + 1, P);
+  const Ranges R = pair_ranges(P, pair);
+  const int n0u = R.hi[0] - R.lo[0], nunits = n0u + R.hi[1] - R.lo[1];
+  // segments of this pair's work, and the last one (helpers drain it)
+  int nseg = 0;
+  Seg last{0, 0, 0};
+  for (int r = 0; r < 2; ++r)
+    for (int u = R.lo[r]; u < R.hi[r];) {
+      last = seg_at(u, R.hi[r], kch);
+      u += last.khi - last.klo;
+      ++nseg;
+    }
 
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_w)) : "memory");
@@ -424,7 +346,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
     if (P.nsplit) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_x2)) : "memory");
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full_bar[s], 1 + P.mt);   // weight producer + one per token sub-tile
-      mbar_init(&empty_bar[s], CN);          // every pair's MMAs consumed the stage
+      mbar_init(&empty_bar[s], 1);           // the pair's MMAs consumed the stage
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull_bar[b], 1);
@@ -451,32 +373,22 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
     // its issuing thread ~250 cycles, tools/probes/tma_rate.cu)
     const int role = warp == 0 ? -1 : warp == 8 ? -2 : warp - 6;   // -1/-2: weight parts, j >= 0: token sub-tile j
     if (lane == 0 && role < P.mt && role >= -1) {
-      auto coords = [&](int u, int& m0, int& n0, int& k) {
-        const int t = u / kch;
-        const int kk = u - t * kch;
-        k = kk * SK_BK * KPB;
-        const int tm = t / P.ntn, tn = t - tm * P.ntn;
-        m0 = tm * P.span + c * P.slice;          // this pair's token slice
-        n0 = tn * 2 * SK_BM + xi * SK_BM;
-      };
       const uint32_t my_tx = 2u * (role < 0 ? AB : KPB * XB);   // both CTAs' bytes
       // units are issued strictly in order: walk the coordinates incrementally
-      // (no divisions on the producer's critical path)
-      int cur_u = u0, cur_m0, cur_n0, cur_k;
-      coords(u0, cur_m0, cur_n0, cur_k);
-      int cur_kk = cur_k / (SK_BK * KPB), cur_t = u0 / kch;
+      // (divisions only at a tile boundary or the jump to the stream-K range)
+      int cur_u = -2, cur_kk = 0, cur_m0 = 0, cur_n0 = 0;
       auto issue = [&](int u, int st) {
-        if (u != cur_u) {                     // advance by one unit
-          cur_u = u;
-          if (++cur_kk == kch) {
-            cur_kk = 0;
-            ++cur_t;
-            coords(u, cur_m0, cur_n0, cur_k);
-          } else {
-            cur_k += SK_BK * KPB;
-          }
+        if (u == cur_u + 1 && cur_kk + 1 < kch) {
+          ++cur_kk;
+        } else {
+          const int t = u / kch;
+          cur_kk = u - t * kch;
+          const int tm = t / P.ntn, tn = t - tm * P.ntn;
+          cur_m0 = tm * P.span;
+          cur_n0 = tn * 2 * SK_BM + xi * SK_BM;
         }
-        const int m0 = cur_m0, n0 = cur_n0, k = cur_k;
+        cur_u = u;
+        const int m0 = cur_m0, n0 = cur_n0, k = cur_kk * SK_BK * KPB;
         const CUtensorMap* xm = P.nsplit && n0 >= P.nsplit ? &tma_x2 : &tma_x;   // dual GEMM: 2nd operand
         // weight coordinates: row-major W -> (k, n0); tiled W -> the first
         // row of the contiguous 128 x 64 chunk (tile n0/128, K chunk k/64)
@@ -491,25 +403,24 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         else if (role >= 0 && KPB > 1)
           tma_load_pair3(xm, &full_bar[st], smem + st * STAGE + AB + role * KPB * XB,
                          m0 + role * P.bn + xi * (P.bn / 2), k / SK_BK);
-        else if (role < 0 && CN == 1)
-          tma_load_pair(&tma_w, &full_bar[st], smem + st * STAGE, wcol, wrow);
         else if (role < 0)
-          tma_load_pair_mc(&tma_w, &full_bar[st], smem + st * STAGE + c * wrows * 128, wcol, wrow + c * wrows, wmask);
+          tma_load_pair(&tma_w, &full_bar[st], smem + st * STAGE, wcol, wrow);
         else
           tma_load_pair(xm, &full_bar[st], smem + st * STAGE + AB + role * XB, k,
                         m0 + role * P.bn + xi * (P.bn / 2));
       };
-      const int pre = min(u1 - u0, stages);
+      auto unit = [&](int i) { return i < n0u ? R.lo[0] + i : R.lo[1] + (i - n0u); };
+      const int pre = min(nunits, stages);
       if (role >= 0) pdl_wait();            // activations are the predecessor's output
-      for (int i = 0; i < pre; ++i) issue(u0 + i, i);   // weights stream ahead of the wait
+      for (int i = 0; i < pre; ++i) issue(unit(i), i);   // weights stream ahead of the wait
       int s = pre % stages;
       uint32_t ph = pre == stages ? 1u : 0u;
       unsigned long long waited = 0, t_start = clock64();
-      for (int u = u0 + pre; u < u1; ++u) {
+      for (int i = pre; i < nunits; ++i) {
         const unsigned long long tw = P.dbg ? clock64() : 0;
         mbar_wait(&empty_bar[s], ph ^ 1);
         if (P.dbg) waited += clock64() - tw;
-        issue(u, s);
+        issue(unit(i), s);
         if (++s == stages) { s = 0; ph ^= 1; }
       }
       if (P.dbg && role == -1) {
@@ -522,21 +433,13 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       // ---- helpers: the odd 32-token blocks of the pair's last segment when
       // it is a whole tile (the ring is idle once its accumulator is full, so
       // the transpose buffers live there)
-      int seg = 0, u = u0, t = 0, klo = 0, khi = 0;
-      for (;;) {
-        t = u / kch;
-        klo = u - t * kch;
-        khi = min(kch, klo + (u1 - u));
-        if (u + (khi - klo) >= u1) break;
-        u += khi - klo;
-        ++seg;
-      }
+      const int seg = nseg - 1, t = last.t, klo = last.klo, khi = last.khi;
       const int tm = t / P.ntn, tn = t - tm * P.ntn;
-      const int m0 = tm * P.span + c * P.slice;
+      const int m0 = tm * P.span;
       const int mcount = min(P.slice, P.M - m0);
       const int nbase = tn * 2 * SK_BM + xi * SK_BM;
       const bool vec = P.vec && nbase + SK_BM <= P.N;
-      if (vec && klo == 0 && khi == kch && u0 < u1) {
+      if (vec && klo == 0 && khi == kch && nseg > 0) {
         const int quarter = warp & 3;
         const int n = nbase + quarter * 32 + lane;
         const float bv = (P.bias && n < P.N) ? __bfloat162float(P.bias[n]) : 0.f;
@@ -560,10 +463,10 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       int s = 0, seg = 0;
       uint32_t ph = 0;
       unsigned long long waited = 0, twait = 0, lat = 0, nlat = 0, t_start = clock64();
-      for (int u = u0; u < u1;) {
-        const int t = u / kch;
-        const int klo = u - t * kch;
-        const int khi = min(kch, klo + (u1 - u));
+      for (int r = 0; r < 2; ++r)
+      for (int u = R.lo[r]; u < R.hi[r];) {
+        const Seg g = seg_at(u, R.hi[r], kch);
+        const int klo = g.klo, khi = g.khi;
         const int b = P.nbuf == 2 ? (seg & 1) : 0;
         const uint32_t use = P.nbuf == 2 ? (seg >> 1) : seg;
         unsigned long long tw = P.dbg ? clock64() : 0;
@@ -584,7 +487,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
           const uint8_t* st = smem + s * STAGE;
           for (int kc = 0; kc < KPB; ++kc) {
             const uint64_t ad = desc_sw128(st + kc * SK_A_BYTES);
-            if (P.mt == 2 && P.aorder) {
+            if (P.mt == 2) {
               // consecutive MMAs share the weight slab (A) across the two token sub-tiles
               const uint64_t bd0 = desc_sw128(st + AB + kc * XB), bd1 = desc_sw128(st + AB + (KPB + kc) * XB);
 #pragma unroll
@@ -601,7 +504,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
                 mma_pair(acc + j * P.bn, ad + 2 * kk, bd + 2 * kk, idesc, (c > klo) | kc | kk);
             }
           }
-          commit_pair(&empty_bar[s], CN == 1 ? pmask : allmask);
+          commit_pair(&empty_bar[s], pmask);
           if (++s == stages) { s = 0; ph ^= 1; }
         }
         commit_pair(&tfull_bar[b], pmask);
@@ -628,9 +531,9 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       // [s, s+1) * mcount / S over the S slots and runs the epilogue -- the
       // fix-up is spread over the S pairs instead of serialised in one owner.
       const int S = P.csplit;
-      const int t = u0 / kch, piece = clu - t * S;
+      const int t = R.lo[1] / kch, piece = pair - t * S;
       const int tm = t / P.ntn, tn = t - tm * P.ntn;
-      const int m0 = tm * P.span + c * P.slice;   // this pair's token slice
+      const int m0 = tm * P.span;
       const int mcount = min(P.slice, P.M - m0);
       const int nbase = tn * 2 * SK_BM + xi * SK_BM;
       const uint32_t tacc = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
@@ -656,63 +559,88 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         }
         __syncwarp();
       }
-      __threadfence();
+      // publish -> arrive: the CTA barrier orders every thread's partial
+      // stores before one thread's gpu-scope release (CUTLASS's semaphore
+      // pattern; a __threadfence in every thread costs ~1 us here)
+      const unsigned long long tf0 = P.dbg ? clock64() : 0;
       epi_bar();
-      unsigned* arrive = P.flags + 2 * SK_MAX_PAIRS + ((t * CN + c) * 2 + xi);
+      unsigned* arrive = P.flags + 2 * SK_MAX_PAIRS + (t * 2 + xi);
       unsigned* done = arrive + 2 * SK_MAX_PAIRS;
       if (warp == 2 && lane == 0) {
-        atomicAdd(arrive, 1u);
+        red_release_add(arrive, 1u);
         long long spins = 0;
         while (ld_acquire(arrive) < static_cast<unsigned>(S)) {
-          __nanosleep(64);
+          __nanosleep(32);
           if (++spins > (1ll << 26)) __trap();
         }
       }
       epi_bar();
-      // reduce my token slice: warp (quarter) takes tokens, lane = 4 weight rows
+      if (P.dbg) e_flag += clock64() - tf0;
+      const unsigned long long tb0 = P.dbg ? clock64() : 0;
+      // reduce my token slice: warp (quarter) takes tokens, lane = 4 weight
+      // rows.  The partials come from L2 (other SMs wrote them): UN tokens'
+      // loads (x S pieces, + the residual for ACC) are issued before any is
+      // used, or the loop runs at one L2 round trip per token
       const int lo = piece * mcount / S, hi = (piece + 1) * mcount / S;
       const int rrow = lane * 4;                      // row within this CTA's 128
       const int nn = nbase + rrow;
       float b4[4] = {0.f, 0.f, 0.f, 0.f};
       if (P.bias)
         for (int q = 0; q < 4; ++q) b4[q] = nn + q < P.N ? __bfloat162float(P.bias[nn + q]) : 0.f;
-      for (int tok = lo + quarter; tok < hi; tok += 4) {
-        float4 acc = make_float4(b4[0], b4[1], b4[2], b4[3]);
-        float4 q[4];
+      const bool act = EPI == EPI_GELU && act_on(P, nn);
+      const bool v4 = nn + 3 < P.N && P.vec;
+      const float* slot0 = P.part + static_cast<size_t>((t * S) * 2 + xi) * P.slot_elems + rrow;
+      const size_t pstride = static_cast<size_t>(2) * P.slot_elems;   // next piece's slot
+      constexpr int UN = 4;
+      for (int tok0 = lo + quarter; tok0 < hi; tok0 += 4 * UN) {
+        float4 q[UN][4];
+        float4 y[UN];
 #pragma unroll
-        for (int p = 0; p < 4; ++p)
-          if (p < S)
-            q[p] = *reinterpret_cast<const float4*>(P.part + static_cast<size_t>(((t * S + p) * CN + c) * 2 + xi) * P.slot_elems +
-                                                    static_cast<size_t>(tok) * SK_BM + rrow);
+        for (int u = 0; u < UN; ++u) {
+          const int tok = tok0 + 4 * u;
 #pragma unroll
-        for (int p = 0; p < 4; ++p)
-          if (p < S) { acc.x += q[p].x; acc.y += q[p].y; acc.z += q[p].z; acc.w += q[p].w; }
-        const size_t o = static_cast<size_t>(m0 + tok) * P.ldo + ocol(P, nn);
-        const bool act = EPI == EPI_GELU && act_on(P, nn);
-        if (nn + 3 < P.N && P.vec) {
-          if (EPI == EPI_ACC_F32) {
-            float4* d = reinterpret_cast<float4*>(static_cast<float*>(P.out) + o);
-            const float4 y = *d;
-            *d = make_float4(y.x + acc.x, y.y + acc.y, y.z + acc.z, y.w + acc.w);
-          } else if (EPI == EPI_STORE_F32) {
-            *reinterpret_cast<float4*>(static_cast<float*>(P.out) + o) = acc;
-          } else {
-            if (act) {
-              acc.x = gelu_tanh(acc.x); acc.y = gelu_tanh(acc.y); acc.z = gelu_tanh(acc.z); acc.w = gelu_tanh(acc.w);
-            }
-            __nv_bfloat162 l2 = __floats2bfloat162_rn(acc.x, acc.y), h2 = __floats2bfloat162_rn(acc.z, acc.w);
-            *reinterpret_cast<uint2*>(static_cast<bf16*>(P.out) + o) =
-                make_uint2(*reinterpret_cast<uint32_t*>(&l2), *reinterpret_cast<uint32_t*>(&h2));
+          for (int p = 0; p < 4; ++p)
+            q[u][p] = (p < S && tok < hi) ? *reinterpret_cast<const float4*>(slot0 + p * pstride + static_cast<size_t>(tok) * SK_BM)
+                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+          y[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (EPI == EPI_ACC_F32 && v4 && tok < hi)
+            y[u] = *reinterpret_cast<const float4*>(static_cast<float*>(P.out) + static_cast<size_t>(m0 + tok) * P.ldo + nn);
+        }
+#pragma unroll
+        for (int u = 0; u < UN; ++u) {
+          const int tok = tok0 + 4 * u;
+          if (tok >= hi) break;
+          float4 acc = make_float4(b4[0], b4[1], b4[2], b4[3]);
+#pragma unroll
+          for (int p = 0; p < 4; ++p) {
+            acc.x += q[u][p].x; acc.y += q[u][p].y; acc.z += q[u][p].z; acc.w += q[u][p].w;
           }
-        } else {
-          const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
-          for (int qq = 0; qq < 4 && nn + qq < P.N; ++qq) {
-            if (EPI == EPI_ACC_F32) static_cast<float*>(P.out)[o + qq] += a4[qq];
-            else if (EPI == EPI_STORE_F32) static_cast<float*>(P.out)[o + qq] = a4[qq];
-            else static_cast<bf16*>(P.out)[o + qq] = __float2bfloat16_rn(act ? gelu_tanh(a4[qq]) : a4[qq]);
+          const size_t o = static_cast<size_t>(m0 + tok) * P.ldo + ocol(P, nn);
+          if (v4) {
+            if (EPI == EPI_ACC_F32) {
+              *reinterpret_cast<float4*>(static_cast<float*>(P.out) + o) =
+                  make_float4(y[u].x + acc.x, y[u].y + acc.y, y[u].z + acc.z, y[u].w + acc.w);
+            } else if (EPI == EPI_STORE_F32) {
+              *reinterpret_cast<float4*>(static_cast<float*>(P.out) + o) = acc;
+            } else {
+              if (act) {
+                acc.x = gelu_tanh(acc.x); acc.y = gelu_tanh(acc.y); acc.z = gelu_tanh(acc.z); acc.w = gelu_tanh(acc.w);
+              }
+              __nv_bfloat162 l2 = __floats2bfloat162_rn(acc.x, acc.y), h2 = __floats2bfloat162_rn(acc.z, acc.w);
+              *reinterpret_cast<uint2*>(static_cast<bf16*>(P.out) + o) =
+                  make_uint2(*reinterpret_cast<uint32_t*>(&l2), *reinterpret_cast<uint32_t*>(&h2));
+            }
+          } else {
+            const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+            for (int qq = 0; qq < 4 && nn + qq < P.N; ++qq) {
+              if (EPI == EPI_ACC_F32) static_cast<float*>(P.out)[o + qq] += a4[qq];
+              else if (EPI == EPI_STORE_F32) static_cast<float*>(P.out)[o + qq] = a4[qq];
+              else static_cast<bf16*>(P.out)[o + qq] = __float2bfloat16_rn(act ? gelu_tanh(a4[qq]) : a4[qq]);
+            }
           }
         }
       }
+      if (P.dbg) e_blk += clock64() - tb0;
       epi_bar();
       if (warp == 2 && lane == 0) {
         // the last reader re-arms both counters for the next launch
@@ -724,14 +652,14 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       }
       tc_fence_before();
     }
-    for (int u = u0; u < u1 && P.csplit == 1;) {
-      const int t = u / kch;
-      const int klo = u - t * kch;
-      const int khi = min(kch, klo + (u1 - u));
+    for (int r = 0; r < 2 && P.csplit == 1; ++r)
+    for (int u = R.lo[r]; u < R.hi[r];) {
+      const Seg g = seg_at(u, R.hi[r], kch);
+      const int t = g.t, klo = g.klo, khi = g.khi;
       const int b = P.nbuf == 2 ? (seg & 1) : 0;
       const uint32_t use = P.nbuf == 2 ? (seg >> 1) : seg;
       const int tm = t / P.ntn, tn = t - tm * P.ntn;
-      const int m0 = tm * P.span + c * P.slice;   // this pair's token slice
+      const int m0 = tm * P.span;
       const int mcount = min(P.slice, P.M - m0);
       const int nbase = tn * 2 * SK_BM + xi * SK_BM;
       const int n = nbase + row;
@@ -746,21 +674,19 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       tc_fence_after();
 
       // segment mode: final epilogue (whole tile, or the k = 0 owner of a split
-      // tile after folding in the later pieces), red.add (split residual tile),
-      // or publish (a later piece of a split tile)
-      enum { FINAL = 0, RED = 1, PUB = 2 };
-      int mode = FINAL, plast = clu;      // plast: last cluster holding a piece
+      // tile after folding in the later pieces) or publish (a later piece of a
+      // split tile: the first segment of its pair's stream-K range)
+      enum { FINAL = 0, PUB = 2 };
+      int mode = FINAL, plast = pair;      // plast: last pair holding a piece
       if (!whole) {
-        if (EPI == EPI_ACC_F32 && P.red) {
-          mode = RED;
-        } else if (klo > 0) {
+        if (klo > 0) {
           mode = PUB;
         } else {
           plast = owner_of((t + 1) * kch - 1, P);
           const unsigned long long tf0 = P.dbg ? clock64() : 0;
           if (warp == 2 && lane == 0) {
-            for (int q = clu + 1; q <= plast; ++q) {
-              const unsigned* f = &P.flags[(q * CN + c) * 2 + xi];
+            for (int q = pair + 1; q <= plast; ++q) {
+              const unsigned* f = &P.flags[q * 2 + xi];
               long long spins = 0;
               while (ld_acquire(f) == 0u) {
                 __nanosleep(64);
@@ -782,7 +708,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       const bool vec = P.vec && nbase + SK_BM <= P.N;
       // last whole tile with helpers: warps 6-9 (done producing) drain the odd
       // 32-token blocks, these warps the even ones
-      const bool helped = P.helpers && vec && whole && u + (khi - klo) >= u1;
+      const bool helped = P.helpers && vec && whole && seg == nseg - 1;
       if (helped) {
         float* ws_ = stg + quarter * (32 * SK_STG_LD);
         for (int cb = 0; cb < mcount; cb += 64) {
@@ -797,13 +723,12 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         tmem_ld32(tacc + cb, r);
         const int ncol = min(32, mcount - cb);
         if (P.dbg) e_ld += clock64() - tl0;
-        if (((EPI == EPI_QKV && !P.qkv_staged) || EPI == EPI_ARGMAX || !vec) && mode == FINAL) {
-          // lane-per-weight-row epilogues (rotary partner / argmax reduce are lanes)
+        if ((EPI == EPI_ARGMAX || !vec) && mode == FINAL) {
+          // lane-per-weight-row epilogues (argmax reduce, unaligned outputs)
           float v[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) + bv;
-          for (int qc = clu + 1; qc <= plast; ++qc) {
-            const int p = qc * CN + c;
+          for (int p = pair + 1; p <= plast; ++p) {
             const float* slot = P.part + static_cast<size_t>(p * 2 + xi) * P.slot_elems + cb * SK_BM + row;
             float q[32];
 #pragma unroll
@@ -811,9 +736,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] += q[j];
           }
-          if (EPI == EPI_QKV) {
-            epi_qkv(P, v, n, nok, m0 + cb, ncol, lane);
-          } else if (EPI == EPI_ARGMAX) {
+          if (EPI == EPI_ARGMAX) {
             // transpose through smem (stride 33: conflict-free both ways) so
             // lane t scans token t's 32 weight rows: 64 shared accesses per
             // block instead of 10 shuffles per token
@@ -849,15 +772,6 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
           }
           continue;
         }
-        if (!vec && mode == RED) {
-          if (nok) {
-            float* dst = static_cast<float*>(P.out) + static_cast<size_t>(m0 + cb) * P.ldo + n;
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (j < ncol) atomicAdd(dst + static_cast<size_t>(j) * P.ldo, __uint_as_float(r[j]) + bv);
-          }
-          continue;
-        }
         // ---- staged: lane -> token j = (i*32+lane)/8, weight rows c4..c4+3
         float* ws_ = stg + quarter * (32 * SK_STG_LD);
 #pragma unroll
@@ -874,22 +788,11 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
             if (j < ncol)
               *reinterpret_cast<float4*>(dst + j * SK_BM) = *reinterpret_cast<const float4*>(ws_ + j * SK_STG_LD + c4);
           }
-        } else if (mode == RED) {
-          float* dst = static_cast<float*>(P.out) + static_cast<size_t>(m0 + cb) * P.ldo + nn;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int j = i * 4 + jb;
-            if (j < ncol) {
-              const float4 w = *reinterpret_cast<const float4*>(ws_ + j * SK_STG_LD + c4);
-              red_add_v4(dst + static_cast<size_t>(j) * P.ldo, w.x, w.y, w.z, w.w);
-            }
-          }
         } else {
           float4 w[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) w[i] = *reinterpret_cast<const float4*>(ws_ + (i * 4 + jb) * SK_STG_LD + c4);
-          for (int qc = clu + 1; qc <= plast; ++qc) {
-            const int p = qc * CN + c;
+          for (int p = pair + 1; p <= plast; ++p) {
             const float* slot = P.part + static_cast<size_t>(p * 2 + xi) * P.slot_elems +
                                 static_cast<size_t>(cb) * SK_BM + quarter * 32 + c4;
             float4 q[8];
@@ -903,9 +806,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
               w[i].x += q[i].x; w[i].y += q[i].y; w[i].z += q[i].z; w[i].w += q[i].w;
             }
           }
-          if (EPI == EPI_QKV) {
-            qkv_store4(P, w, jb, nn, m0, cb, ncol);
-          } else if (EPI == EPI_STORE || EPI == EPI_GELU) {
+          if (EPI == EPI_STORE || EPI == EPI_GELU) {
             bf16* dst = static_cast<bf16*>(P.out) + static_cast<size_t>(m0 + cb) * P.ldo + ocol(P, nn);
             const bool act = EPI == EPI_GELU && act_on(P, nn);
 #pragma unroll
@@ -947,13 +848,12 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       const unsigned long long tb1 = P.dbg ? clock64() : 0;
       if (P.dbg) e_blk += tb1 - tb0;
       if (mode == PUB) {
-        __threadfence();
-        epi_bar();
+        epi_bar();      // every thread's partial stores before the release
         if (warp == 2 && lane == 0) st_release(&P.flags[pair * 2 + xi], 1u);
-      } else if (plast > clu) {
+      } else if (plast > pair) {
         epi_bar();
         if (warp == 2 && lane == 0)
-          for (int q = clu + 1; q <= plast; ++q) P.flags[(q * CN + c) * 2 + xi] = 0u;   // re-arm
+          for (int q = pair + 1; q <= plast; ++q) P.flags[q * 2 + xi] = 0u;   // re-arm
       }
       // this buffer may be overwritten by the next-but-one segment
       tc_fence_before();
@@ -1050,6 +950,9 @@ size_t sk_workspace_bytes() {
 }
 
 const char* sk_last_error() { return g_sk_err.c_str(); }
+void sk_tune(int key, int value) {
+  if (key >= 1 && key < 8) g_tune[key] = value;
+}
 void sk_set_debug(unsigned long long* p) { g_sk_dbg = p; }
 
 int sk_init(void* base, size_t bytes) {
@@ -1084,7 +987,7 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
     for (auto k : {k_gemm_sk<EPI_STORE>, k_gemm_sk<EPI_GELU>, k_gemm_sk<EPI_ACC_F32>, k_gemm_sk<EPI_STORE_F32>,
-                   k_gemm_sk<EPI_ARGMAX>, k_gemm_sk<EPI_QKV>})
+                   k_gemm_sk<EPI_ARGMAX>})
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SK_RING_BUDGET + 1024);
     configured = true;
   }
@@ -1093,52 +996,38 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   P.N = a.N;
   P.ldo = a.ldo;
   P.epi = a.epi;
-  // two 64-wide K sub-chunks per unit when the deeper stage still leaves >= 4
-  // stages (narrow windows) -- decided below once the token tiling is known
-  P.kpb = 1;
-  P.kch = a.K / SK_BK;
   P.ntn = (a.N + 2 * SK_BM - 1) / (2 * SK_BM);
-  // CN pairs per cluster split the token tile into slices and share (multicast)
-  // every weight chunk; CN = 1: the whole window (<= 512 tokens) in one pair
-  static const int force_cn = getenv("FL_SK_CN") ? atoi(getenv("FL_SK_CN")) : 0;
-  int CN = 1;
-  if (force_cn == 1 || force_cn == 2 || force_cn == 4) CN = force_cn;
-  const int smax = CN == 1 ? SK_MAX_SPAN : 256;           // tokens per pair
-  const int ntm = (a.M + CN * smax - 1) / (CN * smax);
+  // token tiling: the whole window (<= 512 tokens) in one pair, as 1-2 UMMA
+  // N sub-tiles, so every weight byte is read once
+  const int ntm = (a.M + SK_MAX_SPAN - 1) / SK_MAX_SPAN;
   const int per = (a.M + ntm - 1) / ntm;                   // tokens per token tile
-  const int slice0 = (per + CN - 1) / CN;
-  const int mt = slice0 <= 256 ? 1 : 2;
-  P.mt = mt;
-  P.bn = (((slice0 + mt - 1) / mt) + 15) / 16 * 16;
-  if (ntm > 1 || CN > 1) P.bn = (P.bn + 31) / 32 * 32;     // 32-token epilogue blocks never cross slices
+  P.mt = per <= 256 ? 1 : 2;
+  P.bn = (((per + P.mt - 1) / P.mt) + 15) / 16 * 16;
+  if (ntm > 1) P.bn = (P.bn + 31) / 32 * 32;               // 32-token epilogue blocks never cross tiles
   P.slice = P.mt * P.bn;
-  P.span = CN * P.slice;
-  P.cn = CN;
-  static const int force_kpb = getenv("FL_SK_KPB") ? atoi(getenv("FL_SK_KPB")) : 0;
+  P.span = P.slice;
+  // two 64-wide K sub-chunks per unit (one request per operand) when the
+  // deeper stage still leaves >= 3 ring stages: a TMA request costs a roughly
+  // fixed time, so bigger boxes stream faster (tools/step_gemm_bench.py,
+  // merged out-projection at 192 / 256 rows: 1462 -> 1302 / 1548 -> 1435 us
+  // per 28 layers with 3 stages of 64 KB instead of 6 of 32 KB)
+  P.kpb = 1;
   {
     const int st2 = 2 * (SK_A_BYTES + P.mt * (P.bn / 2) * SK_BK * 2);
-    const bool ok2 = CN == 1 && a.K % (2 * SK_BK) == 0;
-    if (ok2 && SK_RING_BUDGET / st2 >= 2 && (force_kpb == 2 || (force_kpb == 0 && SK_RING_BUDGET / st2 >= 4)))
-      P.kpb = 2;
-    P.kch = a.K / (SK_BK * P.kpb);
+    if (a.K % (2 * SK_BK) == 0 && SK_RING_BUDGET / st2 >= 3) P.kpb = 2;
+    if (g_tune[3] == 1 || (g_tune[3] == 2 && a.K % (2 * SK_BK) == 0 && SK_RING_BUDGET / st2 >= 2)) P.kpb = g_tune[3];
   }
+  P.kch = a.K / (SK_BK * P.kpb);
   const int stage = P.kpb * (SK_A_BYTES + P.mt * (P.bn / 2) * SK_BK * 2);
   P.stages = SK_RING_BUDGET / stage;
   if (P.stages > SK_MAXST) P.stages = SK_MAXST;
-  static const int force_st = getenv("FL_SK_STAGES") ? atoi(getenv("FL_SK_STAGES")) : 0;
-  if (force_st > 1 && force_st < P.stages) P.stages = force_st;
+  if (g_tune[2] > 1 && g_tune[2] < P.stages) P.stages = g_tune[2];
   P.nbuf = P.slice <= 256 ? 2 : 1;
   const int cols = P.nbuf * P.slice;
   P.ncols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
   P.units = ntm * P.ntn * P.kch;
   P.ntm = ntm;
-  static const int aorder = getenv("FL_SK_AORDER") ? atoi(getenv("FL_SK_AORDER")) : 1;
-  P.aorder = aorder;
-  static const int helpers = getenv("FL_SK_HELPERS") ? atoi(getenv("FL_SK_HELPERS")) : 1;
-  // staged QKV epilogue: GPT-J (interleaved rotary) and GPT-2 (no rotary)
-  P.qkv_staged = (a.epi == EPI_QKV && a.rope.family != FL_FAMILY_NEOX && a.rope.hd % 32 == 0) ? 1 : 0;
-  P.helpers = (helpers && CN == 1 && (a.epi == EPI_STORE || a.epi == EPI_GELU || a.epi == EPI_ACC_F32 ||
-                                      a.epi == EPI_STORE_F32 || P.qkv_staged)) ? 1 : 0;
+  P.helpers = (a.epi == EPI_STORE || a.epi == EPI_GELU || a.epi == EPI_ACC_F32 || a.epi == EPI_STORE_F32) ? 1 : 0;
   void (*kern)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const SkParams) = nullptr;
   switch (a.epi) {
     case EPI_STORE: kern = k_gemm_sk<EPI_STORE>; break;
@@ -1146,27 +1035,25 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
     case EPI_ACC_F32: kern = k_gemm_sk<EPI_ACC_F32>; break;
     case EPI_STORE_F32: kern = k_gemm_sk<EPI_STORE_F32>; break;
     case EPI_ARGMAX: kern = k_gemm_sk<EPI_ARGMAX>; break;
-    case EPI_QKV: kern = k_gemm_sk<EPI_QKV>; break;
     default: g_sk_err = "unknown epilogue"; return -1;
   }
   const int smem = P.stages * stage + 1024;
-  int nclus = num_sms / (2 * CN);
-  if (nclus * CN > SK_MAX_PAIRS) nclus = SK_MAX_PAIRS / CN;
-  // a persistent grid must be co-resident: clusters of 2*CN CTAs at ~200 KB
-  // each only fit where a GPC still has 2*CN free SMs, so ask the occupancy
-  // calculator (SM count is not a multiple of the cluster size per GPC)
+  int npairs = num_sms / 2;
+  if (npairs > SK_MAX_PAIRS) npairs = SK_MAX_PAIRS;
+  // a persistent grid must be co-resident: pairs of ~200 KB CTAs only fit
+  // where a GPC still has 2 free SMs, so ask the occupancy calculator
   {
-    static std::map<std::tuple<const void*, int, int>, int> occ_cache;
-    const auto key = std::make_tuple(reinterpret_cast<const void*>(kern), 2 * CN, smem);
+    static std::map<std::tuple<const void*, int>, int> occ_cache;
+    const auto key = std::make_tuple(reinterpret_cast<const void*>(kern), smem);
     auto it = occ_cache.find(key);
     if (it == occ_cache.end()) {
       cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(2 * CN * 128);
+      cfg.gridDim = dim3(2 * 128);
       cfg.blockDim = dim3(SK_THREADS);
       cfg.dynamicSmemBytes = smem;
       cudaLaunchAttribute at;
       at.id = cudaLaunchAttributeClusterDimension;
-      at.val.clusterDim.x = 2 * CN;
+      at.val.clusterDim.x = 2;
       at.val.clusterDim.y = 1;
       at.val.clusterDim.z = 1;
       cfg.attrs = &at;
@@ -1174,56 +1061,54 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
       int nc = 0;
       if (cudaOccupancyMaxActiveClusters(&nc, kern, &cfg) != cudaSuccess || nc < 1) {
         cudaGetLastError();
-        nc = nclus;
+        nc = npairs;
       }
-      if (getenv("FL_SK_VERBOSE"))
-        fprintf(stderr, "k_gemm_sk: cluster %d x %d B smem -> %d co-resident clusters\n", 2 * CN, smem, nc);
       it = occ_cache.emplace(key, nc).first;
     }
-    if (nclus > it->second) nclus = it->second;
+    if (npairs > it->second) npairs = it->second;
   }
-  // wide windows (tensor-bound): whole or evenly split tiles, so no pair
-  // stalls its MMA on a mid-range epilogue; narrow windows (HBM-bound): every
-  // SM streams an equal share (stream-K)
+  if (g_tune[1] > 0 && g_tune[1] < npairs) npairs = g_tune[1];
+  // Work decomposition (pair_ranges):
+  // * more tiles than pairs: every pair takes the same number of whole tiles
+  //   first (no fix-up), the remaining tiles are dealt out stream-K, so all
+  //   SMs stream equal weight bytes (merged QKV + FFN-up, LM head, wide
+  //   windows);
+  // * at most half as many tiles as pairs (attn-out / FFN-down, 16 tiles):
+  //   even split-K over S <= 4 pairs per tile with a spread reduction, so the
+  //   accumulator is never held for a mid-range fix-up;
+  // * otherwise (narrow windows, HBM-bound): stream-K over all pairs.
   const int tiles = ntm * P.ntn;
-  static const int align_m = getenv("FL_SK_ALIGN_M") ? atoi(getenv("FL_SK_ALIGN_M")) : 64;
-  if (a.M >= align_m && tiles <= nclus) nclus = tiles * (nclus / tiles);
-  // short K (GPT-2 class, K <= 1024): a few whole tiles beat the fix-up of a
-  // stream-K split (fixed cost per launch dominates)
-  else if (a.K <= 1024 && tiles <= nclus) nclus = tiles;
-  static const int force_pairs = getenv("FL_SK_PAIRS") ? atoi(getenv("FL_SK_PAIRS")) : 0;
-  if (force_pairs > 0 && force_pairs / CN < nclus) nclus = force_pairs / CN;
-  // evenly split tiles of the direct epilogues: spread reduction (no owner)
   P.csplit = 1;
-  static const int no_csplit = getenv("FL_SK_NO_CSPLIT") != nullptr;
-  if (!no_csplit && a.M >= align_m && tiles <= nclus && nclus / tiles >= 2 &&
-      (a.epi == EPI_ACC_F32 || a.epi == EPI_STORE_F32 || a.epi == EPI_STORE || a.epi == EPI_GELU)) {
-    P.csplit = nclus / tiles > 4 ? 4 : nclus / tiles;
-    if (P.csplit > P.kch) P.csplit = P.kch;             // every piece holds >= 1 K unit
-    nclus = tiles * P.csplit;
+  P.dpw = 0;
+  const bool direct = a.epi == EPI_ACC_F32 || a.epi == EPI_STORE_F32 || a.epi == EPI_STORE || a.epi == EPI_GELU;
+  if (tiles >= npairs) {
+    P.dpw = tiles / npairs;
+  } else if (a.M >= 64 && direct && 2 * tiles <= npairs && P.kch >= 2) {
+    P.csplit = npairs / tiles > 4 ? 4 : npairs / tiles;
+    if (P.csplit > P.kch) P.csplit = P.kch;                // every piece holds >= 1 K unit
+    npairs = tiles * P.csplit;
+  } else if (a.M >= 64) {
+    // wide windows: even pieces with owner fix-up beat a ragged stream-K split
+    npairs = tiles * min(npairs / tiles, P.kch);
+  } else if (a.K <= 1024) {
+    // short K (GPT-2 class): a few whole tiles beat the fix-up of a split
+    // (the fixed cost per launch dominates)
+    npairs = tiles;
+  } else {
+    const int mu = g_tune[4] > 0 ? g_tune[4] : 4;
+    const int cap = (P.units + mu - 1) / mu;               // >= 4 units per range
+    if (npairs > cap) npairs = cap;
   }
-  // more tiles than pairs with a single-buffered accumulator (> 256 tokens):
-  // k whole tiles per pair instead of stream-K -- a split tile's fix-up would
-  // stall the MMA mid-range (LM head at 320 rows 140 -> 131 us)
-  P.tpr = 0;
-  static const int force_tpr = getenv("FL_SK_TPR") ? atoi(getenv("FL_SK_TPR")) : -1;
-  // ... and, from 128 tokens on, also with a double-buffered accumulator: whole
-  // tiles keep the first tile's epilogue under the second tile's MMAs and need
-  // no fix-up (merged QKV + FFN-up, GPT-J step at 128 / 192 / 256 rows -2.8 /
-  // -3.4 / -5 % against stream-K; at 64 / 96 rows, still HBM-bound, stream-K's
-  // balance wins by 8.5 / 0.6 %; tools/host_gap.py)
-  static const int tpr_wide = getenv("FL_SK_TPR_WIDE") ? atoi(getenv("FL_SK_TPR_WIDE")) : 128;
-  if ((P.nbuf == 1 || (tpr_wide > 0 && a.M >= tpr_wide)) && tiles > nclus && P.csplit == 1 && CN == 1 &&
-      force_tpr != 0) {
-    const int k = (tiles + nclus - 1) / nclus;
-    P.tpr = k;
-    nclus = (tiles + k - 1) / k;
+  if (npairs < 1) npairs = 1;
+  P.npairs = npairs;
+  {
+    // stream-K share of the units after the whole-tile prefix: every range
+    // non-empty, and >= 2 units per range behind a prefix
+    const int ur = P.units - P.dpw * P.kch * npairs;
+    int nsk = P.dpw ? ur / (g_tune[4] > 0 ? g_tune[4] : 2) : ur;
+    if (nsk > npairs) nsk = npairs;
+    P.nsk = nsk < 1 ? 1 : nsk;
   }
-  const int cap = (P.units + 3) / 4;                       // >= 4 chunks per range
-  if (nclus > cap && P.csplit == 1 && !P.tpr) nclus = cap;
-  if (nclus < 1) nclus = 1;
-  P.nclus = nclus;
-  P.npairs = nclus * CN;
   P.bias = static_cast<const bf16*>(a.bias);
   P.out = a.out;
   P.keys = a.keys;
@@ -1231,12 +1116,9 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   P.part = static_cast<float*>(ws);
   P.slot_elems = SK_MAX_SPAN * SK_BM;
   P.flags = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + (size_t)SK_MAX_PAIRS * 2 * SK_MAX_SPAN * SK_BM * 4);
-  P.rope = a.rope;
   P.dbg = g_sk_dbg;
   P.nsplit = a.nsplit;
   P.ogap = a.ogap;
-  static const int use_red = getenv("FL_SK_RED") ? atoi(getenv("FL_SK_RED")) : 0;
-  P.red = use_red;
   P.vec = (a.ldo % 4 == 0 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0) ? 1 : 0;
   CUtensorMap *mw, *mx;
   P.w_tiled = a.w_tiled;
@@ -1244,10 +1126,10 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   if (a.w_tiled) {
     // [rows = ceil(N/128) * 128 * K/64][64]: 128-byte rows, contiguous chunks
     const uint64_t trows = (uint64_t)((a.N + SK_BM - 1) / SK_BM) * SK_BM * (a.K / SK_BK);
-    const uint32_t box = P.kpb > 1 ? 2 * SK_BM : (uint32_t)(SK_BM / CN);
+    const uint32_t box = P.kpb > 1 ? 2 * SK_BM : (uint32_t)SK_BM;
     if (!sk_map({a.w, 0, trows, (uint64_t)SK_BK, (uint64_t)SK_BK * 2, SK_BK, box, 1, 1}, &mw)) return -1;
-  } else if (!sk_map({a.w, 0, (uint64_t)a.N, (uint64_t)a.K, (uint64_t)a.K * 2, SK_BK,
-                      (uint32_t)(SK_BM / CN), 1, P.kpb}, &mw)) {
+  } else if (!sk_map({a.w, 0, (uint64_t)a.N, (uint64_t)a.K, (uint64_t)a.K * 2, SK_BK, (uint32_t)SK_BM, 1, P.kpb},
+                     &mw)) {
     return -1;
   }
   if (!sk_map({a.x, 0, (uint64_t)(a.mcap > a.M ? a.mcap : a.M), (uint64_t)a.K, (uint64_t)a.ldx * 2, SK_BK,
@@ -1258,8 +1140,7 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
       !sk_map({a.x2, 0, (uint64_t)(a.mcap > a.M ? a.mcap : a.M), (uint64_t)a.K, (uint64_t)a.ldx * 2, SK_BK,
                (uint32_t)(P.bn / 2), 1, P.kpb}, &mx2))
     return -1;
-  cudaError_t e = launch_k(kern, dim3(2 * P.npairs), dim3(SK_THREADS), smem, s, dim3(2 * CN, 1, 1), *mw, *mx,
-                           *mx2, P);
+  cudaError_t e = launch_k(kern, dim3(2 * P.npairs), dim3(SK_THREADS), smem, s, dim3(2, 1, 1), *mw, *mx, *mx2, P);
   if (e != cudaSuccess) {
     char buf[256];
     snprintf(buf, sizeof buf, "k_gemm_sk launch (pairs %d smem %d stages %d bn %d mt %d): %s", P.npairs, smem,
@@ -1269,5 +1150,24 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   }
   return 0;
 }
+
+// ---- the TcWorkspace interface (gemm_tc.cuh) over the stream-K kernel
+size_t tc_workspace_bytes(int, int) { return sk_workspace_bytes(); }
+const char* tc_last_error() { return sk_last_error(); }
+void tc_set_debug(unsigned long long* p) { sk_set_debug(p); }
+
+int tc_init(TcWorkspace* ws, void* base, size_t bytes) {
+  ws->base = base;
+  ws->bytes = bytes;
+  if (sk_init(base, bytes)) return -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&ws->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  return 0;
+}
+
+void tc_destroy(TcWorkspace*) {}
+
+int gemm_tc(TcWorkspace* ws, const GemmArgs& a, cudaStream_t s) { return gemm_sk(ws->base, ws->num_sms, a, s); }
 
 }  // namespace fl

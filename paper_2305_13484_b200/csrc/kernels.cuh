@@ -13,17 +13,7 @@ enum Epilogue {
   EPI_GELU = 1,       // out(T)   = gelu(acc + bias)
   EPI_ACC_F32 = 2,    // out(f32) += acc + bias      (residual update)
   EPI_STORE_F32 = 3,  // out(f32) = acc + bias       (partial sums, logits)
-  EPI_ARGMAX = 4,     // keys[m] = max(keys[m], key(acc + bias, n))  (fused greedy argmax)
-  EPI_QKV = 5         // rotary on q/k + q -> q_out, k/v -> KV pool at each row's (slot, pos)
-};
-
-// EPI_QKV: the QKV projection's epilogue does what k_rope_append does
-struct RopeArgs {
-  const fl_row* rows = nullptr;
-  const int32_t* row_pos = nullptr;
-  void* kv_layer = nullptr;     // [C][2][Hl][S][hd] of this layer
-  void* q_out = nullptr;        // [M, Hl*hd]
-  int Hl = 0, hd = 0, rot = 0, family = 0, S = 0;
+  EPI_ARGMAX = 4      // keys[m] = max(keys[m], key(acc + bias, n))  (fused greedy argmax)
 };
 
 struct GemmArgs {
@@ -37,7 +27,6 @@ struct GemmArgs {
   int mcap;           // rows allocated behind x (>= M); fixes the TMA map per buffer
   unsigned long long* keys = nullptr;   // EPI_ARGMAX: per-row packed (logit, index) keys
   int index_base = 0;                   // EPI_ARGMAX: global index of weight row 0
-  RopeArgs rope;                        // EPI_QKV
   int w_tiled = 0;                      // w in the fl_tile_weight layout
   // two GEMMs over one weight stream [W1; W2] (EPI_GELU only, tcgen05 path):
   // weight rows n < nsplit read x and store plainly to out column n; rows

@@ -47,6 +47,20 @@ def preprocess(request: Request, params: CostParams, now: float) -> Context:
     return Context(request.request_id, now + params.preprocess_ms, info)
 
 
+def check_tp(tp, executor, clock: str) -> None:
+    """The modelled TP degree (TPConfig, reference cost.py:26-33) and the
+    executor's real one must agree whenever the device sets the clock.
+    Under the cost clock the TPConfig is only a cost-model parameter, so a
+    1-GPU executor may replay a modelled TP schedule (parity mode)."""
+    if executor is None or tp is None:
+        return
+    real = getattr(executor, "tp_size", None)
+    if real is None or real == tp.tp_size:
+        return
+    if clock == "device" or real > 1:
+        raise InvalidParam(f"TPConfig.tp_size {tp.tp_size} != executor tp_size {real}")
+
+
 class _ActiveTable(MutableMapping):
     """``rid -> RuntimeInfo`` in fusion order, materialised on access.
 
@@ -97,6 +111,7 @@ class FusionStream:
             raise InvalidParam(f"clock must be 'cost' or 'device', got {clock!r}")
         if clock == "device" and executor is None:
             raise InvalidParam("clock='device' needs an executor")
+        check_tp(tp, executor, clock)
         self.params = params
         self.tp = tp
         self.shuffle_enabled = shuffle_enabled

@@ -27,7 +27,6 @@ to schedule: steady-state iterations upload nothing and read nothing back.
 from __future__ import annotations
 
 import ctypes as C
-import os
 
 import torch
 
@@ -59,7 +58,9 @@ class CudaExecutor:
                  state_slots: int = 4096, tp_rank: int = 0, tp_size: int = 1, seed: int = 0,
                  weights: dict | None = None, use_tensor_cores: bool | None = None,
                  capture_logits: bool = False, device: str = "cuda", comm_id: bytes | None = None,
-                 time_steps: bool = False, use_graphs: bool = True, device_plan: bool = False):
+                 time_steps: bool = False, use_graphs: bool = True, device_plan: bool = False,
+                 tiled: bool | None = None, merged_in: bool | None = None,
+                 merged_out: bool | None = None, merged_in_max_rows: int = -1):
         if dtype not in _TORCH_DTYPE:
             raise InvalidParam(f"dtype must be f32 or bf16, got {dtype}")
         self.lib = _lib.load()
@@ -79,6 +80,9 @@ class CudaExecutor:
                 raise InvalidParam("need max_seq or input_len")
             max_seq = input_len + max_new_tokens - 1
         self.S = max_seq
+        if spec.family == "gpt2" and max_seq > spec.max_pos:
+            # learned positions: a row at pos >= max_pos would read past wpe
+            raise InvalidParam(f"max_seq {max_seq} > {spec.name} max_pos {spec.max_pos}")
         self.max_rows = bucket(max_rows or (pool_slots + 16 * (input_len or 32)))
         if self.max_rows < bucket(pool_slots) + 64:
             self.max_rows = bucket(bucket(pool_slots) + 64)
@@ -96,16 +100,25 @@ class CudaExecutor:
         # tensor-core path: projection weights in the GEMM's tiled layout
         # (fl_tile_weight: every 128 x 64 tile the GEMM streams is contiguous);
         # the caller's tensors are left untouched, our own copies are replaced
-        self.tiled = self.use_tc and dtype == "bf16" and not os.environ.get("FL_NO_TILED_WEIGHTS")
+        self.tiled = self.use_tc if tiled is None else bool(tiled) and self.use_tc
+        parallel = spec.family in ("gptj", "neox")
         # parallel residual (gptj, neox): attn-out and FFN-down as one GEMM over
-        # K = Dl + Fl with W_cat = [W_o | W_proj] and b_o + b_proj (tensor-core path)
-        self.merged = (self.use_tc and spec.family in ("gptj", "neox")
-                       and not os.environ.get("FL_NO_MERGED_OUT"))
+        # K = Dl + Fl with W_cat = [W_o | W_proj] and b_o + b_proj, i.e. ONE
+        # all-reduce per layer under TP.  Default: on at tp 1; under TP the
+        # north star's layout (an all-reduce after attn-out AND after FFN-down)
+        if merged_out is None:
+            merged_out = tp_size == 1
+        self.merged = bool(merged_out) and self.use_tc and parallel
+        self.tp_layout = ("one all-reduce per layer (merged attn-out + FFN-down)" if self.merged
+                          else "two all-reduces per layer (after attn-out and after FFN-down)")
         self._wcat, self._bcat = [], []
         # ... and QKV and FFN-up as one GEMM over [W_qkv; W_fc] (rows 3*Dl..
         # read the MLP input, get GELU, land after the attention output)
-        self.merged_in = (self.use_tc and spec.family in ("gptj", "neox") and (3 * hl * spec.head_dim) % 256 == 0
-                          and not os.environ.get("FL_NO_MERGED_IN"))
+        if merged_in is None:
+            merged_in = True
+        self.merged_in = (bool(merged_in) and self.use_tc and parallel
+                          and (3 * hl * spec.head_dim) % 256 == 0)
+        self.merged_in_max_rows = merged_in_max_rows
         self._win, self._bin = [], []
         if self.merged_in:
             for l in range(spec.n_layer):
@@ -213,7 +226,8 @@ class CudaExecutor:
                   for l in range(spec.n_layer)]
             self._win = (C.c_void_p * len(wi))(*wi)
             self._bin = (C.c_void_p * len(bi))(*bi)
-            _lib.check(self.lib.fl_set_merged_in(self.handle, self._win, self._bin))
+            _lib.check(self.lib.fl_set_merged_in(self.handle, self._win, self._bin,
+                                                 int(self.merged_in_max_rows)))
         self.use_graphs = use_graphs
         self._lib_timing = False
         _lib.check(self.lib.fl_configure(self.handle, int(use_graphs), 8, 0))
@@ -253,6 +267,7 @@ class CudaExecutor:
         self.moved_kv_bytes = 0
         self.shuffle_log = []             # (moves, algorithmic bytes, device ms) per shuffle
         self.seen = []
+        self._ring_owner = {}             # state-ring index -> rid whose history it holds
         self.h2d_bytes = 0
         self.d2h_bytes = 0
         self.attn_ctx_rows = 0            # sum over iterations of sum_rows ctx_r
@@ -280,6 +295,7 @@ class CudaExecutor:
         self._pre_passes = []
         self._live_ctx = self._orphan_ctx = self._prefill_ctx = 0
         self.seen = []
+        self._ring_owner = {}
         self.logits_log = []
         self._events = []
 
@@ -318,6 +334,7 @@ class CudaExecutor:
         for other in self._live:
             if other % self.R == rid % self.R:
                 raise CapacityExceeded(f"state ring collision between requests {rid} and {other}")
+        self._ring_owner[rid % self.R] = rid
         self._live[rid] = {"P": P, "stop": stop, "gen": 0}
         self._live_ctx += P
         self._prefill_ctx += (P - 1) * P // 2
@@ -511,6 +528,11 @@ class CudaExecutor:
         rids = list(self.seen if rids is None else rids)
         if not rids:
             return {}
+        for rid in rids:
+            owner = self._ring_owner.get(rid % self.R)
+            if owner != rid:
+                raise CapacityExceeded(f"history of request {rid} was overwritten by request {owner} "
+                                       f"(state_slots {self.R}); read tokens() before the ring wraps")
         with torch.cuda.stream(self.cs):
             idx = torch.tensor([r % self.R for r in rids], device=self.device, dtype=torch.long)
             packed = torch.cat([self.req_ngen[idx].unsqueeze(1), self.tok_hist[idx]], dim=1).cpu()

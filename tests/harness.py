@@ -17,7 +17,8 @@ def scenario_requests(n, mean_ms, lo, hi, max_out, input_len, seed=1):
 
 def run_device(spec_name, requests, *, dtype="f32", shuffle=True, clock="cost", seed=1,
                params=None, tp=None, capture_logits=True, pool_slots=None, use_tc=None,
-               weights=None, record_tokens=True, time_steps=False, comm_id=None, device_plan=False):
+               weights=None, record_tokens=True, time_steps=False, comm_id=None, device_plan=False,
+               executor_opts=None):
     """Serve ``requests`` through the drop-in engine on the device.
     Returns (trace, stream, executor, prompts, weights_cpu_fp32)."""
     import torch
@@ -32,7 +33,8 @@ def run_device(spec_name, requests, *, dtype="f32", shuffle=True, clock="cost", 
                       max_new_tokens=max_out, input_len=input_len,
                       state_slots=max(64, len(requests)), weights=weights,
                       use_tensor_cores=use_tc, capture_logits=capture_logits,
-                      time_steps=time_steps, comm_id=comm_id, device_plan=device_plan)
+                      time_steps=time_steps, comm_id=comm_id, device_plan=device_plan,
+                      **(executor_opts or {}))
     st = fl.FusionStream(requests, params or fl.CostParams(), tp or fl.TPConfig(),
                          shuffle_enabled=shuffle, record_tokens=record_tokens, executor=ex,
                          clock=clock)

@@ -185,3 +185,77 @@ def test_attention_kernel_matches_fp32_reference(hd, M, Hl):
         p = torch.softmax(torch.einsum("hd,hnd->hn", qf[r], k) / hd ** 0.5, dim=-1)
         ref[r] = torch.einsum("hn,hnd->hd", p, v)
     torch.testing.assert_close(out.float().view(M, Hl, hd), ref, atol=2e-2, rtol=2e-2)
+
+
+def _gemm2(x, x2, w, bias, out, epi, use_tc, nsplit=0, ogap=0, keys=None, index_base=0, N=None, K=None):
+    lib = _lib.load()
+    ws = torch.empty(lib.fl_gemm_workspace_bytes(), dtype=torch.uint8, device="cuda")
+    M = x.shape[0]
+    N = N or w.shape[0]
+    K = K or x.shape[1]
+    s = torch.cuda.current_stream()
+    _lib.check(lib.fl_gemm2(x.data_ptr(), x2.data_ptr() if x2 is not None else None, x.stride(0),
+                            w.data_ptr(), bias.data_ptr() if bias is not None else None,
+                            out.data_ptr() if out is not None else None, out.stride(0) if out is not None else 0,
+                            M, N, K, epi, 1, use_tc, nsplit, ogap,
+                            keys.data_ptr() if keys is not None else None, index_base, ws.data_ptr(),
+                            C.c_void_p(s.cuda_stream)))
+    torch.cuda.synchronize()
+
+
+def _tile(w):
+    lib = _lib.load()
+    n, k = w.shape
+    wt = torch.empty(lib.fl_tiled_weight_bytes(n, k) // 2, dtype=torch.bfloat16, device="cuda")
+    _lib.check(lib.fl_tile_weight(w.data_ptr(), n, k, wt.data_ptr(), C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    return wt
+
+
+@pytest.mark.parametrize("M", [8, 40, 96, 136, 192, 256, 320])
+@pytest.mark.parametrize("tiled", [False, True])
+def test_dual_gemm_merged_in_projection(M, tiled):
+    """fl_set_merged_in's GEMM at the GPT-J shape: [W_qkv; W_fc] (12288 +
+    16384 rows, K 4096) in one launch; rows < 12288 read x and store into
+    columns [0, 12288), rows >= 12288 read x2, get GELU and land at column
+    n + 4096 of the shared [M][4Dl + Fl] activation row."""
+    d, q3, F = 4096, 12288, 16384
+    g = torch.Generator(device="cuda").manual_seed(M)
+    x = (torch.randn(M, d, device="cuda", generator=g) * 0.5).bfloat16()
+    x2 = (torch.randn(M, d, device="cuda", generator=g) * 0.5).bfloat16()
+    w = (torch.randn(q3 + F, d, device="cuda", generator=g) * 0.02).bfloat16()
+    b = (torch.randn(q3 + F, device="cuda", generator=g) * 0.1).bfloat16()
+    ld = 4 * d + F
+    out = torch.zeros(M, ld, device="cuda", dtype=torch.bfloat16)
+    _gemm2(x, x2, _tile(w) if tiled else w, b, out, EPI_GELU, 2 if tiled else 1, nsplit=q3, ogap=d,
+           N=q3 + F, K=d)
+    ref_q = x.float() @ w[:q3].float().T + b[:q3].float()
+    ref_f = _gelu(x2.float() @ w[q3:].float().T + b[q3:].float())
+    tol = 2e-3 * (d / 256) ** 0.5
+    assert (out[:, :q3].float() - ref_q).abs().max().item() <= tol + 2 ** -8 * ref_q.abs().max().item()
+    assert (out[:, q3 + d:].float() - ref_f).abs().max().item() <= tol + 2 ** -8 * ref_f.abs().max().item()
+    assert out[:, q3:q3 + d].abs().max().item() == 0      # the attention output's columns are untouched
+
+
+@pytest.mark.parametrize("M", [1, 24, 64, 160, 256, 320, 448])
+@pytest.mark.parametrize("V,d", [(50400, 4096), (50432, 6144), (50257, 768)])
+def test_lm_head_fused_argmax(M, V, d):
+    """K8 with the greedy argmax in the epilogue at the C2/C3/C4 LM heads:
+    the packed (logit, lowest index) key equals torch's argmax of the fp32
+    reference wherever its top-2 gap exceeds the accumulation error."""
+    g = torch.Generator(device="cuda").manual_seed(M + V + d)
+    x = (torch.randn(M, d, device="cuda", generator=g)).bfloat16()
+    w = (torch.randn(V, d, device="cuda", generator=g) * 0.05).bfloat16()
+    b = (torch.randn(V, device="cuda", generator=g) * 0.1).bfloat16()
+    keys = torch.zeros(M, dtype=torch.int64, device="cuda")
+    tiled = d % 64 == 0
+    _gemm2(x, None, _tile(w) if tiled else w, b, None, 4, 2 if tiled else 1, keys=keys, N=V, K=d)
+    ref = x.float() @ w.float().T + b.float()
+    idx = 0xFFFFFFFF - (keys.cpu() & 0xFFFFFFFF)
+    top2 = ref.topk(2, dim=1)
+    gap = (top2.values[:, 0] - top2.values[:, 1]).cpu()
+    sure = gap > 2e-2
+    assert sure.sum() >= 0.8 * M
+    assert torch.equal(idx[sure], top2.indices[:, 0].cpu()[sure])
+    # near-ties: the chosen logit is within the error of the max
+    picked = ref.gather(1, idx.cuda().long()[:, None])[:, 0]
+    assert (top2.values[:, 0] - picked).abs().max().item() <= 2e-2

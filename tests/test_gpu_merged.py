@@ -3,7 +3,7 @@
 fl_set_merged_in runs QKV and FFN-up as one GEMM over [W_qkv; W_fc] (the FFN
 rows read the MLP input -- GPT-J: LN1(x), NeoX: LN2(x) -- get GELU and land
 after the attention output); fl_set_merged_out runs attn-out and FFN-down as
-one GEMM over K = Dl + Fl.  Windows wider than FL_MERGED_IN_MAX_ROWS run QKV
+one GEMM over K = Dl + Fl.  Windows wider than merged_in_max_rows run QKV
 and FFN-up apart over views of the stacked weight.  Every combination must match the oracle within
 the bf16 bar of test_gpu_parity and give the same greedy tokens.
 """
@@ -20,20 +20,17 @@ BF16 = dict(logit_atol=0.15, logit_rtol=0.02, margin=0.15)
 
 
 @pytest.mark.parametrize("spec_name", ["gptj-mini", "neox-mini-w"])
-def test_merged_projections_match_oracle(spec_name, monkeypatch):
+def test_merged_projections_match_oracle(spec_name):
     reqs = scenario_requests(12, 10.0, 3, 40, 40, 16, seed=5)
     runs = {}
     for no_in, no_out, views in ((False, False, False), (True, False, False), (False, True, False),
                                  (True, True, False), (False, False, True)):
-        for var, off in (("FL_NO_MERGED_IN", no_in), ("FL_NO_MERGED_OUT", no_out)):
-            if off:
-                monkeypatch.setenv(var, "1")
-            else:
-                monkeypatch.delenv(var, raising=False)
         # views: stacked weights, but every window runs QKV and FFN-up apart
         # over views of them (the library's wide-window choice)
-        monkeypatch.setenv("FL_MERGED_IN_MAX_ROWS", "0" if views else "100000")
-        trace, st, ex, prompts, w32 = run_device(spec_name, reqs, dtype="bf16", shuffle=True)
+        opts = dict(merged_in=not no_in, merged_out=not no_out,
+                    merged_in_max_rows=0 if views else 100000)
+        trace, st, ex, prompts, w32 = run_device(spec_name, reqs, dtype="bf16", shuffle=True,
+                                                 executor_opts=opts)
         assert ex.use_tc
         assert ex.merged_in == (not no_in) and ex.merged == (not no_out)
         stats = oracle_check(spec_name, ex, prompts, w32, **BF16)

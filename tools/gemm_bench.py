@@ -5,11 +5,11 @@
 import ctypes as C
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-os.environ.setdefault("FL_GEMM_NO_REARM", "1")   # same workspace every call: flags self-reset
 import torch
 from paper_2305_13484_b200 import _lib
 
 lib = _lib.load()
+lib.fl_gemm_set_rearm(0)   # one workspace for every call: the flags self-reset
 ws = torch.empty(lib.fl_gemm_workspace_bytes(), dtype=torch.uint8, device="cuda")
 REPS = 50
 shapes = [(48, 2304, 768), (48, 768, 768), (48, 3072, 768), (48, 768, 3072), (48, 50257, 768),

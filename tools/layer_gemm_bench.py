@@ -11,11 +11,11 @@ plain GEMMs without the epilogues).
 import ctypes as C
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-os.environ.setdefault("FL_GEMM_NO_REARM", "1")
 import torch
 from paper_2305_13484_b200 import _lib
 
 lib = _lib.load()
+lib.fl_gemm_set_rearm(0)   # one workspace for every call: the flags self-reset
 ws = torch.empty(lib.fl_gemm_workspace_bytes(), dtype=torch.uint8, device="cuda")
 L, d, F, V = 28, 4096, 16384, 50400
 g = torch.Generator(device="cuda").manual_seed(0)
