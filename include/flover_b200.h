@@ -151,6 +151,26 @@ int fl_step(fl_handle* h, const fl_row* rows, int n_rows, int n_dec, int rows_ch
  * (layer, K/V, head) from src to dst in one launch.  Slots are disjoint. */
 int fl_shuffle(fl_handle* h, const int32_t* moves, int n, void* cuda_stream);
 
+/* Overlapped preprocessing (the paper's T_pp threads,
+ * PAPER.md:231, which the reference models as an independent delay,
+ * reference engine.py:6-8,24-42,69-83).  A second handle over the same
+ * weights, created with a small STAGING pool (S = prompt length), runs the
+ * prompts' PREFILL rows (n_dec = 0 fl_steps) on a side stream while the
+ * serving handle's fused steps run on the main stream.
+ *
+ * fl_set_side_stream(h, 1): h's launches may share the GPU with another
+ * handle's; its GEMMs then use decompositions without cross-CTA waits (one
+ * whole tile per CTA pair), so neither stream's persistent grid can wait on
+ * CTAs the other stream keeps from being resident.  Call before the first step.
+ *
+ * fl_step_import(h, staging kv, staging slots, staging S, moves, n): queue the
+ * copy of prompt KV from staging slots into h's pool -- moves is a HOST array
+ * of n triples (staging_slot, pool_slot, n_positions) -- to run at the start
+ * of h's next fl_step, inside that step's timing bracket.  The caller orders
+ * the staging writes before that step (an event from the side stream). */
+int fl_set_side_stream(fl_handle* h, int on);
+int fl_step_import(fl_handle* h, const void* src_kv, int src_slots, int src_seq, const int32_t* moves, int n);
+
 /* Number of kernels fl_step / fl_shuffle launched since fl_create. */
 int64_t fl_kernel_launches(const fl_handle* h);
 
@@ -256,6 +276,21 @@ int fl_tile_weight(const void* w, int N, int K, void* out, void* cuda_stream);
  * out must hold 3 + 2n ints.  Returns FL_EINVAL for n outside [0, 8192]. */
 int fl_plan_shuffle(const int32_t* occ, const int64_t* size, int n, int lo, int32_t* out,
                     long long* bytes, void* cuda_stream);
+
+/* A shuffle boundary planned and executed on the device: the
+ * window's occupancy -- occ[n] (nonzero = occupied), size[n] (bytes, the
+ * reference's tensor_size), ctx[n] (live KV positions of each occupant), HOST
+ * arrays of window slots lo .. lo+n-1 -- is uploaded once; Algorithm 1 +
+ * plan_shuffle run on the device (as fl_plan_shuffle) and K10 consumes the
+ * device move list directly (physical slot = logical slot % pool_slots), so
+ * the moves never pass through the host before the copy.  The plan (the
+ * fl_plan_shuffle layout, 3 + 2n int32) and total_bytes_moved are copied,
+ * stream-ordered, to plan_out / bytes_out (host, pinned; either may be NULL)
+ * for the host's mirror of the layout.  With time_steps on, the device clock
+ * covers planner + K10.  Replaces the host plan_shuffle / apply_shuffle pair
+ * (reference buffer.py:226-278) on the device side. */
+int fl_shuffle_planned(fl_handle* h, const int32_t* occ, const int64_t* size, const int32_t* ctx, int n, int lo,
+                       int32_t* plan_out, long long* bytes_out, void* cuda_stream);
 
 #ifdef __cplusplus
 }

@@ -23,7 +23,8 @@ EXPORTS = ("fl_abi_version", "fl_last_error", "fl_workspace_bytes", "fl_create",
            "fl_gemm_workspace_bytes", "fl_gemm", "fl_profile", "fl_profile_read", "fl_configure",
            "fl_last_duration_ms", "fl_attention_workspace_bytes", "fl_attention",
            "fl_gemm_debug", "fl_plan_shuffle", "fl_tiled_weight_bytes", "fl_tile_weight",
-           "fl_set_merged_out", "fl_set_merged_in", "fl_gemm2", "fl_gemm_set_rearm", "fl_gemm_tune")
+           "fl_set_merged_out", "fl_set_merged_in", "fl_gemm2", "fl_gemm_set_rearm", "fl_gemm_tune",
+           "fl_set_side_stream", "fl_step_import", "fl_shuffle_planned")
 PROF_ATTENTION, PROF_GEMM, PROF_SHUFFLE, PROF_STEP = 0, 1, 2, 3
 
 
@@ -109,6 +110,10 @@ def load() -> C.CDLL:
     lib.fl_tile_weight.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
     lib.fl_plan_shuffle.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
                                     C.c_void_p]
+    lib.fl_set_side_stream.argtypes = [C.c_void_p, C.c_int]
+    lib.fl_step_import.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_int32), C.c_int]
+    lib.fl_shuffle_planned.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int,
+                                       C.c_void_p, C.c_void_p, C.c_void_p]
     if lib.fl_abi_version() != 1:
         raise DeviceError("ABI version mismatch")
     _lib = lib

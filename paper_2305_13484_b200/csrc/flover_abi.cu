@@ -91,6 +91,8 @@ struct fl_handle {
   // workspace carve
   fl_row* rows;
   int32_t *row_tok, *row_pos, *row_ctx, *row_order, *moves;
+  char* plan_ws;
+  std::vector<char> plan_stage;           // host staging of the window arrays
   float *x, *y, *logits, *att_o, *att_ml;
   void *h, *h2, *qkv, *q, *a, *f;
   unsigned long long* keys;
@@ -105,6 +107,11 @@ struct fl_handle {
   std::vector<const void*> win, bin;
   bool merged_in = false;
   int merged_in_max_rows = 0;             // windows wider than this run QKV and FFN-up apart
+  bool side = false;                      // runs beside another handle's steps (fl_set_side_stream)
+  // prefill import queued by fl_step_import for the next fl_step
+  struct Import { const void* src_kv; int src_slots, src_seq, n; };
+  Import imp{nullptr, 0, 0, 0};
+  std::vector<int32_t> imp_moves;
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;
   // live profiling
@@ -187,8 +194,8 @@ struct Carve {
 };
 
 struct Layout {
-  size_t rows, row_tok, row_pos, row_ctx, row_order, moves, x, y, logits, att_o, att_ml, h, h2, qkv, q, a, f, keys,
-      tc, total;
+  size_t rows, row_tok, row_pos, row_ctx, row_order, moves, plan, x, y, logits, att_o, att_ml, h, h2, qkv, q, a, f,
+      keys, tc, total;
 };
 
 int check_desc(const fl_model_desc* m, const fl_pool_desc* p) {
@@ -226,6 +233,8 @@ Layout plan(const fl_model_desc* m, const fl_pool_desc* p) {
   L.row_ctx = c.take(Mr * 4);
   L.row_order = c.take(Mr * 4);
   L.moves = c.take(size_t(p->pool_slots) * 3 * 4 + 16);
+  // device-planned shuffle: window occ/ctx (int32) + sizes (int64) in, plan out
+  L.plan = c.take(size_t(p->pool_slots) * 16 + (3 + 2 * size_t(p->pool_slots)) * 4 + 64);
   L.x = c.take(Mr * d * 4);
   L.y = c.take(Mr * d * 4);
   L.logits = c.take(Md * Vl * 4);
@@ -292,6 +301,7 @@ int fl_create(const fl_model_desc* m, const fl_pool_desc* p, fl_handle** out) {
   h->row_ctx = (int32_t*)(w + L.row_ctx);
   h->row_order = (int32_t*)(w + L.row_order);
   h->moves = (int32_t*)(w + L.moves);
+  h->plan_ws = w + L.plan;
   h->x = (float*)(w + L.x);
   h->y = (float*)(w + L.y);
   h->logits = (float*)(w + L.logits);
@@ -440,6 +450,7 @@ int gemm(fl_handle* h, const void* x, int ldx, const void* w, const void* bias, 
   a.x2 = x2;
   a.nsplit = nsplit;
   a.ogap = ogap;
+  a.indep = h->side ? 1 : 0;
   if (nsplit && !h->p.use_tensor_cores) return FL_EINVAL;
   if (epi == fl::EPI_ARGMAX) {
     a.keys = h->keys;
@@ -625,8 +636,20 @@ extern "C" int fl_step(fl_handle* h, const fl_row* rows, int n_rows, int n_dec, 
   }
   const bool want_logits = logits_out != nullptr;
   const bool profiled = h->prof && (h->step_counter++ % h->prof_every == 0);
+  if (h->imp.n > 0) FL_CUDA(cudaMemcpyAsync(h->moves, h->imp_moves.data(), sizeof(int32_t) * 3 * h->imp.n,
+                                           cudaMemcpyHostToDevice, s));
+  // the queued prefill import (fl_step_import) runs first, inside the step's
+  // timing bracket, so the device clock charges it to the admitting iteration
+  auto run_import = [&]() {
+    if (h->imp.n <= 0) return;
+    fl::launch_kv_copy(h->moves, h->imp.n, h->imp.src_kv, h->imp.src_slots, h->imp.src_seq, p.kv, p.pool_slots,
+                       p.max_seq, h->m.n_layer, h->Hl, h->m.head_dim, h->m.dtype, s);
+    fl::g_launches += 1;
+    h->imp.n = 0;
+  };
   if (!h->use_graphs) {
     if (h->time_steps) FL_CUDA(cudaEventRecord(h->t0, s));
+    run_import();
     if (h->prof && !profiled) {
       const bool save = h->prof;
       h->prof = false;
@@ -668,6 +691,7 @@ extern "C" int fl_step(fl_handle* h, const fl_row* rows, int n_rows, int n_dec, 
       ge.pending = false;
     }
     if (h->time_steps) FL_CUDA(cudaEventRecord(h->t0, s));   // after any capture work
+    run_import();
     FL_CUDA(cudaGraphLaunch(ge.exec, s));
     ge.pending = profiled;
   }
@@ -849,5 +873,72 @@ extern "C" int fl_set_merged_out(fl_handle* h, const void* const* w_cat, const v
   for (auto p : h->wcat)
     if (!p) return fail(FL_EINVAL, "null merged weight");
   h->merged = true;
+  return FL_OK;
+}
+
+extern "C" int fl_set_side_stream(fl_handle* h, int on) {
+  if (!h) return fail(FL_EINVAL, "null handle");
+  if (!h->graphs.empty()) return fail(FL_EINVAL, "fl_set_side_stream after the first step");
+  h->side = on != 0;
+  return FL_OK;
+}
+
+extern "C" int fl_step_import(fl_handle* h, const void* src_kv, int src_slots, int src_seq, const int32_t* moves,
+                              int n) {
+  if (!h) return fail(FL_EINVAL, "null handle");
+  if (n < 0 || n > h->p.pool_slots) return fail(FL_EINVAL, "%d imports > pool %d", n, h->p.pool_slots);
+  if (n > 0 && (!src_kv || !moves || src_slots < 1 || src_seq < 1))
+    return fail(FL_EINVAL, "bad import source");
+  for (int i = 0; i < n; ++i) {
+    const int s0 = moves[3 * i], d0 = moves[3 * i + 1], c = moves[3 * i + 2];
+    if (s0 < 0 || s0 >= src_slots || d0 < 0 || d0 >= h->p.pool_slots || c < 0 || c > src_seq ||
+        c > h->p.max_seq)
+      return fail(FL_EINVAL, "bad import %d: staging %d -> slot %d (%d positions)", i, s0, d0, c);
+  }
+  h->imp = {src_kv, src_slots, src_seq, n};
+  h->imp_moves.assign(moves, moves + 3 * n);
+  return FL_OK;
+}
+
+namespace fl {
+int launch_plan_shuffle(const int32_t* occ, const int64_t* size, int n, int lo, int32_t* out, long long* bytes,
+                        cudaStream_t s);
+}
+
+extern "C" int fl_shuffle_planned(fl_handle* h, const int32_t* occ, const int64_t* size, const int32_t* ctx, int n,
+                                  int lo, int32_t* plan_out, long long* bytes_out, void* stream) {
+  if (!h) return fail(FL_EINVAL, "null handle");
+  if (n < 0 || n > h->p.pool_slots) return fail(FL_EINVAL, "window of %d slots > pool %d", n, h->p.pool_slots);
+  if (n > 0 && (!occ || !size || !ctx)) return fail(FL_EINVAL, "null window array");
+  for (int i = 0; i < n; ++i)
+    if (ctx[i] < 0 || ctx[i] > h->p.max_seq) return fail(FL_EINVAL, "slot %d: %d live positions", i, ctx[i]);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t nn = n > 0 ? n : 1;
+  // one staging copy: sizes (int64) | occ (int32) | ctx (int32)
+  h->plan_stage.resize(nn * 16);
+  if (n > 0) {
+    std::memcpy(h->plan_stage.data(), size, (size_t)n * 8);
+    std::memcpy(h->plan_stage.data() + nn * 8, occ, (size_t)n * 4);
+    std::memcpy(h->plan_stage.data() + nn * 12, ctx, (size_t)n * 4);
+  }
+  int64_t* d_size = reinterpret_cast<int64_t*>(h->plan_ws);
+  int32_t* d_occ = reinterpret_cast<int32_t*>(h->plan_ws + nn * 8);
+  int32_t* d_ctx = reinterpret_cast<int32_t*>(h->plan_ws + nn * 12);
+  int32_t* d_plan = reinterpret_cast<int32_t*>(h->plan_ws + nn * 16);
+  long long* d_bytes = reinterpret_cast<long long*>(h->plan_ws + nn * 16 + ((3 + 2 * nn) * 4 + 7) / 8 * 8);
+  FL_CUDA(cudaMemcpyAsync(h->plan_ws, h->plan_stage.data(), nn * 16, cudaMemcpyHostToDevice, s));
+  if (h->time_steps) FL_CUDA(cudaEventRecord(h->t0, s));
+  {
+    ProfScope ps(h, FL_PROF_SHUFFLE, s);
+    if (fl::launch_plan_shuffle(d_occ, d_size, n, lo, d_plan, d_bytes, s))
+      return fail(FL_ECUDA, "planner launch: %s", cudaGetErrorString(cudaGetLastError()));
+    fl::launch_shuffle_planned(d_plan, d_ctx, lo, n / 2 + 1, h->p.kv, h->m.n_layer, h->p.pool_slots, h->Hl,
+                               h->p.max_seq, h->m.head_dim, h->m.dtype, s);
+  }
+  if (h->time_steps) FL_CUDA(cudaEventRecord(h->t1, s));
+  fl::g_launches += 2;
+  if (plan_out) FL_CUDA(cudaMemcpyAsync(plan_out, d_plan, (3 + 2 * nn) * 4, cudaMemcpyDeviceToHost, s));
+  if (bytes_out) FL_CUDA(cudaMemcpyAsync(bytes_out, d_bytes, 8, cudaMemcpyDeviceToHost, s));
+  FL_CUDA(cudaGetLastError());
   return FL_OK;
 }

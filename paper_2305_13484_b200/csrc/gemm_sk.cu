@@ -1081,7 +1081,12 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   P.csplit = 1;
   P.dpw = 0;
   const bool direct = a.epi == EPI_ACC_F32 || a.epi == EPI_STORE_F32 || a.epi == EPI_STORE || a.epi == EPI_GELU;
-  if (tiles >= npairs) {
+  if (a.indep) {
+    // one whole tile per pair and no fix-up anywhere: correct whatever part
+    // of the grid is resident (another stream's kernels may hold SMs)
+    npairs = tiles;
+    P.dpw = 1;
+  } else if (tiles >= npairs) {
     P.dpw = tiles / npairs;
   } else if (a.M >= 64 && direct && 2 * tiles <= npairs && P.kch >= 2) {
     P.csplit = npairs / tiles > 4 ? 4 : npairs / tiles;

@@ -34,6 +34,9 @@ struct GemmArgs {
   // nsplit is a multiple of 256 (whole pair tiles on either side).
   const void* x2 = nullptr;
   int nsplit = 0, ogap = 0;
+  // no cross-CTA waits (whole tiles, one per CTA pair, grid not co-resident):
+  // for launches that may share the GPU with another stream's GEMMs
+  int indep = 0;
 };
 
 // SIMT FFMA GEMM (fp32 path and the reference path for the tensor-core GEMM).
@@ -82,6 +85,10 @@ void launch_apply_tokens(const unsigned long long* keys, const fl_row* rows,
                          int32_t* req_ngen, int32_t* tok_hist, int R, int max_new, cudaStream_t s);
 
 // K10: move live KV prefixes between physical slots
+void launch_kv_copy(const int32_t* moves, int n_moves, const void* src_kv, int src_C, int src_S, void* dst_kv,
+                    int dst_C, int dst_S, int L, int Hl, int hd, int dtype, cudaStream_t s);
+void launch_shuffle_planned(const int32_t* plan, const int32_t* ctx_of, int lo, int max_moves, void* kv, int L,
+                            int C, int Hl, int S, int hd, int dtype, cudaStream_t s);
 void launch_shuffle(const int32_t* moves, int n_moves, void* kv, int L, int C, int Hl, int S,
                     int hd, int dtype, cudaStream_t s);
 

@@ -28,6 +28,7 @@ What is new underneath:
 
 from __future__ import annotations
 
+import heapq
 from collections.abc import MutableMapping
 
 from .buffer import BufferLayout, apply_shuffle, plan_shuffle
@@ -137,17 +138,31 @@ class FusionStream:
         self.device_ms: list = []     # per-iteration device time (executor runs)
         self.widest_window = 0        # widest live window seen (rows per iteration)
 
+        # overlapped preprocessing on the device: an executor
+        # with a side-stream prefill lane starts every arrived prompt at the
+        # next iteration boundary.  Under the cost clock readiness still
+        # follows the model (arrival + preprocess_ms, identical schedule);
+        # under the device clock a context is ready at its launch boundary
+        # plus the MEASURED prefill time (``_measured_pp``).
+        self._side = executor is not None and getattr(executor, "side_prefill", False)
+        self._measured_pp = self._side and clock == "device"
+        self._by_arrival = sorted(requests, key=lambda r: (r.arrival_time, r.request_id))
+        self._next_launch = 0
+        self._ready: list = []        # measured mode: heap of (ready, rid, ctx)
+        self._admitted = 0
         pending = []
-        for req in sorted(requests, key=lambda r: (r.arrival_time, r.request_id)):
+        for req in self._by_arrival:
             rid = req.request_id
             self.requests[rid] = req
             self.phase[rid] = Phase.RECEIVED
             self._emit(req.arrival_time, EventKind.ARRIVED, rid)
             self.phase[rid] = advance_phase(Phase.RECEIVED, Phase.PREPROCESSING)
             self._emit(req.arrival_time, EventKind.PREPROCESS_START, rid)
+            self.eos_at[rid] = req.actual_output_length
+            if self._measured_pp:
+                continue
             ctx = preprocess(req, params, req.arrival_time)
             self._emit(ctx.ready_time, EventKind.PREPROCESS_DONE, rid)
-            self.eos_at[rid] = req.actual_output_length
             pending.append(ctx)
         pending.sort(key=lambda c: (c.ready_time, c.request_id))
         self.pending: list = pending
@@ -175,9 +190,45 @@ class FusionStream:
 
     # -- queue ---------------------------------------------------------------
     def next_ready_time(self):
+        if self._measured_pp:
+            if not self._ready:
+                self._resolve(block=True)
+            return self._ready[0][0] if self._ready else None
         if self._next_pending >= len(self.pending):
             return None
         return self.pending[self._next_pending].ready_time
+
+    def idle_advance(self) -> None:
+        """Nothing fused: jump the clock to the next admissible context
+        (engine.py:200-201).  With measured prefill, an idle stream first
+        jumps to the next arrival and starts its prompt there."""
+        while True:
+            t = self.next_ready_time()
+            if t is not None:
+                self.now = max(self.now, t)
+                return
+            if self._next_launch >= len(self._by_arrival):
+                raise EmptyStream("no pending contexts")
+            self.now = max(self.now, self._by_arrival[self._next_launch].arrival_time)
+            self._launch_prefills()
+
+    def _launch_prefills(self) -> None:
+        """Start every prompt that arrived by ``now`` on the side stream."""
+        lo = self._next_launch
+        hi = lo
+        arr = self._by_arrival
+        while hi < len(arr) and arr[hi].arrival_time <= self.now:
+            hi += 1
+        if hi > lo:
+            self._next_launch += self.executor.launch_prefill(arr[lo:hi], self.now)
+
+    def _resolve(self, block: bool) -> None:
+        for rid, ready in self.executor.poll_prefill(block):
+            self._emit(ready, EventKind.PREPROCESS_DONE, rid)
+            req = self.requests[rid]
+            info = RuntimeInfo(rid, None, req.batch_size * self.params.request_bytes, "gpu",
+                               req.max_output_length, 0)
+            heapq.heappush(self._ready, (ready, rid, Context(rid, ready, info)))
 
     def _schedule_finish(self, rid, base, max_out):
         old = self._finish_of.pop(rid, None)
@@ -188,16 +239,33 @@ class FusionStream:
         self._finish_at.setdefault(at, []).append(rid)
         self._base[rid] = base
 
+    def _next_admissible(self):
+        """The next context in (ready, id) order if it is ready by ``now``."""
+        if self._measured_pp:
+            if self._ready and self._ready[0][0] <= self.now:
+                return heapq.heappop(self._ready)[2]
+            return None
+        pend = self.pending
+        if self._next_pending < len(pend) and pend[self._next_pending].ready_time <= self.now:
+            self._next_pending += 1
+            return pend[self._next_pending - 1]
+        return None
+
     def try_fuse_pending(self) -> int:
         """Admit, in FIFO order, every context ready at or before ``now``."""
         n = 0
-        pend = self.pending
         cap = self.max_window
-        while self._next_pending < len(pend) and pend[self._next_pending].ready_time <= self.now:
+        if self._side:
+            self._launch_prefills()
+            if self._measured_pp:
+                self._resolve(block=False)
+        while True:
             if cap is not None and self.layout.buffer_size >= cap:
                 break
-            ctx = pend[self._next_pending]
-            self._next_pending += 1
+            ctx = self._next_admissible()
+            if ctx is None:
+                break
+            self._admitted += 1
             rid = ctx.request_id
             slot = self.layout.fuse_request(rid, ctx.runtime.tensor_size)
             rt = ctx.runtime
@@ -249,14 +317,19 @@ class FusionStream:
         if self.shuffle_enabled:
             lay.trim_boundaries()
             if done and lay.has_interior_holes():
-                plan = plan_shuffle(lay)
-                if self.executor is not None and getattr(self.executor, "device_plan", False):
-                    self.executor.check_device_plan(lay, plan)   # csrc/planner.cu, bit-exact
+                on_device = self.executor is not None and getattr(self.executor, "device_plan", False)
+                if on_device:
+                    # planned and executed on the device (csrc/planner.cu + K10);
+                    # the host only mirrors the returned plan
+                    plan, dev_sh = self.executor.shuffle_on_device(lay)
+                else:
+                    plan = plan_shuffle(lay)
                 if plan.moves:
                     apply_shuffle(lay, plan)
-                    dev_sh = None
-                    if self.executor is not None:
-                        dev_sh = self.executor.on_shuffle(plan)
+                    if not on_device:
+                        dev_sh = None
+                        if self.executor is not None:
+                            dev_sh = self.executor.on_shuffle(plan)
                     if self.clock == "device":
                         self.now += dev_sh
                     else:
@@ -266,6 +339,8 @@ class FusionStream:
             lay.trim_leading()
 
     def finished_all(self) -> bool:
+        if self._measured_pp:
+            return not self.active and self._admitted >= len(self.requests)
         return not self.active and self._next_pending >= len(self.pending)
 
 
@@ -286,7 +361,7 @@ def drive(stream: FusionStream) -> FusionStream:
     """The loop of engine.py:199-203, idle jump included."""
     while not stream.finished_all():
         if not stream.active:
-            stream.now = max(stream.now, stream.next_ready_time())
+            stream.idle_advance()
         stream.try_fuse_pending()
         stream.step_iteration()
     if stream.executor is not None:

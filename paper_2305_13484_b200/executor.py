@@ -60,11 +60,16 @@ class CudaExecutor:
                  capture_logits: bool = False, device: str = "cuda", comm_id: bytes | None = None,
                  time_steps: bool = False, use_graphs: bool = True, device_plan: bool = False,
                  tiled: bool | None = None, merged_in: bool | None = None,
-                 merged_out: bool | None = None, merged_in_max_rows: int = -1):
+                 merged_out: bool | None = None, merged_in_max_rows: int = -1,
+                 prefill: str = "inline", prefill_slots: int = 32):
         if dtype not in _TORCH_DTYPE:
             raise InvalidParam(f"dtype must be f32 or bf16, got {dtype}")
+        if prefill not in ("inline", "side"):
+            raise InvalidParam(f"prefill must be 'inline' or 'side', got {prefill!r}")
         self.lib = _lib.load()
-        self.device_plan = bool(device_plan)   # plan every shuffle boundary on the device too
+        # plan AND execute every shuffle boundary on the device (fl_shuffle_planned)
+        self.device_plan = bool(device_plan)
+        self._plan_host = None
         self.device_plans = 0
         self.spec = spec
         self.prompts = prompts
@@ -238,6 +243,9 @@ class CudaExecutor:
             _lib.check(self.lib.fl_comm_init(self.handle, buf, tp_rank, tp_size))
 
         self.cs = torch.cuda.Stream(device=self.device)
+        # overlapped preprocessing: prompts run on a side stream
+        self.side_prefill = prefill == "side"
+        self.lane = _PrefillLane(self, prefill_slots) if self.side_prefill else None
         torch.cuda.synchronize(self.device)      # weights / pool written on the default stream
 
         # ---- host bookkeeping
@@ -281,6 +289,7 @@ class CudaExecutor:
         self._orphan_ctx = 0
         self._prefill_ctx = 0
         self.clock_reduce = None          # callable(ms) -> ms agreed across TP ranks
+        self._imports = []                # (staging slot, physical slot, positions, ready event)
 
     def reset(self):
         """Forget host bookkeeping between independent runs (device buffers,
@@ -298,6 +307,9 @@ class CudaExecutor:
         self._ring_owner = {}
         self.logits_log = []
         self._events = []
+        self._imports = []
+        if self.lane is not None:
+            self.lane.reset()
 
     # ----------------------------------------------------------------- utils
     @property
@@ -310,6 +322,8 @@ class CudaExecutor:
         return int(self.lib.fl_kernel_launches(self.handle))
 
     def close(self):
+        if getattr(self, "lane", None) is not None:
+            self.lane.close()
         if getattr(self, "handle", None):
             self.lib.fl_destroy(self.handle)
             self.handle = None
@@ -335,7 +349,11 @@ class CudaExecutor:
             if other % self.R == rid % self.R:
                 raise CapacityExceeded(f"state ring collision between requests {rid} and {other}")
         self._ring_owner[rid % self.R] = rid
-        self._live[rid] = {"P": P, "stop": stop, "gen": 0}
+        staged = self.lane.take(rid) if self.lane is not None else None
+        self._live[rid] = {"P": P, "stop": stop, "gen": 0, "staged": staged is not None}
+        if staged is not None:
+            q, ev = staged
+            self._imports.append((q, slot % self.C, P - 1, ev))
         self._live_ctx += P
         self._prefill_ctx += (P - 1) * P // 2
         self._new.append(rid)
@@ -366,7 +384,8 @@ class CudaExecutor:
                 pr = self.prompts[occ]
                 P = len(pr)
                 rows.append((phys, occ, P - 1, pr[P - 1], _lib.ROW_DECODE, 0))
-                prefill.extend((phys, occ, j, pr[j], _lib.ROW_PREFILL, 0) for j in range(P - 1))
+                if not self._live[occ]["staged"]:     # side-stream prefill imports its KV instead
+                    prefill.extend((phys, occ, j, pr[j], _lib.ROW_PREFILL, 0) for j in range(P - 1))
             else:
                 rows.append((phys, occ, -1, -1, _lib.ROW_DECODE, 0))
         self._n_real_dec = len(rows)
@@ -428,8 +447,22 @@ class CudaExecutor:
                 self.prefill_rows_total += len(chunk)
                 self.h2d_bytes += len(chunk) * C.sizeof(_lib.Row)
             self._pre_passes = []
+        if self._imports:
+            # prompt KV of requests prefilled on the side stream: the step
+            # waits for their prefill, then copies staging -> slot first
+            for _, _, _, ev in self._imports:
+                cs.wait_event(ev)
+            flat = (C.c_int32 * (3 * len(self._imports)))(*[v for q, d, n, _ in self._imports for v in (q, d, n)])
+            _lib.check(self.lib.fl_step_import(self.handle, C.c_void_p(self.lane.kv.data_ptr()), self.lane.Q,
+                                               self.lane.S, flat, len(self._imports)))
+            self.h2d_bytes += 12 * len(self._imports)
         _lib.check(self.lib.fl_step(self.handle, self._rows, self._n_rows, self._n_dec, int(changed),
                                     logits_ptr, C.c_void_p(cs.cuda_stream)))
+        if self._imports:
+            done = torch.cuda.Event()
+            done.record(cs)
+            self.lane.release([q for q, _, _, _ in self._imports], done)
+            self._imports = []
         self._account(main_ctx, self._n_rows)
         self.iterations += 1
         self.rows_total += self._n_rows
@@ -504,15 +537,71 @@ class CudaExecutor:
             return self.clock_reduce(ms) if self.clock_reduce else ms
         return None
 
-    def check_device_plan(self, layout, plan) -> None:
-        """Run Alg. 1 + plan_shuffle on the device (csrc/planner.cu) for this
-        boundary and require it to equal the host plan (SURVEY 8f #3)."""
-        from .devplan import device_plan_shuffle
-        from .errors import DeviceError
-        dplan = device_plan_shuffle(layout, device=self.device, stream=self.cs)
+    def launch_prefill(self, requests, now: float) -> int:
+        """Start the prompts of ``requests`` (arrived by ``now``) on the side
+        stream; returns how many were launched (the lane has a bounded number
+        of staging slots; the rest wait for the next boundary)."""
+        return self.lane.launch(requests, now)
+
+    def poll_prefill(self, block: bool = False) -> list:
+        """[(rid, ready time)] of side-stream prefills that completed: ready =
+        the boundary they were launched at + their measured device time."""
+        return self.lane.poll(block)
+
+    def shuffle_on_device(self, layout):
+        """A shuffle boundary planned AND executed on the device (SURVEY 8f #3,
+        ``device_plan=True``): the window's occupancy goes up once, Alg. 1 +
+        plan_shuffle run in csrc/planner.cu and K10 copies from the device
+        move list (fl_shuffle_planned); the host planner is not called.  The
+        plan comes back through a pinned buffer only so the host can mirror
+        the layout (its next rows and evictions depend on it).  Returns
+        (ShufflePlan, device ms or None)."""
+        from .buffer import ShuffleMove, ShufflePlan
+        lo, n = layout.buffer_offset, layout.buffer_size
+        if n > self.C:
+            raise CapacityExceeded(f"live window of {n} slots exceeds the KV pool ({self.C})")
+        slots = layout.slots
+        occ, size, ctx = [], [], []
+        for s in range(lo, lo + n):
+            rid = slots[s].occupant
+            occ.append(0 if rid is None else 1)
+            size.append(slots[s].size)
+            info = self._live.get(rid) if rid is not None else None
+            ctx.append(info["P"] + info["gen"] - 1 if info else 0)
+        if self._plan_host is None:
+            self._plan_host = torch.empty(3 + 2 * max(self.C, 1), dtype=torch.int32, pin_memory=True)
+            self._plan_bytes = torch.empty(1, dtype=torch.int64, pin_memory=True)
+        a_occ = (C.c_int32 * max(n, 1))(*occ)
+        a_size = (C.c_int64 * max(n, 1))(*size)
+        a_ctx = (C.c_int32 * max(n, 1))(*ctx)
+        cs = self.stream
+        _lib.check(self.lib.fl_shuffle_planned(self.handle, a_occ, a_size, a_ctx, n, lo,
+                                               C.c_void_p(self._plan_host.data_ptr()),
+                                               C.c_void_p(self._plan_bytes.data_ptr()), C.c_void_p(cs.cuda_stream)))
+        self.h2d_bytes += 16 * n
+        self.d2h_bytes_plans = getattr(self, "d2h_bytes_plans", 0) + 4 * (3 + 2 * n) + 8
         self.device_plans += 1
-        if dplan != plan:
-            raise DeviceError(f"device plan {dplan} != host plan {plan}")
+        ms = self._last_ms() if self._lib_timing else None      # synchronises on the step events
+        cs.synchronize()                                          # the plan read-back landed
+        out = self._plan_host
+        offset, wlen, nm = int(out[0]), int(out[1]), int(out[2])
+        moves = tuple(ShuffleMove(slots[int(out[3 + 2 * r])].occupant, int(out[3 + 2 * r]), int(out[4 + 2 * r]),
+                                  slots[int(out[3 + 2 * r])].size) for r in range(nm))
+        plan = ShufflePlan(moves, offset, wlen, int(self._plan_bytes[0]), layout.version)
+        if moves:
+            nbytes = 0
+            for m in moves:
+                info = self._live[m.request_id]
+                nbytes += 2 * (info["P"] + info["gen"] - 1) * self.spec.kv_bytes_per_token(
+                    2 if self.dtype == "bf16" else 4, self.tp_size)
+                self._orphans.pop(m.src_slot, None)
+            self.moved_kv_bytes += nbytes
+            self.shuffles += 1
+            if ms is not None:
+                self.shuffle_log.append((len(moves), nbytes, ms))
+        if ms is not None and self.clock_reduce:
+            ms = self.clock_reduce(ms)
+        return plan, ms
 
     def on_drain(self, stream):
         self.cs.synchronize()
@@ -557,3 +646,126 @@ class CudaExecutor:
                                                 C.byref(f)))
             out[name] = {"ms": ms.value, "records": n.value, "bytes": b.value, "flops": f.value}
         return out
+
+
+class _PrefillLane:
+    """Overlapped preprocessing: the paper's T_pp threads
+     that prepare a request's context while the fused stream
+    keeps iterating; the reference models them as an independent delay
+    (engine.py:6-8,24-42,69-83).
+
+    A second library handle over the same weights runs each arrived prompt's
+    PREFILL rows (n_dec = 0 steps) on a side stream into a small staging
+    pool [L][Q][2][Hl][S_p][hd] (S_p = prompt length); its GEMMs avoid
+    cross-CTA waits (fl_set_side_stream) so it can share the SMs with the
+    serving stream.  At fusion the serving step imports the prompt KV into
+    the request's slot (fl_step_import) after waiting for the prefill's
+    event; the staging slot is reused once that import ran.  Prompts of a
+    boundary are batched into one prefill pass (one weight read)."""
+
+    def __init__(self, ex: CudaExecutor, slots: int):
+        spec = ex.spec
+        self.ex = ex
+        self.lib = ex.lib
+        self.Q = max(1, int(slots))
+        self.S = max(2, max(len(p) for p in ex.prompts.values()) if ex.prompts else 2)
+        tdt = _TORCH_DTYPE[ex.dtype]
+        hl = spec.n_head // ex.tp_size
+        dev = ex.device
+        self.kv = torch.empty((spec.n_layer, self.Q, 2, hl, self.S, spec.head_dim), dtype=tdt, device=dev)
+        i32 = dict(dtype=torch.int32, device=dev)
+        self._state = [torch.zeros(1, **i32) for _ in range(3)] + [torch.zeros((1, 1), **i32)]
+        self.max_rows = bucket(min(self.Q * (self.S - 1), 512))
+        self.pdesc = _lib.PoolDesc(self.Q, self.S, self.max_rows, 1, 1, ex.pdesc.use_tensor_cores,
+                                   self.kv.data_ptr(), *[t.data_ptr() for t in self._state], None, 0)
+        nbytes = self.lib.fl_workspace_bytes(C.byref(ex.mdesc), C.byref(self.pdesc))
+        if nbytes == 0:
+            _lib.check(-1)
+        self.ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        self.pdesc.workspace = self.ws.data_ptr()
+        self.pdesc.workspace_bytes = nbytes
+        h = C.c_void_p()
+        _lib.check(self.lib.fl_create(C.byref(ex.mdesc), C.byref(self.pdesc), C.byref(h)))
+        self.handle = h
+        _lib.check(self.lib.fl_set_side_stream(h, 1))
+        if ex.merged:
+            _lib.check(self.lib.fl_set_merged_out(h, ex._wcat, ex._bcat))
+        if ex.merged_in:
+            _lib.check(self.lib.fl_set_merged_in(h, ex._win, ex._bin, int(ex.merged_in_max_rows)))
+        _lib.check(self.lib.fl_configure(h, int(ex.use_graphs), 8, 0))
+        if ex.tp_size > 1:
+            raise InvalidParam("side-stream prefill is single-GPU (its collectives would need a second "
+                               "communicator)")
+        self.ps = torch.cuda.Stream(device=dev)
+        self.launched_rows = 0
+        self.passes = 0
+        self.reset()
+
+    def reset(self):
+        self.free = list(range(self.Q))
+        self.free_ev = {}          # staging slot -> event after the import that last read it
+        self.inflight = {}         # rid -> [slot, e0, e1, launch time, resolved]
+        self.ready = {}            # rid -> (slot, e1) prefilled, not yet fused
+
+    def launch(self, requests, now: float) -> int:
+        rids = []
+        for req in requests:
+            if not self.free:
+                break
+            rids.append((req.request_id, self.free.pop(0)))
+        if not rids:
+            return 0
+        ex = self.ex
+        rows = []
+        for rid, q in rids:
+            pr = ex.prompts[rid]
+            rows.extend((q, rid, j, pr[j], _lib.ROW_PREFILL, 0) for j in range(len(pr) - 1))
+            ev = self.free_ev.pop(q, None)
+            if ev is not None:
+                self.ps.wait_event(ev)          # the previous occupant's import has read it
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(self.ps)
+        for i in range(0, len(rows), self.max_rows):
+            chunk = rows[i:i + self.max_rows]
+            chunk = chunk + [_PAD] * (bucket(len(chunk)) - len(chunk))
+            arr = (_lib.Row * len(chunk))(*[_lib.Row(*r) for r in chunk])
+            _lib.check(self.lib.fl_step(self.handle, arr, len(chunk), 0, 1, None, C.c_void_p(self.ps.cuda_stream)))
+            ex.h2d_bytes += len(chunk) * C.sizeof(_lib.Row)
+            self.launched_rows += len(chunk)
+            self.passes += 1
+        e1.record(self.ps)
+        for rid, q in rids:
+            self.inflight[rid] = [q, e0, e1, now]
+        return len(rids)
+
+    def poll(self, block: bool) -> list:
+        out = []
+        for rid, (q, e0, e1, t) in list(self.inflight.items()):
+            if not block and not e1.query():
+                continue
+            e1.synchronize()
+            out.append((rid, t + e0.elapsed_time(e1)))
+            self.ready[rid] = (q, e1)
+            del self.inflight[rid]
+        return out
+
+    def take(self, rid):
+        """(staging slot, event) of rid's finished or in-flight prefill, or
+        None (never launched: the prompt then runs inline in the fused step)."""
+        if rid in self.ready:
+            return self.ready.pop(rid)
+        if rid in self.inflight:
+            q, _, e1, _ = self.inflight.pop(rid)
+            return q, e1
+        return None
+
+    def release(self, slots, ev):
+        for q in slots:
+            self.free_ev[q] = ev
+            self.free.append(q)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.fl_destroy(self.handle)
+            self.handle = None

@@ -66,14 +66,42 @@ def test_device_plan_rejects_oversized_window():
         devplan.device_plan_shuffle(lay)
 
 
-def test_device_planner_in_the_serving_loop():
-    """C1 with every shuffle boundary also planned on the device: plans equal
-    the host's (the executor raises otherwise) and the trace is still the
-    reference's golden trace."""
-    from harness import run_device, scenario_requests
+@pytest.mark.parametrize("shuffle_seed", [1, 7])
+def test_device_planner_in_the_serving_loop(monkeypatch, shuffle_seed):
+    """every shuffle boundary planned AND executed on the device
+    (fl_shuffle_planned: Alg. 1 + plan_shuffle in csrc/planner.cu, K10 fed
+    from the device move list).  The host planner is taken out of the loop
+    (it raises if called), yet the trace is the reference's golden trace and
+    the tokens equal the host-planned run's and the oracle's."""
+    from harness import oracle_check, run_device, scenario_requests
     from schedule_dump import sha
+    import paper_2305_13484_b200.engine as eng
     gold = {c["name"]: c for c in load("schedules.json.gz")["cases"]}["c1/tp1/on"]
-    reqs = scenario_requests(32, 20.0, 8, 64, 64, 16, seed=1)
+    reqs = scenario_requests(32, 20.0, 8, 64, 64, 16, seed=shuffle_seed)
+    _, _, host, _, _ = run_device("tiny", reqs, dtype="f32", shuffle=True, capture_logits=False)
+
+    def no_host_plan(*a, **k):
+        raise AssertionError("host plan_shuffle called in device-plan mode")
+    monkeypatch.setattr(eng, "plan_shuffle", no_host_plan)
     trace, st, ex, prompts, w32 = run_device("tiny", reqs, dtype="f32", shuffle=True, device_plan=True)
-    assert sha(trace.format_lines()) == gold["trace_sha"]
+    if shuffle_seed == 1:
+        assert sha(trace.format_lines()) == gold["trace_sha"]
+    assert ex.device_plans > 0 and ex.shuffles == host.shuffles > 0
+    assert ex.moved_kv_bytes == host.moved_kv_bytes
+    assert ex.tokens() == host.tokens()
+    stats = oracle_check("tiny", ex, prompts, w32, logit_atol=2e-3, logit_rtol=1e-3, margin=5e-3)
+    assert stats["mismatched"] == 0, stats
+
+
+def test_device_planner_device_clock_bf16():
+    """Device clock + tcgen05 path: the measured shuffle time covers planner
+    + K10; all requests complete with their full token counts."""
+    from harness import run_device, scenario_requests
+    reqs = scenario_requests(24, 2.0, 4, 40, 40, 16, seed=3)
+    trace, st, ex, _, _ = run_device("gptj-mini", reqs, dtype="bf16", shuffle=True, device_plan=True,
+                                     clock="device", params=fl.CostParams(preprocess_ms=0.0),
+                                     capture_logits=False)
     assert ex.device_plans > 0
+    assert all(ms > 0 for _, _, ms in ex.shuffle_log)
+    toks = ex.tokens()
+    assert [len(toks[r.request_id]) for r in reqs] == [r.actual_output_length for r in reqs]
