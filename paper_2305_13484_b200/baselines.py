@@ -81,8 +81,6 @@ def run_dynamic_batching(requests, cfg: BatchWindowConfig, params: CostParams,
     from .engine import check_tp
     check_tp(tp or TPConfig(), executor, clock)
     tp = tp or TPConfig()
-    from .engine import check_tp
-    check_tp(tp, executor, "cost")
     ordered = sorted(requests, key=lambda r: (r.arrival_time, r.request_id))
     ev = []
     for r in ordered:
@@ -114,10 +112,10 @@ def run_dynamic_batching(requests, cfg: BatchWindowConfig, params: CostParams,
         for k in range(1, n_iters + 1):
             dur = model_dur
             if bs is not None:
-                dev = executor.run_iteration(bs)
+                executor.run_iteration(bs)
                 bs.iteration_index += 1
                 if clock == "device":
-                    dur = dev
+                    dur = executor.iteration_ms()
             t = start + k * dur if clock == "cost" else t + dur
             for m in members:
                 if k <= m.actual_output_length:

@@ -198,6 +198,7 @@ struct SkParams {
   int slot_elems;   // floats per (pair, half) slot
   int vec;          // out rows 16-byte aligned: vector stores
   int csplit;       // >1: tile K split evenly over S pairs, spread reduction
+  int red;          // EPI_ACC_F32: pieces of split tiles red.add into the residual (no fix-up)
   int slice;        // tokens per pair (mt * bn)
   int kpb;          // 64-wide K sub-chunks per unit/stage (2: one 3-D request per operand)
   int ntm;          // token tiles
@@ -224,15 +225,21 @@ FL_DEV bool act_on(const SkParams& P, int n) { return !P.nsplit || n >= P.nsplit
 struct Ranges {
   int lo[2], hi[2];
 };
+// Processing order: the stream-K share FIRST, then the whole tiles.  A split
+// tile's pieces other than k = 0 are then the very first segments of the
+// following pairs (published right away), and the k = 0 owner's fold-in and
+// epilogue overlap the MMAs of its whole tiles instead of trailing the
+// launch (an owner last in its range added ~8 us of exposed fix-up at 128
+// tokens: tools/gemm_cta_dump.py).
 FL_DEV Ranges pair_ranges(const SkParams& P, int q) {
   Ranges r;
   const int dpu = P.dpw * P.kch;
-  r.lo[0] = q * dpu;
-  r.hi[0] = r.lo[0] + dpu;
+  r.lo[1] = q * dpu;
+  r.hi[1] = r.lo[1] + dpu;
   const int base = dpu * P.npairs, ur = P.units - base;
   const int qs = q < P.nsk ? q : P.nsk;
-  r.lo[1] = base + static_cast<int>((static_cast<long long>(qs) * ur) / P.nsk);
-  r.hi[1] = q < P.nsk ? base + static_cast<int>((static_cast<long long>(q + 1) * ur) / P.nsk) : r.lo[1];
+  r.lo[0] = base + static_cast<int>((static_cast<long long>(qs) * ur) / P.nsk);
+  r.hi[0] = q < P.nsk ? base + static_cast<int>((static_cast<long long>(q + 1) * ur) / P.nsk) : r.lo[0];
   return r;
 }
 // the pair whose stream-K range holds unit x (x past the whole-tile prefix)
@@ -531,7 +538,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       // [s, s+1) * mcount / S over the S slots and runs the epilogue -- the
       // fix-up is spread over the S pairs instead of serialised in one owner.
       const int S = P.csplit;
-      const int t = R.lo[1] / kch, piece = pair - t * S;
+      const int t = R.lo[0] / kch, piece = pair - t * S;
       const int tm = t / P.ntn, tn = t - tm * P.ntn;
       const int m0 = tm * P.span;
       const int mcount = min(P.slice, P.M - m0);
@@ -676,9 +683,11 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       // segment mode: final epilogue (whole tile, or the k = 0 owner of a split
       // tile after folding in the later pieces) or publish (a later piece of a
       // split tile: the first segment of its pair's stream-K range)
-      enum { FINAL = 0, PUB = 2 };
+      enum { FINAL = 0, PUB = 2, RED = 3 };
       int mode = FINAL, plast = pair;      // plast: last pair holding a piece
-      if (!whole) {
+      if (!whole && EPI == EPI_ACC_F32 && P.red) {
+        mode = RED;                        // residual: every piece red.adds its partial
+      } else if (!whole) {
         if (klo > 0) {
           mode = PUB;
         } else {
@@ -723,6 +732,16 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         tmem_ld32(tacc + cb, r);
         const int ncol = min(32, mcount - cb);
         if (P.dbg) e_ld += clock64() - tl0;
+        if (EPI == EPI_ACC_F32 && mode == RED && !vec) {
+          // unaligned residual rows: scalar float atomics, lane = weight row
+          if (nok) {
+            float* dst = static_cast<float*>(P.out) + static_cast<size_t>(m0 + cb) * P.ldo + n;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j < ncol) atomicAdd(dst + static_cast<size_t>(j) * P.ldo, __uint_as_float(r[j]) + bv);
+          }
+          continue;
+        }
         if ((EPI == EPI_ARGMAX || !vec) && mode == FINAL) {
           // lane-per-weight-row epilogues (argmax reduce, unaligned outputs)
           float v[32];
@@ -780,7 +799,19 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         const int c4 = (lane & 7) * 4;
         const int jb = lane >> 3;
         const int nn = nbase + quarter * 32 + c4;
-        if (mode == PUB) {
+        if (EPI == EPI_ACC_F32 && mode == RED) {
+          float* dst = static_cast<float*>(P.out) + static_cast<size_t>(m0 + cb) * P.ldo + nn;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int j = i * 4 + jb;
+            if (j < ncol) {
+              const float4 v = *reinterpret_cast<const float4*>(ws_ + j * SK_STG_LD + c4);
+              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + static_cast<size_t>(j) * P.ldo),
+                           "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                           : "memory");
+            }
+          }
+        } else if (mode == PUB) {
           float* dst = pub + static_cast<size_t>(cb) * SK_BM + quarter * 32 + c4;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
@@ -1081,6 +1112,8 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   P.csplit = 1;
   P.dpw = 0;
   const bool direct = a.epi == EPI_ACC_F32 || a.epi == EPI_STORE_F32 || a.epi == EPI_STORE || a.epi == EPI_GELU;
+  // split residual tiles always red.add (no fix-up waits for EPI_ACC_F32)
+  P.red = (a.epi == EPI_ACC_F32 && !a.indep) ? 1 : 0;
   if (a.indep) {
     // one whole tile per pair and no fix-up anywhere: correct whatever part
     // of the grid is resident (another stream's kernels may hold SMs)
@@ -1088,6 +1121,10 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
     P.dpw = 1;
   } else if (tiles >= npairs) {
     P.dpw = tiles / npairs;
+  } else if (a.epi == EPI_ACC_F32 && a.K > 1024) {
+    // residual GEMMs (attn-out / FFN-down, 16 tiles): pure stream-K over all
+    // pairs, every piece of a split tile red.adds into the fp32 residual --
+    // no fix-up, no waits, all 148 SMs stream equal weight bytes
   } else if (a.M >= 64 && direct && 2 * tiles <= npairs && P.kch >= 2) {
     P.csplit = npairs / tiles > 4 ? 4 : npairs / tiles;
     if (P.csplit > P.kch) P.csplit = P.kch;                // every piece holds >= 1 K unit

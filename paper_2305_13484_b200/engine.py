@@ -145,6 +145,7 @@ class FusionStream:
         # under the device clock a context is ready at its launch boundary
         # plus the MEASURED prefill time (``_measured_pp``).
         self._side = executor is not None and getattr(executor, "side_prefill", False)
+        self._eos = getattr(executor, "eos_token", None) if executor is not None else None
         self._measured_pp = self._side and clock == "device"
         self._by_arrival = sorted(requests, key=lambda r: (r.arrival_time, r.request_id))
         self._next_launch = 0
@@ -158,7 +159,10 @@ class FusionStream:
             self._emit(req.arrival_time, EventKind.ARRIVED, rid)
             self.phase[rid] = advance_phase(Phase.RECEIVED, Phase.PREPROCESSING)
             self._emit(req.arrival_time, EventKind.PREPROCESS_START, rid)
-            self.eos_at[rid] = req.actual_output_length
+            # EOS mode (executor.eos_token): the stop is discovered on the
+            # device; until then only max_output_length bounds the request
+            self.eos_at[rid] = (req.max_output_length if self._eos is not None
+                                else req.actual_output_length)
             if self._measured_pp:
                 continue
             ctx = preprocess(req, params, req.arrival_time)
@@ -281,26 +285,35 @@ class FusionStream:
 
     # -- the atomic iteration --------------------------------------------------
     def step_iteration(self) -> None:
+        """One atomic iteration (engine.py:128-177).  With an executor the
+        step is launched first; the end-of-iteration layout work (evictions,
+        trims, the shuffle plan and its K10 launch) needs no clock and runs on
+        the host while the step executes; the clock advance and the events
+        follow once the step's (measured or modelled) duration is known."""
         if not self.active:
             raise EmptyStream("no fused requests to iterate")
         lay = self.layout
         if lay.buffer_size > self.widest_window:
             self.widest_window = lay.buffer_size
-        dev = None
-        if self.executor is not None:
-            dev = self.executor.run_iteration(self)
-            if dev is not None:
-                self.device_ms.append(dev)
-        if self.clock == "device":
-            duration = dev
-        else:
+        ex = self.executor
+        dev_clock = self.clock == "device"
+        if ex is not None:
+            ex.run_iteration(self)            # launched (device clock: timed, read below)
+        if not dev_clock:
             duration = iteration_time(len(self.active), lay.live_bytes(), self.params, self.tp)
-        self.now += duration
-        now = self.now
-        if self.record_tokens:
-            self._tok.append((len(self._ev), now, tuple(self.active._rows), self.iteration_index + 1))
+        snap = tuple(self.active._rows) if self.record_tokens else None
+        it = self.iteration_index
 
-        done = self._finish_at.pop(self.iteration_index, ())
+        if self._eos is not None:
+            # data-dependent stop: a request whose token of this iteration is
+            # EOS finishes now -- record_token's eos_at (core.py:108-123)
+            # becomes the iteration count at which the token appeared
+            for rid in ex.eos_hits():
+                base = self._base[rid]
+                if self._finish_of.get(rid) != it:
+                    self.eos_at[rid] = it - base + 1
+                    self._schedule_finish(rid, base, self.requests[rid].max_output_length)
+        done = self._finish_at.pop(it, ())
         rows = self.active._rows
         for rid in done:
             slot = lay.per_request_offset[rid]
@@ -308,35 +321,43 @@ class FusionStream:
             del rows[rid]
             del self._finish_of[rid]
             self.phase[rid] = advance_phase(self.phase[rid], Phase.FINISHED)
-            self._emit(now, EventKind.EVICTED, rid)
-            if self.executor is not None:
-                self.executor.on_evict(rid, slot)
-        self._emit(now, EventKind.ITERATION_COMPLETED, None, duration)
+            if ex is not None:
+                ex.on_evict(rid, slot)
         self.iteration_index += 1
 
+        plan = None
         if self.shuffle_enabled:
             lay.trim_boundaries()
             if done and lay.has_interior_holes():
-                on_device = self.executor is not None and getattr(self.executor, "device_plan", False)
+                on_device = ex is not None and getattr(ex, "device_plan", False)
                 if on_device:
                     # planned and executed on the device (csrc/planner.cu + K10);
                     # the host only mirrors the returned plan
-                    plan, dev_sh = self.executor.shuffle_on_device(lay)
+                    plan = ex.shuffle_on_device(lay)
                 else:
                     plan = plan_shuffle(lay)
                 if plan.moves:
                     apply_shuffle(lay, plan)
-                    if not on_device:
-                        dev_sh = None
-                        if self.executor is not None:
-                            dev_sh = self.executor.on_shuffle(plan)
-                    if self.clock == "device":
-                        self.now += dev_sh
-                    else:
-                        self.now += shuffle_time(plan.total_bytes_moved, self.params)
-                    self._emit(self.now, EventKind.SHUFFLE_EXECUTED, None, plan.total_bytes_moved)
+                    if not on_device and ex is not None:
+                        ex.on_shuffle(plan, timed=dev_clock)
+                else:
+                    plan = None
         else:
             lay.trim_leading()
+
+        if dev_clock:
+            duration = ex.iteration_ms()
+            self.device_ms.append(duration)
+        self.now += duration
+        now = self.now
+        if snap is not None:
+            self._tok.append((len(self._ev), now, snap, it + 1))
+        for rid in done:
+            self._emit(now, EventKind.EVICTED, rid)
+        self._emit(now, EventKind.ITERATION_COMPLETED, None, duration)
+        if plan is not None:
+            self.now += ex.shuffle_ms() if dev_clock else shuffle_time(plan.total_bytes_moved, self.params)
+            self._emit(self.now, EventKind.SHUFFLE_EXECUTED, None, plan.total_bytes_moved)
 
     def finished_all(self) -> bool:
         if self._measured_pp:

@@ -28,6 +28,7 @@ from __future__ import annotations
 
 import ctypes as C
 
+import numpy as np
 import torch
 
 from . import _lib
@@ -38,6 +39,26 @@ GEMM_KEYS = ("w_qkv", "w_o", "w_fc", "w_proj")
 
 _TORCH_DTYPE = {"f32": torch.float32, "bf16": torch.bfloat16}
 _PAD = (0, -1, -1, -1, _lib.ROW_ORPHAN, 1)
+_ROW_P = C.POINTER(_lib.Row)
+# streams / events / synchronisation go through this name, so the host path
+# can be driven on CPU against a stub library (tests/test_tp_host.py)
+_cuda = torch.cuda
+
+
+def _pad_rows(a):
+    """Pad an int32 [n, 6] row table to its bucket with PAD rows."""
+    n = len(a)
+    b = bucket(n)
+    if b == n:
+        return np.ascontiguousarray(a)
+    out = np.empty((b, 6), dtype=np.int32)
+    out[:n] = a
+    out[n:] = _PAD
+    return out
+
+
+def _rows_ptr(a):
+    return a.ctypes.data_as(_ROW_P)
 
 
 def bucket(n: int) -> int:
@@ -61,12 +82,17 @@ class CudaExecutor:
                  time_steps: bool = False, use_graphs: bool = True, device_plan: bool = False,
                  tiled: bool | None = None, merged_in: bool | None = None,
                  merged_out: bool | None = None, merged_in_max_rows: int = -1,
-                 prefill: str = "inline", prefill_slots: int = 32):
+                 prefill: str = "inline", prefill_slots: int = 32, eos_token: int | None = None):
         if dtype not in _TORCH_DTYPE:
             raise InvalidParam(f"dtype must be f32 or bf16, got {dtype}")
         if prefill not in ("inline", "side"):
             raise InvalidParam(f"prefill must be 'inline' or 'side', got {prefill!r}")
         self.lib = _lib.load()
+        # data-dependent stop: a request finishes when its greedy
+        # token equals eos_token (or at max_output_length); None = the
+        # reference's pre-sampled actual_output_length
+        self.eos_token = None if eos_token is None else int(eos_token)
+        self._tok_host = None
         # plan AND execute every shuffle boundary on the device (fl_shuffle_planned)
         self.device_plan = bool(device_plan)
         self._plan_host = None
@@ -153,7 +179,7 @@ class CudaExecutor:
                 n, k = t.shape
                 tt = torch.empty(self.lib.fl_tiled_weight_bytes(n, k) // 2, dtype=tdt, device=self.device)
                 _lib.check(self.lib.fl_tile_weight(C.c_void_p(t.data_ptr()), n, k, C.c_void_p(tt.data_ptr()),
-                                                   C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)))
+                                                   C.c_void_p(_cuda.current_stream(self.device).cuda_stream)))
                 self.w[name] = tt
                 del t
         if self.merged_in:
@@ -192,7 +218,7 @@ class CudaExecutor:
             # the workspace and the allocator
             es = 2 if dtype == "bf16" else 4
             slot = spec.n_layer * 2 * hl * self.S * spec.head_dim * es
-            free, _ = torch.cuda.mem_get_info(self.device)
+            free, _ = _cuda.mem_get_info(self.device)
             self.C = max(1, min(state_slots, int((free - 6 * 2**30) // slot)))
             self.max_rows = bucket(max_rows or (self.C + 16 * (input_len or 32)))
             if self.max_rows < bucket(self.C) + 64:
@@ -234,7 +260,6 @@ class CudaExecutor:
             _lib.check(self.lib.fl_set_merged_in(self.handle, self._win, self._bin,
                                                  int(self.merged_in_max_rows)))
         self.use_graphs = use_graphs
-        self._lib_timing = False
         _lib.check(self.lib.fl_configure(self.handle, int(use_graphs), 8, 0))
         if tp_size > 1 and comm_id is None:
             raise InvalidParam("tp_size > 1 needs comm_id (see tp.make_comm_id)")
@@ -242,11 +267,12 @@ class CudaExecutor:
             buf = C.create_string_buffer(bytes(comm_id), 128)
             _lib.check(self.lib.fl_comm_init(self.handle, buf, tp_rank, tp_size))
 
-        self.cs = torch.cuda.Stream(device=self.device)
+        self.cs = _cuda.Stream(device=self.device)
         # overlapped preprocessing: prompts run on a side stream
-        self.side_prefill = prefill == "side"
-        self.lane = _PrefillLane(self, prefill_slots) if self.side_prefill else None
-        torch.cuda.synchronize(self.device)      # weights / pool written on the default stream
+        self.side_prefill = False
+        self.lane = None
+        self.set_prefill(prefill, prefill_slots)
+        _cuda.synchronize(self.device)      # weights / pool written on the default stream
 
         # ---- host bookkeeping
         self.capture_logits = capture_logits
@@ -290,6 +316,10 @@ class CudaExecutor:
         self._prefill_ctx = 0
         self.clock_reduce = None          # callable(ms) -> ms agreed across TP ranks
         self._imports = []                # (staging slot, physical slot, positions, ready event)
+        self._prompt_cache = {}
+        self._step_ev = self._shuffle_ev = None
+        self._shuffle_pending = None
+        self._n_orph = 0
 
     def reset(self):
         """Forget host bookkeeping between independent runs (device buffers,
@@ -310,6 +340,19 @@ class CudaExecutor:
         self._imports = []
         if self.lane is not None:
             self.lane.reset()
+            if not self.side_prefill:
+                self.lane.close()
+                self.lane = None
+
+    def set_prefill(self, mode: str, slots: int = 32) -> None:
+        """'inline': prompts enter the admitting fused step as PREFILL rows;
+        'side': they run on a side stream as soon as they arrive
+        (_PrefillLane).  Switch between serves, not inside one."""
+        if mode not in ("inline", "side"):
+            raise InvalidParam(f"prefill must be 'inline' or 'side', got {mode!r}")
+        self.side_prefill = mode == "side"
+        if self.side_prefill and self.lane is None:
+            self.lane = _PrefillLane(self, slots)
 
     # ----------------------------------------------------------------- utils
     @property
@@ -340,7 +383,12 @@ class CudaExecutor:
         P = len(prompt)
         if request is not None and P != request.input_len:
             raise InvalidParam(f"request {rid}: prompt has {P} tokens, input_len {request.input_len}")
-        stop = min(request.actual_output_length, request.max_output_length) if request else self.max_new
+        if request is None:
+            stop = self.max_new
+        elif self.eos_token is not None:
+            stop = request.max_output_length        # the EOS token may end it earlier
+        else:
+            stop = min(request.actual_output_length, request.max_output_length)
         if P + stop - 1 > self.S:
             raise CapacityExceeded(f"request {rid} needs {P + stop - 1} positions > max_seq {self.S}")
         if stop > self.max_new:
@@ -349,7 +397,7 @@ class CudaExecutor:
             if other % self.R == rid % self.R:
                 raise CapacityExceeded(f"state ring collision between requests {rid} and {other}")
         self._ring_owner[rid % self.R] = rid
-        staged = self.lane.take(rid) if self.lane is not None else None
+        staged = self.lane.take(rid) if self.side_prefill else None
         self._live[rid] = {"P": P, "stop": stop, "gen": 0, "staged": staged is not None}
         if staged is not None:
             q, ev = staged
@@ -363,54 +411,85 @@ class CudaExecutor:
         info = self._live.pop(rid)
         self._live_ctx -= info["P"] + info["gen"]
         # KV positions written: prefill 0..P-2 plus one per generated token
-        self._orphans[slot] = info["P"] + info["stop"] - 1
+        self._orphans[slot] = info["P"] + info["gen"] - 1
 
     def _build_rows(self, layout):
+        """The iteration's row table as one int32 [n, 6] array (fl_row
+        layout): window rows (DECODE / ORPHAN, window order) padded to a
+        bucket, then the prompt rows of newly fused requests.  Vectorised:
+        the window is read once, everything else is numpy."""
         lo, n = layout.buffer_offset, layout.buffer_size
         if n > self.C:
             raise CapacityExceeded(f"live window of {n} slots exceeds the KV pool ({self.C})")
+        if self._orphans:
+            for s in [k for k in self._orphans if k < lo]:
+                del self._orphans[s]
         slots = layout.slots
-        new = set(self._new)
-        for s in [k for k in self._orphans if k < lo]:
-            del self._orphans[s]
-        rows = []
+        occ = np.fromiter((-1 if sl.occupant is None else sl.occupant for sl in slots[lo:lo + n]),
+                          dtype=np.int32, count=n)
+        n_dec = bucket(n)
+        win = np.empty((n_dec, 6), dtype=np.int32)
+        win[:] = _PAD
+        w = win[:n]
+        w[:, 0] = np.arange(lo, lo + n, dtype=np.int64) % self.C
+        w[:, 1] = occ
+        w[:, 2] = -1
+        w[:, 3] = -1
+        orph = occ < 0
+        w[:, 4] = np.where(orph, _lib.ROW_ORPHAN, _lib.ROW_DECODE)
+        w[:, 5] = 0
+        if orph.any():
+            idx = np.nonzero(orph)[0]
+            get = self._orphans.get
+            w[idx, 5] = [get(lo + int(k), 1) for k in idx]
         prefill = []
-        for s in range(lo, lo + n):
-            occ = slots[s].occupant
-            phys = s % self.C
-            if occ is None:
-                rows.append((phys, -1, -1, -1, _lib.ROW_ORPHAN, self._orphans.get(s, 1)))
-            elif occ in new:
-                pr = self.prompts[occ]
+        if self._new:
+            pos = {int(r): k for k, r in enumerate(occ) if r >= 0} if len(self._new) > 4 else None
+            for rid in self._new:
+                k = pos[rid] if pos is not None else int(np.nonzero(occ == rid)[0][0])
+                pr = self._prompt_np(rid)
                 P = len(pr)
-                rows.append((phys, occ, P - 1, pr[P - 1], _lib.ROW_DECODE, 0))
-                if not self._live[occ]["staged"]:     # side-stream prefill imports its KV instead
-                    prefill.extend((phys, occ, j, pr[j], _lib.ROW_PREFILL, 0) for j in range(P - 1))
-            else:
-                rows.append((phys, occ, -1, -1, _lib.ROW_DECODE, 0))
-        self._n_real_dec = len(rows)
-        rows.extend([_PAD] * (bucket(len(rows)) - len(rows)))
-        n_dec = len(rows)
+                w[k, 2] = P - 1
+                w[k, 3] = pr[P - 1]
+                if not self._live[rid]["staged"] and P > 1:   # side-stream prefill imports its KV instead
+                    blk = np.empty((P - 1, 6), dtype=np.int32)
+                    blk[:, 0] = w[k, 0]
+                    blk[:, 1] = rid
+                    blk[:, 2] = np.arange(P - 1)
+                    blk[:, 3] = pr[:P - 1]
+                    blk[:, 4] = _lib.ROW_PREFILL
+                    blk[:, 5] = 0
+                    prefill.append(blk)
+        self._n_real_dec = n
+        self._n_orph = int(orph.sum())
+        self._orphan_ctx = int(w[orph, 5].sum()) if self._n_orph else 0
         # prompt rows beyond the iteration's row budget run first as
         # prefill-only passes (their KV lands before the decode rows read it)
         room = self.max_rows - n_dec
         if room < 0:
             raise CapacityExceeded(f"window of {n_dec} rows > max_rows {self.max_rows}")
-        cut = max(0, len(prefill) - room)
-        head, tail = prefill[:cut], prefill[cut:]
+        pre = np.concatenate(prefill) if prefill else np.empty((0, 6), dtype=np.int32)
+        cut = max(0, len(pre) - room)
+        head, tail = pre[:cut], pre[cut:]
         self._pre_passes = []
         for i in range(0, len(head), self.max_rows):
-            chunk = head[i:i + self.max_rows]
-            self._pre_passes.append(chunk + [_PAD] * (bucket(len(chunk)) - len(chunk)))
-        rows.extend(tail)
-        self._tail_ctx = sum(r[2] + 1 for r in tail)
-        rows.extend([_PAD] * (bucket(len(rows)) - len(rows)))
+            self._pre_passes.append(_pad_rows(head[i:i + self.max_rows]))
+        self._tail_ctx = int((tail[:, 2] + 1).sum()) if len(tail) else 0
+        rows = _pad_rows(np.concatenate([win, tail])) if len(tail) else win
         if len(rows) > self.max_rows:
-            rows = rows[:self.max_rows]       # padding only; real rows always fit
-        arr = (_lib.Row * len(rows))(*[_lib.Row(*r) for r in rows])
-        return arr, len(rows), n_dec
+            rows = np.ascontiguousarray(rows[:self.max_rows])   # padding only; real rows always fit
+        return rows, len(rows), n_dec
 
-    def run_iteration(self, stream) -> float | None:
+    def _prompt_np(self, rid):
+        a = self._prompt_cache.get(rid)
+        if a is None:
+            a = self._prompt_cache[rid] = np.asarray(self.prompts[rid], dtype=np.int32)
+        return a
+
+    def run_iteration(self, stream) -> None:
+        """Launch one fused iteration (stream-ordered, non-blocking).  Under
+        the device clock its duration is read later with iteration_ms(), so
+        the host's end-of-iteration bookkeeping overlaps the running step."""
         layout = stream.layout
         has_new = bool(self._new)
         # rows are re-uploaded when the window changes -- or when another stream's
@@ -419,30 +498,24 @@ class CudaExecutor:
                    or layout is not self._rows_layout)
         if changed:
             self._rows, self._n_rows, self._n_dec = self._build_rows(layout)
+            self._rows_p = _rows_ptr(self._rows)
             self._rows_version = layout.version
             self._rows_layout = layout
             self.h2d_bytes += self._n_rows * C.sizeof(_lib.Row)
-            self._orphan_ctx = sum(r.ctx for r in self._rows[:self._n_dec] if r.kind == _lib.ROW_ORPHAN)
         main_ctx = self._live_ctx + self._orphan_ctx + (self._tail_ctx if changed else 0)
         self._tail_ctx = 0
         cs = self.stream
-        dev_clock = stream.clock == "device"
-        self._set_timing(dev_clock)
-        timed = not dev_clock and self.time_steps
+        timed = stream.clock == "device" or self.time_steps
         if timed:
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
+            e0 = _cuda.Event(enable_timing=True)
+            e1 = _cuda.Event(enable_timing=True)
             e0.record(cs)
-        dev_ms = 0.0
         logits_ptr = self.logits_buf.data_ptr() if self.capture_logits else None
         if changed and self._pre_passes:
             for chunk in self._pre_passes:
-                arr = (_lib.Row * len(chunk))(*[_lib.Row(*r) for r in chunk])
-                _lib.check(self.lib.fl_step(self.handle, arr, len(chunk), 0, 1, None,
+                _lib.check(self.lib.fl_step(self.handle, _rows_ptr(chunk), len(chunk), 0, 1, None,
                                             C.c_void_p(cs.cuda_stream)))
-                self._account(sum(r[2] + 1 for r in chunk), len(chunk))
-                if dev_clock:
-                    dev_ms += self._last_ms()
+                self._account(int((chunk[:, 2] + 1).sum()), len(chunk))
                 self.rows_total += len(chunk)
                 self.prefill_rows_total += len(chunk)
                 self.h2d_bytes += len(chunk) * C.sizeof(_lib.Row)
@@ -456,26 +529,29 @@ class CudaExecutor:
             _lib.check(self.lib.fl_step_import(self.handle, C.c_void_p(self.lane.kv.data_ptr()), self.lane.Q,
                                                self.lane.S, flat, len(self._imports)))
             self.h2d_bytes += 12 * len(self._imports)
-        _lib.check(self.lib.fl_step(self.handle, self._rows, self._n_rows, self._n_dec, int(changed),
+        _lib.check(self.lib.fl_step(self.handle, self._rows_p, self._n_rows, self._n_dec, int(changed),
                                     logits_ptr, C.c_void_p(cs.cuda_stream)))
         if self._imports:
-            done = torch.cuda.Event()
+            done = _cuda.Event()
             done.record(cs)
             self.lane.release([q for q, _, _, _ in self._imports], done)
             self._imports = []
+        if timed:
+            e1.record(cs)
+            if stream.clock == "device":
+                self._step_ev = (e0, e1)
+            else:
+                self._events.append((e0, e1))
         self._account(main_ctx, self._n_rows)
         self.iterations += 1
         self.rows_total += self._n_rows
         self.prefill_rows_total += self._n_rows - self._n_dec
-        n_orph = sum(1 for s in range(layout.buffer_offset, layout.buffer_offset + layout.buffer_size)
-                     if layout.slots[s].occupant is None) if changed else self._last_orph
-        self._last_orph = n_orph
-        self.orphan_rows_total += n_orph
-        self.decode_rows_total += self._n_real_dec - n_orph
+        self.orphan_rows_total += self._n_orph
+        self.decode_rows_total += self._n_real_dec - self._n_orph
         if self.capture_logits:
-            rids = [r.rid for r in self._rows[:self._n_dec]]
-            kinds = [r.kind for r in self._rows[:self._n_dec]]
-            with torch.cuda.stream(cs):
+            rids = self._rows[:self._n_dec, 1].tolist()
+            kinds = self._rows[:self._n_dec, 4].tolist()
+            with _cuda.stream(cs):
                 lg = self.logits_buf[:self._n_dec].float().cpu()
             self.logits_log.append((stream.iteration_index, rids, kinds, lg))
         self._prev_had_new = has_new
@@ -483,13 +559,25 @@ class CudaExecutor:
         for info in self._live.values():
             info["gen"] += 1
         self._live_ctx += len(self._live)
-        if dev_clock:
-            dev_ms += self._last_ms()
-            return self.clock_reduce(dev_ms) if self.clock_reduce else dev_ms
-        if timed:
-            e1.record(cs)
-            self._events.append((e0, e1))
-        return None
+
+    def iteration_ms(self) -> float:
+        """Device time of the last iteration launched under the device clock
+        (waits for it; agreed across TP ranks when clock_reduce is set)."""
+        e0, e1 = self._step_ev
+        e1.synchronize()
+        ms = e0.elapsed_time(e1)
+        return self.clock_reduce(ms) if self.clock_reduce else ms
+
+    def shuffle_ms(self) -> float:
+        """Device time of the last shuffle boundary (K10, or planner + K10)."""
+        e0, e1 = self._shuffle_ev
+        e1.synchronize()
+        ms = e0.elapsed_time(e1)
+        if self._shuffle_pending is not None:
+            n, nbytes = self._shuffle_pending
+            self.shuffle_log.append((n, nbytes, ms))
+            self._shuffle_pending = None
+        return self.clock_reduce(ms) if self.clock_reduce else ms
 
     def _account(self, ctx_sum: int, n_rows: int):
         """Algorithmic HBM bytes of this fl_step's K4 launches: K and
@@ -504,17 +592,9 @@ class CudaExecutor:
             self.attn_bytes_profiled += b
         self._fl_calls += 1
 
-    def _set_timing(self, on: bool):
-        if on != self._lib_timing:
-            _lib.check(self.lib.fl_configure(self.handle, int(self.use_graphs), 8, int(on)))
-            self._lib_timing = on
-
-    def _last_ms(self) -> float:
-        ms = C.c_float()
-        _lib.check(self.lib.fl_last_duration_ms(self.handle, C.byref(ms)))
-        return float(ms.value)
-
-    def on_shuffle(self, plan) -> float | None:
+    def on_shuffle(self, plan, timed: bool = False) -> None:
+        """apply_shuffle on the device: the plan's moves -> K10 (launched, not
+        waited for; ``timed``: bracket it for shuffle_ms())."""
         moves = []
         nbytes = 0
         for m in plan.moves:
@@ -527,15 +607,35 @@ class CudaExecutor:
         flat = (C.c_int32 * (3 * len(moves)))(*[v for mv in moves for v in mv])
         self.h2d_bytes += 12 * len(moves)
         cs = self.stream
+        if timed:
+            e0, e1 = _cuda.Event(enable_timing=True), _cuda.Event(enable_timing=True)
+            e0.record(cs)
         _lib.check(self.lib.fl_shuffle(self.handle, flat, len(moves), C.c_void_p(cs.cuda_stream)))
+        if timed:
+            e1.record(cs)
+            self._shuffle_ev = (e0, e1)
+            self._shuffle_pending = (len(moves), nbytes)
         self.shuffles += 1
         for s in [m.src_slot for m in plan.moves]:
             self._orphans.pop(s, None)
-        if self._lib_timing:
-            ms = self._last_ms()
-            self.shuffle_log.append((len(moves), nbytes, ms))
-            return self.clock_reduce(ms) if self.clock_reduce else ms
-        return None
+
+    def eos_hits(self) -> list:
+        """Live requests whose token of the iteration just run is the EOS
+        token: one pinned read of the per-request next-token array after the
+        step (the stop now depends on device data, so this is the one D2H
+        per iteration EOS mode needs)."""
+        if self.eos_token is None or not self._live:
+            return []
+        if self._tok_host is None:
+            self._tok_host = torch.empty(self.R, dtype=torch.int32, pin_memory=self.device.type == "cuda")
+        cs = self.stream
+        with _cuda.stream(cs):
+            self._tok_host.copy_(self.req_tok, non_blocking=True)
+        cs.synchronize()
+        self.d2h_bytes_eos = getattr(self, "d2h_bytes_eos", 0) + 4 * self.R
+        t = self._tok_host
+        R, eos = self.R, self.eos_token
+        return [rid for rid in self._live if int(t[rid % R]) == eos]
 
     def launch_prefill(self, requests, now: float) -> int:
         """Start the prompts of ``requests`` (arrived by ``now``) on the side
@@ -569,20 +669,23 @@ class CudaExecutor:
             info = self._live.get(rid) if rid is not None else None
             ctx.append(info["P"] + info["gen"] - 1 if info else 0)
         if self._plan_host is None:
-            self._plan_host = torch.empty(3 + 2 * max(self.C, 1), dtype=torch.int32, pin_memory=True)
-            self._plan_bytes = torch.empty(1, dtype=torch.int64, pin_memory=True)
+            self._plan_host = torch.empty(3 + 2 * max(self.C, 1), dtype=torch.int32, pin_memory=self.device.type == "cuda")
+            self._plan_bytes = torch.empty(1, dtype=torch.int64, pin_memory=self.device.type == "cuda")
         a_occ = (C.c_int32 * max(n, 1))(*occ)
         a_size = (C.c_int64 * max(n, 1))(*size)
         a_ctx = (C.c_int32 * max(n, 1))(*ctx)
         cs = self.stream
+        e0, e1 = _cuda.Event(enable_timing=True), _cuda.Event(enable_timing=True)
+        e0.record(cs)
         _lib.check(self.lib.fl_shuffle_planned(self.handle, a_occ, a_size, a_ctx, n, lo,
                                                C.c_void_p(self._plan_host.data_ptr()),
                                                C.c_void_p(self._plan_bytes.data_ptr()), C.c_void_p(cs.cuda_stream)))
+        e1.record(cs)
+        self._shuffle_ev = (e0, e1)
         self.h2d_bytes += 16 * n
         self.d2h_bytes_plans = getattr(self, "d2h_bytes_plans", 0) + 4 * (3 + 2 * n) + 8
         self.device_plans += 1
-        ms = self._last_ms() if self._lib_timing else None      # synchronises on the step events
-        cs.synchronize()                                          # the plan read-back landed
+        e1.synchronize()                 # the plan read-back (ordered before e1) has landed
         out = self._plan_host
         offset, wlen, nm = int(out[0]), int(out[1]), int(out[2])
         moves = tuple(ShuffleMove(slots[int(out[3 + 2 * r])].occupant, int(out[3 + 2 * r]), int(out[4 + 2 * r]),
@@ -597,11 +700,10 @@ class CudaExecutor:
                 self._orphans.pop(m.src_slot, None)
             self.moved_kv_bytes += nbytes
             self.shuffles += 1
-            if ms is not None:
-                self.shuffle_log.append((len(moves), nbytes, ms))
-        if ms is not None and self.clock_reduce:
-            ms = self.clock_reduce(ms)
-        return plan, ms
+            self._shuffle_pending = (len(moves), nbytes)
+        else:
+            self._shuffle_pending = None
+        return plan
 
     def on_drain(self, stream):
         self.cs.synchronize()
@@ -622,7 +724,7 @@ class CudaExecutor:
             if owner != rid:
                 raise CapacityExceeded(f"history of request {rid} was overwritten by request {owner} "
                                        f"(state_slots {self.R}); read tokens() before the ring wraps")
-        with torch.cuda.stream(self.cs):
+        with _cuda.stream(self.cs):
             idx = torch.tensor([r % self.R for r in rids], device=self.device, dtype=torch.long)
             packed = torch.cat([self.req_ngen[idx].unsqueeze(1), self.tok_hist[idx]], dim=1).cpu()
         self.d2h_bytes = packed.numel() * 4
@@ -696,7 +798,7 @@ class _PrefillLane:
         if ex.tp_size > 1:
             raise InvalidParam("side-stream prefill is single-GPU (its collectives would need a second "
                                "communicator)")
-        self.ps = torch.cuda.Stream(device=dev)
+        self.ps = _cuda.Stream(device=dev)
         self.launched_rows = 0
         self.passes = 0
         self.reset()
@@ -723,8 +825,8 @@ class _PrefillLane:
             ev = self.free_ev.pop(q, None)
             if ev is not None:
                 self.ps.wait_event(ev)          # the previous occupant's import has read it
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
+        e0 = _cuda.Event(enable_timing=True)
+        e1 = _cuda.Event(enable_timing=True)
         e0.record(self.ps)
         for i in range(0, len(rows), self.max_rows):
             chunk = rows[i:i + self.max_rows]

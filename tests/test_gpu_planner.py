@@ -97,7 +97,7 @@ def test_device_planner_device_clock_bf16():
     """Device clock + tcgen05 path: the measured shuffle time covers planner
     + K10; all requests complete with their full token counts."""
     from harness import run_device, scenario_requests
-    reqs = scenario_requests(24, 2.0, 4, 40, 40, 16, seed=3)
+    reqs = scenario_requests(32, 0.1, 4, 40, 40, 16, seed=3)      # all live at once: holes
     trace, st, ex, _, _ = run_device("gptj-mini", reqs, dtype="bf16", shuffle=True, device_plan=True,
                                      clock="device", params=fl.CostParams(preprocess_ms=0.0),
                                      capture_logits=False)
@@ -105,3 +105,35 @@ def test_device_planner_device_clock_bf16():
     assert all(ms > 0 for _, _, ms in ex.shuffle_log)
     toks = ex.tokens()
     assert [len(toks[r.request_id]) for r in reqs] == [r.actual_output_length for r in reqs]
+
+
+@pytest.mark.parametrize("shuffle", [True, False])
+def test_eos_token_stop(shuffle):
+    """Data-dependent EOS: requests stop at their first greedy
+    EOS token instead of a pre-sampled length.  Bars: each stream is the
+    prefix (through the first EOS) of the same request's stream run to
+    max_output_length; and the device run's trace equals the reference
+    schedule of requests whose actual_output_length is the discovered stop
+    (record_token's eos_at, reference core.py:108-123) -- bit-exact."""
+    from collections import Counter
+    from harness import run_device, scenario_requests
+    from paper_2305_13484_b200.core import Request
+    reqs = scenario_requests(24, 10.0, 40, 40, 40, 16, seed=9)      # every request runs to 40
+    _, _, full, _, _ = run_device("tiny", reqs, dtype="f32", shuffle=shuffle, capture_logits=False)
+    ftok = full.tokens()
+    # the EOS token: the most frequent token in the first halves of the streams
+    eos = Counter(t for v in ftok.values() for t in v[:20]).most_common(1)[0][0]
+    trace, st, ex, _, _ = run_device("tiny", reqs, dtype="f32", shuffle=shuffle, capture_logits=False,
+                                     executor_opts=dict(eos_token=eos))
+    toks = ex.tokens()
+    stops = {}
+    for r in reqs:
+        f = ftok[r.request_id]
+        k = f.index(eos) + 1 if eos in f else len(f)
+        stops[r.request_id] = k
+        assert toks[r.request_id] == f[:k], r.request_id
+    assert any(k < 40 for k in stops.values())
+    ref = [Request(r.request_id, r.batch_size, r.input_len, r.max_output_length, stops[r.request_id],
+                   r.arrival_time) for r in reqs]
+    expect = fl.run_fusion(ref, fl.CostParams(), shuffle_enabled=shuffle)
+    assert trace.format_lines() == expect.format_lines()

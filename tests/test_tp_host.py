@@ -151,44 +151,38 @@ def test_tp_merged_out_projection_matches_unsharded_oracle(name, world):
 
 
 # ---------------------------------------------------------------- gloo, world 2
-class _FakeExecutor:
-    """Reports a rank-dependent 'device' time; the schedule must not care."""
-
-    def __init__(self, rank, reduce):
-        self.rank, self.clock_reduce = rank, reduce
-
-    def on_fuse(self, rid, slot, request):
-        pass
-
-    def on_evict(self, rid, slot):
-        pass
-
-    def run_iteration(self, stream):
-        ms = 1.0 + 0.25 * self.rank + 0.01 * (stream.iteration_index % 7)
-        return self.clock_reduce(ms)
-
-    def on_shuffle(self, plan):
-        return self.clock_reduce(0.1 * (1 + self.rank))
-
-    def on_drain(self, stream):
-        pass
-
-
 def _worker(rank, world, port, out):
+    """One TP rank driving the REAL executor host path (CudaExecutor on a
+    stub library, tests/stub_device.py): weight sharding, comm-id broadcast
+    and fl_comm_init, per-step row tables, shuffles, and the device clock
+    agreed across ranks by max_reduce_clock -- with rank-dependent step
+    times, the replicated schedules must stay identical."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
+        from stub_device import stub_device
+        from paper_2305_13484_b200.executor import CudaExecutor
+        from paper_2305_13484_b200.models import get_spec
         from paper_2305_13484_b200.tp import make_comm_id, max_reduce_clock
         cid = make_comm_id(rank, device=torch.device("cpu"), id_fn=lambda: bytes(range(128)))
-        reduce = max_reduce_clock(device=torch.device("cpu"))
         sc = fl.Scenario("tp", fl.Discipline.FUSION, 24, fl.PoissonArrival(3.0),
-                         fl.UniformLength(2, 20), 20)
+                         fl.UniformLength(2, 20), 20, input_len=8)
         reqs = fl.build_requests(sc, 7)
-        st = fl.FusionStream(reqs, fl.CostParams(preprocess_ms=0.0), fl.TPConfig(world),
-                             executor=_FakeExecutor(rank, reduce), clock="device")
-        fl.drive(st)
+        spec = get_spec("gptj-mini")
+        prompts = fl.synthetic_prompts(reqs, spec.vocab, 7)
+        with stub_device(rank) as rec:
+            ex = CudaExecutor(spec, prompts, dtype="bf16", pool_slots=24, input_len=8, max_new_tokens=20,
+                              state_slots=64, tp_rank=rank, tp_size=world, comm_id=cid, device="cpu")
+            ex.clock_reduce = max_reduce_clock(device=torch.device("cpu"))
+            st = fl.FusionStream(reqs, fl.CostParams(preprocess_ms=0.0), fl.TPConfig(world),
+                                 executor=ex, clock="device")
+            fl.drive(st)
+            hl = (ex.mdesc.tp_rank, ex.mdesc.tp_size, int(ex.kv.shape[3]))
         digest = hashlib.sha256("\n".join(fl.Trace("f", st.events).format_lines()).encode()).hexdigest()
-        out.put((rank, cid, digest, st.iteration_index))
+        steps = hashlib.sha256(repr(rec.steps).encode()).hexdigest()
+        out.put((rank, rec.comm, digest, st.iteration_index, steps, len(rec.shuffles), ex.tp_layout, hl))
     finally:
         dist.destroy_process_group()
 
@@ -200,10 +194,17 @@ def test_gloo_world2_comm_id_and_clock_agreement():
     procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    res = sorted(q.get(timeout=120) for _ in procs)
+    res = sorted(q.get(timeout=180) for _ in procs)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    (r0, id0, d0, n0), (r1, id1, d1, n1) = res
-    assert id0 == id1 == bytes(range(128))
+    (r0, c0, d0, n0, s0, sh0, lay0, hl0), (r1, c1, d1, n1, s1, sh1, lay1, hl1) = res
+    # the NCCL unique id reached both ranks, each initialised its own rank of 2
+    assert c0 == (bytes(range(128)), 0, 2) and c1 == (bytes(range(128)), 1, 2)
+    # replicated schedule: identical traces, row tables and shuffles per step
     assert d0 == d1 and n0 == n1 > 0
+    assert s0 == s1 and sh0 == sh1 > 0
+    # under TP the north star's layout: an all-reduce after attn-out AND FFN-down
+    assert lay0 == lay1 == "two all-reduces per layer (after attn-out and after FFN-down)"
+    # each rank holds its own half of the heads in its KV pool
+    assert hl0 == (0, 2, 1) and hl1 == (1, 2, 1)

@@ -70,7 +70,7 @@ int main() {
   cudaMalloc(&d, 8 * 148);
   uint8_t* g; cudaMalloc(&g, (size_t)4096 * 16384);
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
-  for (int N : {64, 128, 176, 256}) {
+  for (int N : {16, 32, 64, 128, 256}) {
     for (int grid : {1, 148}) {
      for (int tma_on : {0, 2}) {
       probe<<<grid, 128, 210 * 1024>>>(4096, N, d, g, tma_on);

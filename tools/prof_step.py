@@ -20,6 +20,7 @@ ap.add_argument("--rows", type=int, default=48)
 ap.add_argument("--iters", type=int, default=200)
 ap.add_argument("--profile", action="store_true")
 ap.add_argument("--pre", type=int, default=5, help="decode iterations before the measured loop (context growth)")
+ap.add_argument("--dump", default=None, help="with --profile: write per-class algorithmic bytes/launch JSON here")
 a = ap.parse_args()
 cfg = bench.CONFIGS[a.config]
 spec = get_spec(cfg["spec"])
@@ -49,5 +50,16 @@ t2 = time.perf_counter()
 print(f"rows={a.rows} host launch {1e6*(t1-t0)/a.iters:.1f} us/iter, wall {1e6*(t2-t0)/a.iters:.1f} us/iter, "
       f"device {1e3*e0.elapsed_time(e1)/a.iters:.1f} us/iter")
 if a.profile:
-    for k, v in ex.profile_read().items():
-        print(k, f"{1e3*v['ms']/a.iters:.1f} us/iter", v["records"] // a.iters, "records/iter")
+    pr = ex.profile_read()
+    for k, v in pr.items():
+        print(k, f"{1e3*v['ms']/a.iters:.1f} us/iter", v["records"], "records")
+    if a.dump:
+        import json
+        att_b = ex.attn_bytes_profiled
+        out = {"rows": a.rows, "config": a.config, "pre": a.pre}
+        for k, v in pr.items():
+            if v["records"]:
+                b = att_b if k == "attention" else v["bytes"]
+                out[k] = {"algorithmic_bytes_per_launch": b / v["records"], "records": v["records"],
+                          "us_per_launch": 1e3 * v["ms"] / v["records"]}
+        json.dump(out, open(a.dump, "w"), indent=1)
