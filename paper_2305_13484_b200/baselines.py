@@ -154,10 +154,17 @@ def run_dynamic_batching(requests, cfg: BatchWindowConfig, params: CostParams,
 # does not depend on how requests are batched).
 
 def run_concurrent_instances(requests, params: CostParams, tp: TPConfig | None = None,
-                             record_tokens: bool = True, *, executor=None) -> Trace:
+                             record_tokens: bool = True, *, executor=None, clock: str = "cost",
+                             max_instances: int = 64) -> Trace:
+    if clock not in ("cost", "device"):
+        raise InvalidParam(f"clock must be 'cost' or 'device', got {clock!r}")
+    if clock == "device" and executor is None:
+        raise InvalidParam("clock='device' needs an executor")
     tp = tp or TPConfig()
     from .engine import check_tp
-    check_tp(tp, executor, "cost")
+    check_tp(tp, executor, clock)
+    if clock == "device":
+        return _instances_on_device(requests, params, record_tokens, executor, max_instances)
     ordered = sorted(requests, key=lambda r: (r.arrival_time, r.request_id))
     ev = []
     for r in ordered:
@@ -252,3 +259,91 @@ def _replay_instances(executor, ordered, token_log) -> None:
             free.append(slot)
             del streams[rid]
     executor.on_drain(None)
+
+
+def _instances_on_device(requests, params: CostParams, record_tokens: bool, executor,
+                         max_instances: int) -> Trace:
+    """Concurrent instances under the DEVICE clock: instead of
+    the reference's contention model (baselines.py:130-229, cost.py:112-116)
+    the instances really run side by side -- each live request is a batch-1
+    decoder on its own stream and library handle (executor.instance_pool) --
+    and time is the device's: every token is stamped by its step's end event
+    (one device timeline for all streams), an instance starts at the first
+    moment it is ready and an instance slot is free, and an idle device jumps
+    to the next ready time (engine.py:200-201).  ``executor.instance_stats``
+    keeps (live instances, step ms) of every step, the measured contention."""
+    import time as _time
+
+    ordered = sorted(requests, key=lambda r: (r.arrival_time, r.request_id))
+    ev = []
+    for r in ordered:
+        ev.append(TraceEvent(r.arrival_time, EventKind.ARRIVED, r.request_id, None))
+        ev.append(TraceEvent(r.arrival_time, EventKind.PREPROCESS_START, r.request_id, None))
+        ev.append(TraceEvent(r.arrival_time + params.preprocess_ms, EventKind.PREPROCESS_DONE,
+                             r.request_id, None))
+    trace = Trace("concurrent", ev)
+    if not ordered:
+        return trace
+    torch = __import__("torch")
+    from . import executor as exmod
+    cu = exmod._cuda
+    pool = executor.instance_pool(min(max_instances, len(ordered)))
+    ready = sorted(((r.arrival_time + params.preprocess_ms, r.request_id, r) for r in ordered),
+                   key=lambda x: (x[0], x[1]))
+    nxt = 0
+    free_slots = list(range(executor.C))
+    live = {}                      # instance index -> [rid, slot, tokens done, last time, e0, e1, request]
+    stats = []
+    e_start = cu.Event(enable_timing=True)
+    e_start.record(pool.streams[0])
+    cu.synchronize()
+    t0 = _time.perf_counter()
+    offset = 0.0                   # virtual - device time (idle jumps)
+
+    def now_ms():
+        return (_time.perf_counter() - t0) * 1e3 + offset
+
+    def start(i, rid, req, at):
+        slot = free_slots.pop(0)
+        executor.on_fuse(rid, slot, req)
+        executor._new.clear()      # instance steps carry their own prompt rows
+        ev.append(TraceEvent(at, EventKind.FUSED, rid, None))
+        e0, e1 = pool.step(i, rid, slot, first=True)
+        live[i] = [rid, slot, 0, at, e0, e1, req, len(live) + 1]
+
+    while live or nxt < len(ready):
+        if not live and nxt < len(ready) and ready[nxt][0] > now_ms():
+            offset += ready[nxt][0] - now_ms()           # idle device: jump to the next ready time
+        t = now_ms()
+        while nxt < len(ready) and ready[nxt][0] <= t and pool.free:
+            at, rid, req = ready[nxt]
+            nxt += 1
+            start(pool.free.pop(0), rid, req, max(at, t))
+        for i in list(live):
+            x = live[i]
+            if not x[5].query():
+                continue
+            x[5].synchronize()
+            tj = e_start.elapsed_time(x[5]) + offset
+            stats.append((x[7], x[4].elapsed_time(x[5])))
+            x[2] += 1
+            rid, req = x[0], x[6]
+            tj = max(tj, x[3])
+            if record_tokens:
+                ev.append(TraceEvent(tj, EventKind.TOKEN_GENERATED, rid, x[2]))
+                ev.append(TraceEvent(tj, EventKind.ITERATION_COMPLETED, rid, tj - x[3]))
+            x[3] = tj
+            if x[2] == req.actual_output_length:
+                ev.append(TraceEvent(tj, EventKind.EVICTED, rid, None))
+                executor.on_evict(rid, x[1])
+                executor._live_ctx = 0
+                free_slots.append(x[1])
+                pool.free.append(i)
+                del live[i]
+            else:
+                x[4], x[5] = pool.step(i, rid, x[1], first=False)
+                x[7] = len(live)
+    cu.synchronize()
+    executor.instance_stats = stats
+    trace.sort()
+    return trace

@@ -54,7 +54,8 @@ constexpr int SK_STG_LD = 36;              // transpose row stride (floats): con
 
 thread_local std::string g_sk_err;
 // diagnostic overrides (fl_gemm_tune; -1 = the built-in choice): 1 max pairs,
-// 2 ring stages, 3 K sub-chunks per unit, 4 min units per stream-K range
+// 2 ring stages, 3 K sub-chunks per unit, 4 min units per stream-K range,
+// 5 tokens per token tile (span cap, <= 512)
 int g_tune[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
 unsigned long long* g_sk_dbg = nullptr;
 
@@ -390,7 +391,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         } else {
           const int t = u / kch;
           cur_kk = u - t * kch;
-          const int tm = t / P.ntn, tn = t - tm * P.ntn;
+          const int tn = t / P.ntm, tm = t - tn * P.ntm;
           cur_m0 = tm * P.span;
           cur_n0 = tn * 2 * SK_BM + xi * SK_BM;
         }
@@ -441,7 +442,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       // it is a whole tile (the ring is idle once its accumulator is full, so
       // the transpose buffers live there)
       const int seg = nseg - 1, t = last.t, klo = last.klo, khi = last.khi;
-      const int tm = t / P.ntn, tn = t - tm * P.ntn;
+      const int tn = t / P.ntm, tm = t - tn * P.ntm;
       const int m0 = tm * P.span;
       const int mcount = min(P.slice, P.M - m0);
       const int nbase = tn * 2 * SK_BM + xi * SK_BM;
@@ -539,7 +540,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       // fix-up is spread over the S pairs instead of serialised in one owner.
       const int S = P.csplit;
       const int t = R.lo[0] / kch, piece = pair - t * S;
-      const int tm = t / P.ntn, tn = t - tm * P.ntn;
+      const int tn = t / P.ntm, tm = t - tn * P.ntm;
       const int m0 = tm * P.span;
       const int mcount = min(P.slice, P.M - m0);
       const int nbase = tn * 2 * SK_BM + xi * SK_BM;
@@ -665,7 +666,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       const int t = g.t, klo = g.klo, khi = g.khi;
       const int b = P.nbuf == 2 ? (seg & 1) : 0;
       const uint32_t use = P.nbuf == 2 ? (seg >> 1) : seg;
-      const int tm = t / P.ntn, tn = t - tm * P.ntn;
+      const int tn = t / P.ntm, tm = t - tn * P.ntm;
       const int m0 = tm * P.span;
       const int mcount = min(P.slice, P.M - m0);
       const int nbase = tn * 2 * SK_BM + xi * SK_BM;
@@ -1030,7 +1031,12 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   P.ntn = (a.N + 2 * SK_BM - 1) / (2 * SK_BM);
   // token tiling: the whole window (<= 512 tokens) in one pair, as 1-2 UMMA
   // N sub-tiles, so every weight byte is read once
-  const int ntm = (a.M + SK_MAX_SPAN - 1) / SK_MAX_SPAN;
+  // windows wider than span_cap tokens run as several token tiles, each with
+  // double-buffered accumulators; tiles are numbered weight-tile-major
+  // (t = tn * ntm + tm), so the token tiles of one weight tile are adjacent
+  // units and their second weight read hits L2
+  const int span_cap = g_tune[5] > 0 ? g_tune[5] : 256;
+  const int ntm = (a.M + span_cap - 1) / span_cap;
   const int per = (a.M + ntm - 1) / ntm;                   // tokens per token tile
   P.mt = per <= 256 ? 1 : 2;
   P.bn = (((per + P.mt - 1) / P.mt) + 15) / 16 * 16;

@@ -364,7 +364,18 @@ class CudaExecutor:
     def launches(self) -> int:
         return int(self.lib.fl_kernel_launches(self.handle))
 
+    def instance_pool(self, k: int) -> "InstancePool":
+        """K batch-1 instances on K streams (concurrent-instances baseline)."""
+        if getattr(self, "_ipool", None) is None or self._ipool.k < k:
+            if getattr(self, "_ipool", None) is not None:
+                self._ipool.close()
+            self._ipool = InstancePool(self, k)
+        return self._ipool
+
     def close(self):
+        if getattr(self, "_ipool", None) is not None:
+            self._ipool.close()
+            self._ipool = None
         if getattr(self, "lane", None) is not None:
             self.lane.close()
         if getattr(self, "handle", None):
@@ -750,6 +761,33 @@ class CudaExecutor:
         return out
 
 
+def _side_handle(ex: "CudaExecutor", kv, state, C_slots: int, S: int, max_rows: int, R: int, max_new: int):
+    """A second library handle over ex's weights (own workspace, own pool
+    descriptor) whose launches may run beside other handles' on other
+    streams (fl_set_side_stream: GEMMs without cross-CTA waits).  Returns
+    (handle, workspace tensor, pool descriptor)."""
+    if ex.tp_size > 1:
+        raise InvalidParam("side handles are single-GPU (their collectives would need their own communicator)")
+    lib = ex.lib
+    pdesc = _lib.PoolDesc(C_slots, S, max_rows, R, max_new, ex.pdesc.use_tensor_cores, kv.data_ptr(),
+                          *[t.data_ptr() for t in state], None, 0)
+    nbytes = lib.fl_workspace_bytes(C.byref(ex.mdesc), C.byref(pdesc))
+    if nbytes == 0:
+        _lib.check(-1)
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=ex.device)
+    pdesc.workspace = ws.data_ptr()
+    pdesc.workspace_bytes = nbytes
+    h = C.c_void_p()
+    _lib.check(lib.fl_create(C.byref(ex.mdesc), C.byref(pdesc), C.byref(h)))
+    _lib.check(lib.fl_set_side_stream(h, 1))
+    if ex.merged:
+        _lib.check(lib.fl_set_merged_out(h, ex._wcat, ex._bcat))
+    if ex.merged_in:
+        _lib.check(lib.fl_set_merged_in(h, ex._win, ex._bin, int(ex.merged_in_max_rows)))
+    _lib.check(lib.fl_configure(h, int(ex.use_graphs), 8, 0))
+    return h, ws, pdesc
+
+
 class _PrefillLane:
     """Overlapped preprocessing: the paper's T_pp threads
      that prepare a request's context while the fused stream
@@ -778,26 +816,7 @@ class _PrefillLane:
         i32 = dict(dtype=torch.int32, device=dev)
         self._state = [torch.zeros(1, **i32) for _ in range(3)] + [torch.zeros((1, 1), **i32)]
         self.max_rows = bucket(min(self.Q * (self.S - 1), 512))
-        self.pdesc = _lib.PoolDesc(self.Q, self.S, self.max_rows, 1, 1, ex.pdesc.use_tensor_cores,
-                                   self.kv.data_ptr(), *[t.data_ptr() for t in self._state], None, 0)
-        nbytes = self.lib.fl_workspace_bytes(C.byref(ex.mdesc), C.byref(self.pdesc))
-        if nbytes == 0:
-            _lib.check(-1)
-        self.ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
-        self.pdesc.workspace = self.ws.data_ptr()
-        self.pdesc.workspace_bytes = nbytes
-        h = C.c_void_p()
-        _lib.check(self.lib.fl_create(C.byref(ex.mdesc), C.byref(self.pdesc), C.byref(h)))
-        self.handle = h
-        _lib.check(self.lib.fl_set_side_stream(h, 1))
-        if ex.merged:
-            _lib.check(self.lib.fl_set_merged_out(h, ex._wcat, ex._bcat))
-        if ex.merged_in:
-            _lib.check(self.lib.fl_set_merged_in(h, ex._win, ex._bin, int(ex.merged_in_max_rows)))
-        _lib.check(self.lib.fl_configure(h, int(ex.use_graphs), 8, 0))
-        if ex.tp_size > 1:
-            raise InvalidParam("side-stream prefill is single-GPU (its collectives would need a second "
-                               "communicator)")
+        self.handle, self.ws, self.pdesc = _side_handle(ex, self.kv, self._state, self.Q, self.S, self.max_rows, 1, 1)
         self.ps = _cuda.Stream(device=dev)
         self.launched_rows = 0
         self.passes = 0
@@ -871,3 +890,71 @@ class _PrefillLane:
         if getattr(self, "handle", None):
             self.lib.fl_destroy(self.handle)
             self.handle = None
+
+
+class InstancePool:
+    """Concurrent model instances on the device: the
+    reference's one-instance-per-request discipline (baselines.py:130-229)
+    whose contention it MODELS with contention_gamma (cost.py:112-116).
+    Here every live instance is a batch-1 decoder with its own library
+    handle (own workspace, no cross-CTA waits) on its own CUDA stream, over
+    the shared weights and KV pool (its own slot, its own state row), so K
+    live instances really share the GPU and the contention is measured."""
+
+    def __init__(self, ex: CudaExecutor, k: int):
+        self.ex = ex
+        self.k = max(1, int(k))
+        self.S_rows = bucket(max(len(p) for p in ex.prompts.values()) if ex.prompts else 8)
+        state = [ex.req_tok, ex.req_pos, ex.req_ngen, ex.tok_hist]
+        self.handles, self.ws, self.streams = [], [], []
+        for _ in range(self.k):
+            h, ws, _ = _side_handle(ex, ex.kv, state, ex.C, ex.S, max(8, self.S_rows), ex.R, ex.max_new)
+            self.handles.append(h)
+            self.ws.append(ws)
+            self.streams.append(_cuda.Stream(device=ex.device))
+        self.free = list(range(self.k))
+
+    def step(self, i: int, rid: int, slot: int, first: bool):
+        """Launch one batch-1 decode step of request rid on instance i (the
+        first also runs the prompt); returns the (start, end) events."""
+        ex = self.ex
+        pr = ex._prompt_np(rid)
+        P = len(pr)
+        phys = slot % ex.C
+        if first:
+            rows = np.empty((P, 6), dtype=np.int32)
+            rows[0] = (phys, rid, P - 1, pr[P - 1], _lib.ROW_DECODE, 0)
+            if P > 1:
+                rows[1:, 0] = phys
+                rows[1:, 1] = rid
+                rows[1:, 2] = np.arange(P - 1)
+                rows[1:, 3] = pr[:P - 1]
+                rows[1:, 4] = _lib.ROW_PREFILL
+                rows[1:, 5] = 0
+            n_dec = 1
+            dec = np.empty((8, 6), dtype=np.int32)
+            dec[:] = _PAD
+            dec[0] = rows[0]
+            rows = _pad_rows(np.concatenate([dec, rows[1:]])) if P > 1 else dec
+            n_dec = 8
+        else:
+            rows = np.empty((8, 6), dtype=np.int32)
+            rows[:] = _PAD
+            rows[0] = (phys, rid, -1, -1, _lib.ROW_DECODE, 0)
+            n_dec = 8
+        st = self.streams[i]
+        e0, e1 = _cuda.Event(enable_timing=True), _cuda.Event(enable_timing=True)
+        e0.record(st)
+        _lib.check(ex.lib.fl_step(self.handles[i], _rows_ptr(rows), len(rows), n_dec, 1, None,
+                                  C.c_void_p(st.cuda_stream)))
+        e1.record(st)
+        ex.h2d_bytes += len(rows) * C.sizeof(_lib.Row)
+        ex.rows_total += len(rows)
+        ex.iterations += 1
+        return e0, e1
+
+    def close(self):
+        for h in self.handles:
+            if h:
+                self.ex.lib.fl_destroy(h)
+        self.handles = []
