@@ -57,6 +57,7 @@ thread_local std::string g_sk_err;
 // 2 ring stages, 3 K sub-chunks per unit, 4 min units per stream-K range,
 // 5 tokens per token tile (span cap, <= 512)
 int g_tune[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
+int g_l2_ahead = -1;                      // fl_gemm_tune key 8
 unsigned long long* g_sk_dbg = nullptr;
 
 FL_DEV uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -208,6 +209,9 @@ struct SkParams {
   int helpers;      // warps 6-9 help drain the last whole tile
   int nsplit, ogap; // dual GEMM (GemmArgs::nsplit): rows >= nsplit read x2, GELU, column + ogap
   unsigned long long* dbg;   // diagnostics: per CTA [prod wait, prod total, mma wait, mma total]
+  int dbg_skip_x;            // diagnostics (fl_gemm_tune 6): no activation loads
+  int dbg_skip_mma;          // diagnostics (fl_gemm_tune 7): no MMAs (pipeline + epilogue only)
+  int l2_ahead;              // units of weights prefetched into L2 behind the ring fill
 };
 
 // dual GEMM: output column and activation of weight row n (identity / on
@@ -402,6 +406,10 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         // row of the contiguous 128 x 64 chunk (tile n0/128, K chunk k/64)
         const int wcol = P.w_tiled ? 0 : k;
         const int wrow = P.w_tiled ? ((n0 >> 7) * P.kch64 + (k >> 6)) * SK_BM : n0;
+        if (P.dbg_skip_x && role >= 0) {        // diagnostic: weights only (results garbage)
+          if (leader) mbar_expect_tx(&full_bar[st], 0);
+          return;
+        }
         if (leader) mbar_expect_tx(&full_bar[st], my_tx);
         if (P.dbg && role < 0) issue_clk[st] = clock64();
         if (role < 0 && KPB > 1 && P.w_tiled)
@@ -418,9 +426,34 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
                         m0 + role * P.bn + xi * (P.bn / 2));
       };
       auto unit = [&](int i) { return i < n0u ? R.lo[0] + i : R.lo[1] + (i - n0u); };
+      // L2 prefetch of a unit's weights (no smem): a CTA that starts while its
+      // predecessor is still running can only fill its ring, then waits for
+      // the activations (griddepcontrol.wait); meanwhile the next units'
+      // weights are pulled into L2, so its first stages after the wait land
+      // at L2 latency instead of HBM latency
+      auto prefetch = [&](int u) {
+        const int t = u / kch, kk = u - t * kch;
+        const int tn = t / P.ntm;
+        const int n0 = tn * 2 * SK_BM + xi * SK_BM, k = kk * SK_BK * KPB;
+        if (KPB > 1 && P.w_tiled)
+          asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                           reinterpret_cast<uint64_t>(&tma_w)), "r"(0), "r"(((n0 >> 7) * P.kch64 + (k >> 6)) * SK_BM)
+                       : "memory");
+        else if (KPB > 1)
+          asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                           reinterpret_cast<uint64_t>(&tma_w)), "r"(0), "r"(n0), "r"(k / SK_BK)
+                       : "memory");
+        else
+          asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                           reinterpret_cast<uint64_t>(&tma_w)), "r"(P.w_tiled ? 0 : k),
+                       "r"(P.w_tiled ? ((n0 >> 7) * P.kch64 + (k >> 6)) * SK_BM : n0)
+                       : "memory");
+      };
       const int pre = min(nunits, stages);
       if (role >= 0) pdl_wait();            // activations are the predecessor's output
       for (int i = 0; i < pre; ++i) issue(unit(i), i);   // weights stream ahead of the wait
+      if (role == -1 && P.l2_ahead > 0)
+        for (int i = pre; i < min(nunits, pre + P.l2_ahead); ++i) prefetch(unit(i));
       int s = pre % stages;
       uint32_t ph = pre == stages ? 1u : 0u;
       unsigned long long waited = 0, t_start = clock64();
@@ -493,7 +526,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
           }
           tc_fence_after();
           const uint8_t* st = smem + s * STAGE;
-          for (int kc = 0; kc < KPB; ++kc) {
+          for (int kc = 0; kc < KPB && !P.dbg_skip_mma; ++kc) {
             const uint64_t ad = desc_sw128(st + kc * SK_A_BYTES);
             if (P.mt == 2) {
               // consecutive MMAs share the weight slab (A) across the two token sub-tiles
@@ -984,6 +1017,7 @@ size_t sk_workspace_bytes() {
 const char* sk_last_error() { return g_sk_err.c_str(); }
 void sk_tune(int key, int value) {
   if (key >= 1 && key < 8) g_tune[key] = value;
+  if (key == 8) g_l2_ahead = value;
 }
 void sk_set_debug(unsigned long long* p) { g_sk_dbg = p; }
 
@@ -1031,11 +1065,13 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   P.ntn = (a.N + 2 * SK_BM - 1) / (2 * SK_BM);
   // token tiling: the whole window (<= 512 tokens) in one pair, as 1-2 UMMA
   // N sub-tiles, so every weight byte is read once
-  // windows wider than span_cap tokens run as several token tiles, each with
-  // double-buffered accumulators; tiles are numbered weight-tile-major
-  // (t = tn * ntm + tm), so the token tiles of one weight tile are adjacent
-  // units and their second weight read hits L2
-  const int span_cap = g_tune[5] > 0 ? g_tune[5] : 256;
+  // windows wider than span_cap tokens run as several token tiles; tiles are
+  // numbered weight-tile-major (t = tn * ntm + tm), so the token tiles of one
+  // weight tile are adjacent units (their second weight read can hit L2).
+  // Measured (tools/step_gemm_bench.py, C3 shapes): a cap of 256 tokens with
+  // double-buffered accumulators is 1.2-1.3x SLOWER at 288-512 rows than the
+  // whole window (<= 512) as one token tile -- the default
+  const int span_cap = g_tune[5] > 0 ? g_tune[5] : SK_MAX_SPAN;
   const int ntm = (a.M + span_cap - 1) / span_cap;
   const int per = (a.M + ntm - 1) / ntm;                   // tokens per token tile
   P.mt = per <= 256 ? 1 : 2;
@@ -1165,6 +1201,9 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   P.slot_elems = SK_MAX_SPAN * SK_BM;
   P.flags = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + (size_t)SK_MAX_PAIRS * 2 * SK_MAX_SPAN * SK_BM * 4);
   P.dbg = g_sk_dbg;
+  P.dbg_skip_x = g_tune[6] == 1 ? 1 : 0;
+  P.dbg_skip_mma = g_tune[7] == 1 ? 1 : 0;
+  P.l2_ahead = g_l2_ahead >= 0 ? g_l2_ahead : 0;   // measured: 4..32 units slow every M (0.67 -> 0.57 at 144 rows)
   P.nsplit = a.nsplit;
   P.ogap = a.ogap;
   P.vec = (a.ldo % 4 == 0 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0) ? 1 : 0;
