@@ -12,7 +12,9 @@ import os
 
 from .errors import DeviceError, raise_for_status
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libflover_b200.so")
+# FL_LIB: an alternative build of the same library (A/B timing in tools/)
+LIB_PATH = os.environ.get("FL_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                    "libflover_b200.so")
 
 FL_FAMILY = {"gpt2": 0, "gptj": 1, "neox": 2}
 FL_DTYPE = {"f32": 0, "bf16": 1}

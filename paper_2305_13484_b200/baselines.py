@@ -325,7 +325,8 @@ def _instances_on_device(requests, params: CostParams, record_tokens: bool, exec
                 continue
             x[5].synchronize()
             tj = e_start.elapsed_time(x[5]) + offset
-            stats.append((x[7], x[4].elapsed_time(x[5])))
+            if x[2] > 0:                  # decode steps only (the first one also runs the prompt)
+                stats.append((x[7], x[4].elapsed_time(x[5])))
             x[2] += 1
             rid, req = x[0], x[6]
             tj = max(tj, x[3])

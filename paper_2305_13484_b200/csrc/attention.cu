@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
     const T* __restrict__ q, const fl_row* __restrict__ rows, const int32_t* __restrict__ row_ctx,
     int M, int Hl, const T* __restrict__ kv_layer, int S, T* __restrict__ out,
     float* __restrict__ ws_o, float* __restrict__ ws_ml, int max_splits, int keys_per_split,
-    int splits, const int32_t* __restrict__ order, int ldo, const AttnFuse F) {
+    int splits, const int32_t* __restrict__ order, int ldo) {
   using Cfg = AttnCfg<T, HD>;
   constexpr int VEC = Cfg::VEC, NV = Cfg::NV, G = Cfg::G, PER = Cfg::PER, KPW = Cfg::KPW;
   constexpr int CW = Cfg::CW, TK = Cfg::TK, STAGES = Cfg::STAGES, NP = CW;
@@ -125,10 +125,6 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
   __shared__ __align__(8) uint64_t empty[STAGES];
   __shared__ float s_m[NP], s_l[NP];
   __shared__ __align__(16) float s_acc[NP][HD];
-  // fused rotary + KV append (rows < F.n_fused): the rotated, pre-scaled q
-  // and the row's new k / v (the key at position ctx - 1, never streamed)
-  __shared__ __align__(16) float s_q[HD];
-  __shared__ __align__(16) T s_kv[2][HD];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -168,8 +164,7 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
         const int ctx = row_ctx[r];
         const int k0 = sp * keys_per_split;
         if (k0 >= ctx) continue;
-        const bool newkey = r < F.n_fused && rows[r].kind != FL_ROW_ORPHAN;
-        const int k1 = min(newkey ? ctx - 1 : ctx, k0 + keys_per_split);
+        const int k1 = min(ctx, k0 + keys_per_split);
         const size_t slot = rows[r].slot;
         const T* Kb = kv_layer + ((slot * 2 + 0) * Hl + h) * head_stride;
         const T* Vb = kv_layer + ((slot * 2 + 1) * Hl + h) * head_stride;
@@ -203,59 +198,10 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
     const int ctx = row_ctx[r];
     const int k0 = sp * keys_per_split;
     if (k0 >= ctx) continue;
-    const bool fused = r < F.n_fused;
-    const bool newkey = fused && rows[r].kind != FL_ROW_ORPHAN;
-    // the split holding key ctx - 1 also owns the row's new key (and its append)
-    const bool mine = newkey && (ctx - 1) / keys_per_split == sp;
-    const int k1 = min(newkey ? ctx - 1 : ctx, k0 + keys_per_split);
+    const int k1 = min(ctx, k0 + keys_per_split);
     const int nsplit = (ctx + keys_per_split - 1) / keys_per_split;
 
     float qv[PER][VEC], acc[PER][VEC];
-    if (fused) {
-      // rotary of q (and of the new k) at position ctx - 1, element-wise from
-      // the raw q|k|v row (GPT-J interleaved pairs, NeoX rotate-half), staged
-      // in smem; the append of k / v to this row's slot
-      const T* base = static_cast<const T*>(F.qkv) + static_cast<size_t>(r) * F.ldq + h * HD;
-      const float fpos = static_cast<float>(ctx - 1);
-      for (int e = threadIdx.x; e < HD; e += CW * 32) {
-        float qe = to_f(base[e]);
-        float ke = mine ? to_f(base[D + e]) : 0.f;
-        if (F.rot > 0 && e < F.rot) {
-          int j, partner;
-          float sign;
-          if (F.family == FL_FAMILY_GPTJ) {
-            j = e >> 1;
-            partner = e ^ 1;
-            sign = (e & 1) ? 1.f : -1.f;
-          } else {
-            const int half = F.rot >> 1;
-            j = e < half ? e : e - half;
-            partner = e < half ? e + half : e - half;
-            sign = e < half ? -1.f : 1.f;
-          }
-          float sn, cs;
-          rope_sincos(fpos, j, F.rot, &sn, &cs);
-          qe = qe * cs + sign * to_f(base[partner]) * sn;
-          if (mine) ke = ke * cs + sign * to_f(base[D + partner]) * sn;
-        }
-        s_q[e] = qe * scale;
-        if (mine) {
-          s_kv[0][e] = from_f<T>(ke);
-          s_kv[1][e] = base[2 * D + e];
-        }
-      }
-      asm volatile("bar.sync 1, %0;" ::"n"(CW * 32) : "memory");
-      if (mine) {
-        const size_t slot = rows[r].slot;
-        const size_t pos = static_cast<size_t>(ctx - 1);
-        T* Kd = const_cast<T*>(kv_layer) + ((slot * 2 + 0) * Hl + h) * head_stride + pos * HD;
-        T* Vd = const_cast<T*>(kv_layer) + ((slot * 2 + 1) * Hl + h) * head_stride + pos * HD;
-        for (int v = threadIdx.x; v < 2 * NV; v += CW * 32) {
-          const uint4 w = *reinterpret_cast<const uint4*>(&s_kv[v / NV][(v % NV) * VEC]);
-          *reinterpret_cast<uint4*>((v < NV ? Kd : Vd) + (v % NV) * VEC) = w;
-        }
-      }
-    }
     const T* qr = q + static_cast<size_t>(r) * D + h * HD;
 #pragma unroll
     for (int p = 0; p < PER; ++p) {
@@ -263,49 +209,12 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
 #pragma unroll
       for (int j = 0; j < VEC; ++j) acc[p][j] = 0.f;
       if (vi < NV) {
-        if (fused) {
+        load16(qr + vi * VEC, qv[p]);
 #pragma unroll
-          for (int j = 0; j < VEC; ++j) qv[p][j] = s_q[vi * VEC + j];
-        } else {
-          load16(qr + vi * VEC, qv[p]);
-#pragma unroll
-          for (int j = 0; j < VEC; ++j) qv[p][j] *= scale;
-        }
+        for (int j = 0; j < VEC; ++j) qv[p][j] *= scale;
       }
     }
     float m = -INFINITY, l = 0.f;
-    if (mine && warp == 0) {
-      // the new key, taken by key group 0 of warp 0 before the streamed tiles
-      float dot = 0.f;
-      if (kw == 0) {
-#pragma unroll
-        for (int p = 0; p < PER; ++p) {
-          const int vi = g + p * G;
-          if (vi < NV) {
-            float kf[VEC];
-            widen16<T>(*reinterpret_cast<const uint4*>(&s_kv[0][vi * VEC]), kf);
-#pragma unroll
-            for (int j = 0; j < VEC; ++j) dot = fmaf(qv[p][j], kf[j], dot);
-          }
-        }
-      }
-#pragma unroll
-      for (int o = G / 2; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-      if (kw == 0) {
-        m = dot;
-        l = 1.f;
-#pragma unroll
-        for (int p = 0; p < PER; ++p) {
-          const int vi = g + p * G;
-          if (vi < NV) {
-            float vf[VEC];
-            widen16<T>(*reinterpret_cast<const uint4*>(&s_kv[1][vi * VEC]), vf);
-#pragma unroll
-            for (int j = 0; j < VEC; ++j) acc[p][j] = vf[j];
-          }
-        }
-      }
-    }
 
     for (int t0 = k0; t0 < k1; t0 += TK) {
       const int nk = min(TK, k1 - t0);
@@ -316,7 +225,10 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
       for (int kb = warp * KPW; kb < nk; kb += CW * KPW) {
         const int k = kb + kw;
         const bool valid = k < nk;
-        float dot = 0.f;
+        // four independent partial sums: the dot product is otherwise one
+        // dependent FMA chain of PER*VEC links per key (latency-bound at the
+        // ~2 consumer warps per scheduler the smem ring leaves room for)
+        float d4[4] = {0.f, 0.f, 0.f, 0.f};
         if (valid) {
 #pragma unroll
           for (int p = 0; p < PER; ++p) {
@@ -325,10 +237,11 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
               float kf[VEC];
               widen16<T>(*reinterpret_cast<const uint4*>(Ks + k * Cfg::ROW + vi * 16), kf);
 #pragma unroll
-              for (int j = 0; j < VEC; ++j) dot = fmaf(qv[p][j], kf[j], dot);
+              for (int j = 0; j < VEC; ++j) d4[j & 3] = fmaf(qv[p][j], kf[j], d4[j & 3]);
             }
           }
         }
+        float dot = (d4[0] + d4[1]) + (d4[2] + d4[3]);
 #pragma unroll
         for (int o = G / 2; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
         if (valid) {
@@ -437,7 +350,7 @@ __global__ void k_attn_combine(const int32_t* __restrict__ row_ctx, int Hl,
 template <typename T, int HD>
 static int attn_launch(const void* q, const fl_row* rows, const int32_t* row_ctx, int M, int Hl,
                        const void* kv_layer, int S, int kps, void* out, float* ws_o, float* ws_ml,
-                       const int32_t* order, int ldo, cudaStream_t s, const AttnFuse& F) {
+                       const int32_t* order, int ldo, cudaStream_t s) {
   using Cfg = AttnCfg<T, HD>;
   static int num_sms = 0;
   if (!num_sms) {
@@ -451,7 +364,7 @@ static int attn_launch(const void* q, const fl_row* rows, const int32_t* row_ctx
   const int items = M * Hl * splits;
   const int grid = items < 2 * num_sms ? items : 2 * num_sms;
   launch_k(k_attn_tma<T, HD>, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM, s, 1, (const T*)q, rows,
-           row_ctx, M, Hl, (const T*)kv_layer, S, (T*)out, ws_o, ws_ml, ms, kps, splits, order, ldo, F);
+           row_ctx, M, Hl, (const T*)kv_layer, S, (T*)out, ws_o, ws_ml, ms, kps, splits, order, ldo);
   if (splits > 1) {
     launch_k(k_attn_combine<T, HD>, dim3(Hl, M), dim3(HD < 128 ? HD : 128), 0, s, 1, row_ctx, Hl,
              ws_o, ws_ml, ms, kps, (T*)out, ldo);
@@ -495,17 +408,16 @@ void launch_row_order(const int32_t* row_ctx, int M, int32_t* order, cudaStream_
 
 int launch_attention(const void* q, const fl_row* rows, const int32_t* row_ctx, int M, int Hl,
                      int hd, const void* kv_layer, int C, int S, int kps, void* out, float* ws_o,
-                     float* ws_ml, int dtype, cudaStream_t s, const int32_t* order, int ldo,
-                     const AttnFuse& F) {
+                     float* ws_ml, int dtype, cudaStream_t s, const int32_t* order, int ldo) {
   if (ldo <= 0) ldo = Hl * hd;
   if (M <= 0) return 0;
 #define FL_ATT(HDV)                                                                          \
   case HDV:                                                                                  \
     return dtype == FL_DTYPE_BF16                                                            \
                ? attn_launch<bf16, HDV>(q, rows, row_ctx, M, Hl, kv_layer, S, kps, out, ws_o, \
-                                        ws_ml, order, ldo, s, F)                             \
+                                        ws_ml, order, ldo, s)                                \
                : attn_launch<float, HDV>(q, rows, row_ctx, M, Hl, kv_layer, S, kps, out,      \
-                                         ws_o, ws_ml, order, ldo, s, F);
+                                         ws_o, ws_ml, order, ldo, s);
   switch (hd) {
     FL_ATT(64)
     FL_ATT(96)

@@ -147,16 +147,4 @@ inline cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t s
   return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 
-// sin/cos of the rotary angle pos * 10000^(-2j/rot): the fp32 angle (as the
-// precise path forms it) reduced to [-pi, pi] with a two-constant Cody-Waite
-// step, then the SFU sincos -- |error| ~1e-6 against sincosf, which spends
-// hundreds of instructions per call on its general range reduction
-FL_DEV void rope_sincos(float pos, int j, int rot, float* sn, float* cs) {
-  const float x = pos * exp2f(-(2.f * j / rot) * 13.287712379549449f);   // log2(10000)
-  const float kq = rintf(x * 0.15915494309189535f);
-  float rr = fmaf(-kq, 6.28318548202514648f, x);       // 2pi, fp32 head
-  rr = fmaf(-kq, -1.7484556e-07f, rr);                  // 2pi - head
-  __sincosf(rr, sn, cs);
-}
-
 }  // namespace fl

@@ -526,32 +526,16 @@ int enqueue_step(fl_handle* h, int n_rows, int n_dec, bool want_logits, cudaStre
     } else {
       FL_GEMM(h->h, d, W[FL_W_QKV], W[FL_W_QKV_B], h->qkv, h->ldaf, n_rows, 3 * Dl, d, fl::EPI_STORE, s);
     }
-    // rotary on q/k + KV append at each row's (slot, pos).  bf16: fused into
-    // K4 for the window rows (their new key never round-trips through the
-    // pool before it is used); only PREFILL rows -- whose keys other rows of
-    // this step read -- go through the separate kernel first
-    const bool fuse = dt == FL_DTYPE_BF16 && hd % 8 == 0;
-    const int r0 = fuse ? n_dec : 0;
-    if (n_rows > r0) {
-      fl::launch_rope_append(static_cast<char*>(h->qkv) + (size_t)r0 * h->ldaf * es, h->rows + r0,
-                             h->row_pos + r0, n_rows - r0, Hl, hd, m.rotary_dim, m.family, kvl, p.pool_slots,
-                             p.max_seq, static_cast<char*>(h->q) + (size_t)r0 * Dl * es, dt, s, h->ldaf);
-      fl::g_launches += 1;
-    }
+    // rotary on q/k, q -> h->q, k/v appended to the pool at each row's (slot, pos)
+    fl::launch_rope_append(h->qkv, h->rows, h->row_pos, n_rows, Hl, hd, m.rotary_dim, m.family,
+                           kvl, p.pool_slots, p.max_seq, h->q, dt, s, h->ldaf);
+    fl::g_launches += 1;
     // K4
     {
       ProfScope ps(h, FL_PROF_ATTENTION, s);
-      fl::AttnFuse F;
-      if (fuse) {
-        F.qkv = h->qkv;
-        F.ldq = h->ldaf;
-        F.rot = m.family == FL_FAMILY_GPT2 ? 0 : m.rotary_dim;
-        F.family = m.family;
-        F.n_fused = n_dec;
-      }
       fl::g_launches += fl::launch_attention(h->q, h->rows, h->row_ctx, n_rows, Hl, hd, kvl,
                                              p.pool_slots, p.max_seq, att_keys, h->a, h->att_o,
-                                             h->att_ml, dt, s, ordered ? h->row_order : nullptr, h->ldaf, F);
+                                             h->att_ml, dt, s, ordered ? h->row_order : nullptr, h->ldaf);
     }
     fl::g_launches += 1;
     // K5 attn-out (+ all-reduce); merged into K7 for parallel-residual models

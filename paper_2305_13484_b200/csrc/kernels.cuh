@@ -68,20 +68,10 @@ int attn_max_splits(int S);
 // keys per split: one split per (row, head) when rows*heads fill the GPU.
 int attn_keys_per_split(int row_heads, int S);
 // returns the number of kernels launched (1 or 2)
-// Rotary + KV append fused into attention for rows [0, n_fused) (the live
-// window): their q is rotated from the raw q|k|v row, their new k / v is
-// appended to the slot by the split that owns key ctx - 1 and folded in from
-// registers (never streamed).  n_fused = 0: q comes rotated from `q` and every
-// key from the pool (launch_rope_append ran first).
-struct AttnFuse {
-  const void* qkv = nullptr;
-  int ldq = 0, rot = 0, family = 0, n_fused = 0;
-};
 int launch_attention(const void* q, const fl_row* rows, const int32_t* row_ctx, int M, int Hl,
                      int hd, const void* kv_layer, int C, int S, int keys_per_split, void* out,
                      float* ws_o, float* ws_ml, int dtype, cudaStream_t s,
-                     const int32_t* order = nullptr, int ldo = 0,
-                     const AttnFuse& F = AttnFuse());
+                     const int32_t* order = nullptr, int ldo = 0);
 // order[i] = row of rank i by descending context (attention's snake schedule)
 void launch_row_order(const int32_t* row_ctx, int M, int32_t* order, cudaStream_t s);
 

@@ -904,11 +904,12 @@ class InstancePool:
     def __init__(self, ex: CudaExecutor, k: int):
         self.ex = ex
         self.k = max(1, int(k))
-        self.S_rows = bucket(max(len(p) for p in ex.prompts.values()) if ex.prompts else 8)
+        # the first step of an instance: an 8-row decode window + its prompt rows
+        self.S_rows = bucket(8 + (max(len(p) for p in ex.prompts.values()) if ex.prompts else 8))
         state = [ex.req_tok, ex.req_pos, ex.req_ngen, ex.tok_hist]
         self.handles, self.ws, self.streams = [], [], []
         for _ in range(self.k):
-            h, ws, _ = _side_handle(ex, ex.kv, state, ex.C, ex.S, max(8, self.S_rows), ex.R, ex.max_new)
+            h, ws, _ = _side_handle(ex, ex.kv, state, ex.C, ex.S, self.S_rows, ex.R, ex.max_new)
             self.handles.append(h)
             self.ws.append(ws)
             self.streams.append(_cuda.Stream(device=ex.device))
