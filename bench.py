@@ -91,7 +91,7 @@ def cpu_cores() -> int:
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_power_cap,utilization.gpu")
     NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, index: int):
@@ -124,7 +124,7 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
+        sm, mx, reasons, util = [], None, set(), []
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 7:
@@ -134,12 +134,19 @@ class ClockSampler:
                 mx = float(parts[1])
             except ValueError:
                 continue
+            if len(parts) > 7:
+                try:
+                    util.append(float(parts[7]))
+                except ValueError:
+                    pass
             for name, val in zip(self.NAMES, parts[3:7]):
                 if val.lower() == "active":
                     reasons.add(name)
         under = [v for v in sm if v > 500] or sm
         return {"sm_mhz": statistics.median(under) if under else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                # nvidia-smi utilization.gpu: % of the sample period a kernel ran
+                "gpu_busy_pct": statistics.fmean(util) if util else None}
 
 
 # ----------------------------------------------------------------- workload

@@ -1163,7 +1163,7 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
     P.dpw = 1;
   } else if (tiles >= npairs) {
     P.dpw = tiles / npairs;
-  } else if (a.epi == EPI_ACC_F32 && a.K > 1024) {
+  } else if (a.epi == EPI_ACC_F32) {
     // residual GEMMs (attn-out / FFN-down, 16 tiles): pure stream-K over all
     // pairs, every piece of a split tile red.adds into the fp32 residual --
     // no fix-up, no waits, all 148 SMs stream equal weight bytes
