@@ -126,6 +126,7 @@ struct fl_handle {
   // CUDA graphs of the step, keyed by (n_rows, n_dec, logits, profiled)
   struct GraphEntry {
     cudaGraphExec_t exec = nullptr;
+    int64_t kernels = 0;     // kernel nodes of the captured step (counted per replay)
     std::vector<Rec> recs;   // event pairs baked into a profiled graph
     bool pending = false;    // recs hold an unread replay
   };
@@ -669,7 +670,10 @@ extern "C" int fl_step(fl_handle* h, const fl_row* rows, int n_rows, int n_dec, 
       h->sink = &entry.recs;
       h->capturing = true;
       FL_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      const int64_t k0 = fl::g_launches.load();
       int e = enqueue_step(h, n_rows, n_dec, want_logits, s);
+      entry.kernels = fl::g_launches.load() - k0;   // capture enqueues nothing: count replays
+      fl::g_launches -= entry.kernels;
       cudaGraph_t g = nullptr;
       cudaError_t ce = cudaStreamEndCapture(s, &g);
       h->capturing = false;
@@ -693,6 +697,7 @@ extern "C" int fl_step(fl_handle* h, const fl_row* rows, int n_rows, int n_dec, 
     if (h->time_steps) FL_CUDA(cudaEventRecord(h->t0, s));   // after any capture work
     run_import();
     FL_CUDA(cudaGraphLaunch(ge.exec, s));
+    fl::g_launches += ge.kernels;
     ge.pending = profiled;
   }
   if (h->time_steps) FL_CUDA(cudaEventRecord(h->t1, s));
