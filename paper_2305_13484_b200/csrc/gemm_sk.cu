@@ -211,6 +211,7 @@ struct SkParams {
   unsigned long long* dbg;   // diagnostics: per CTA [prod wait, prod total, mma wait, mma total]
   int dbg_skip_x;            // diagnostics (fl_gemm_tune 6): no activation loads
   int dbg_skip_mma;          // diagnostics (fl_gemm_tune 7): no MMAs (pipeline + epilogue only)
+  int dbg_skip_epi;          // diagnostics (fl_gemm_tune 8 = -2): no epilogue (TMEM drained unread)
   int l2_ahead;              // units of weights prefetched into L2 behind the ring fill
 };
 
@@ -470,7 +471,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       }
     }
     __syncwarp();
-    if (warp >= 6 && P.helpers && P.csplit == 1) {
+    if (warp >= 6 && P.helpers && P.csplit == 1 && !P.dbg_skip_epi) {
       // ---- helpers: the odd 32-token blocks of the pair's last segment when
       // it is a whole tile (the ring is idle once its accumulator is full, so
       // the transpose buffers live there)
@@ -713,6 +714,14 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       epi_bar();
       if (P.dbg) e_wait += clock64() - tw0;
       tc_fence_after();
+      if (P.dbg_skip_epi) {                     // diagnostic: no epilogue work at all
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(&tempty_bar[b], prank);
+        u += khi - klo;
+        ++seg;
+        continue;
+      }
 
       // segment mode: final epilogue (whole tile, or the k = 0 owner of a split
       // tile after folding in the later pieces) or publish (a later piece of a
@@ -1203,7 +1212,8 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   P.dbg = g_sk_dbg;
   P.dbg_skip_x = g_tune[6] == 1 ? 1 : 0;
   P.dbg_skip_mma = g_tune[7] == 1 ? 1 : 0;
-  P.l2_ahead = g_l2_ahead >= 0 ? g_l2_ahead : 0;   // measured: 4..32 units slow every M (0.67 -> 0.57 at 144 rows)
+  P.l2_ahead = g_l2_ahead >= 0 ? g_l2_ahead : 0;
+  P.dbg_skip_epi = g_l2_ahead == -2 ? 1 : 0;   // measured: 4..32 units slow every M (0.67 -> 0.57 at 144 rows)
   P.nsplit = a.nsplit;
   P.ogap = a.ogap;
   P.vec = (a.ldo % 4 == 0 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0) ? 1 : 0;
