@@ -126,6 +126,27 @@ FL_DEV void mma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t i
       "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
 }
+// Warp-uniform issue: the whole MMA warp runs the loop and one elected lane
+// issues.  Descriptors computed in uniform control flow stay in uniform
+// registers; issued from a lane-0 branch instead, every tcgen05.mma was
+// wrapped in an ELECT loop with five R2UR.BROADCASTs (~165 clk per MMA
+// against 82-94 clk back to back, tools/probes/mma2_probe.cu).
+FL_DEV void mma_pair_elect(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+FL_DEV void commit_pair_elect(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}"
+      ::"r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
 // arrive on `bar` in both CTAs of the pair (mask = 3 << even rank of the pair)
 FL_DEV void commit_pair(uint64_t* bar, uint16_t mask) {
   asm volatile(
@@ -500,7 +521,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && leader) {
+    if (leader) {                          // the whole warp; one elected lane issues
       const uint32_t idesc = idesc_bf16(2 * SK_BM, P.bn);
       int s = 0, seg = 0;
       uint32_t ph = 0;
@@ -534,8 +555,8 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
               const uint64_t bd0 = desc_sw128(st + AB + kc * XB), bd1 = desc_sw128(st + AB + (KPB + kc) * XB);
 #pragma unroll
               for (int kk = 0; kk < SK_BK / 16; ++kk) {
-                mma_pair(acc, ad + 2 * kk, bd0 + 2 * kk, idesc, (c > klo) | kc | kk);
-                mma_pair(acc + P.bn, ad + 2 * kk, bd1 + 2 * kk, idesc, (c > klo) | kc | kk);
+                mma_pair_elect(acc, ad + 2 * kk, bd0 + 2 * kk, idesc, (c > klo) | kc | kk);
+                mma_pair_elect(acc + P.bn, ad + 2 * kk, bd1 + 2 * kk, idesc, (c > klo) | kc | kk);
               }
               continue;
             }
@@ -543,17 +564,17 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
               const uint64_t bd = desc_sw128(st + AB + (j * KPB + kc) * XB);
 #pragma unroll
               for (int kk = 0; kk < SK_BK / 16; ++kk)
-                mma_pair(acc + j * P.bn, ad + 2 * kk, bd + 2 * kk, idesc, (c > klo) | kc | kk);
+                mma_pair_elect(acc + j * P.bn, ad + 2 * kk, bd + 2 * kk, idesc, (c > klo) | kc | kk);
             }
           }
-          commit_pair(&empty_bar[s], pmask);
+          commit_pair_elect(&empty_bar[s], pmask);
           if (++s == stages) { s = 0; ph ^= 1; }
         }
-        commit_pair(&tfull_bar[b], pmask);
+        commit_pair_elect(&tfull_bar[b], pmask);
         u += khi - klo;
         ++seg;
       }
-      if (P.dbg) {
+      if (P.dbg && lane == 0) {
         P.dbg[4 * blockIdx.x + 2] = waited;
         P.dbg[4 * blockIdx.x + 3] = clock64() - t_start;
         P.dbg[4 * (2048 + blockIdx.x) + 0] = twait;
