@@ -1,2 +1,5 @@
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
-for cn in 1 2 4; do FL_SK_VERBOSE=1 FL_SK_CN=$cn timeout 600 python tools/layer_gemm_bench.py 320 128 8 2>&1 | sort | uniq | sed "s/^/cn=$cn /"; done
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 200 python tools/step_gemm_bench.py 8 64 144 256 > gpurun_out/elect.log 2>&1
+ONLY=in GEMM_DBG=1 timeout 200 python tools/step_gemm_bench.py 8 144 >> gpurun_out/elect.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_merged.py -x -q > gpurun_out/elect_tests.log 2>&1
