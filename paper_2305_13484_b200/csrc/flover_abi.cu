@@ -16,6 +16,7 @@
 // (logit, index) max-reduce for the greedy token.
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>   // header-only; ranges cost nothing without a tool attached
 
 #include <atomic>
 #include <map>
@@ -34,6 +35,13 @@
 namespace {
 
 thread_local std::string g_err;
+
+// NVTX range over one C-ABI call (Nsight timelines: fl_step / fl_shuffle /
+// fl_shuffle_planned per fused iteration)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -616,6 +624,7 @@ void harvest(fl_handle* h, std::vector<fl_handle::Rec>& recs) {
 
 extern "C" int fl_step(fl_handle* h, const fl_row* rows, int n_rows, int n_dec, int rows_changed,
                        float* logits_out, void* stream) {
+  NvtxRange nvtx(n_dec ? "fl_step" : "fl_step(prefill)");
   if (!h) return fail(FL_EINVAL, "null handle");
   if (n_rows < 1 || n_dec < 0 || n_dec > n_rows) return fail(FL_EINVAL, "bad row counts");
   if (n_rows > h->p.max_rows) return fail(FL_ECAPACITY, "%d rows > max_rows %d", n_rows, h->p.max_rows);
@@ -709,6 +718,7 @@ extern "C" int fl_step(fl_handle* h, const fl_row* rows, int n_rows, int n_dec, 
 }
 
 extern "C" int fl_shuffle(fl_handle* h, const int32_t* moves, int n, void* stream) {
+  NvtxRange nvtx("fl_shuffle");
   if (!h) return fail(FL_EINVAL, "null handle");
   if (n <= 0) return FL_OK;
   if (n > h->p.pool_slots) return fail(FL_EINVAL, "%d moves > pool %d", n, h->p.pool_slots);
@@ -912,6 +922,7 @@ int launch_plan_shuffle(const int32_t* occ, const int64_t* size, int n, int lo, 
 
 extern "C" int fl_shuffle_planned(fl_handle* h, const int32_t* occ, const int64_t* size, const int32_t* ctx, int n,
                                   int lo, int32_t* plan_out, long long* bytes_out, void* stream) {
+  NvtxRange nvtx("fl_shuffle_planned");
   if (!h) return fail(FL_EINVAL, "null handle");
   if (n < 0 || n > h->p.pool_slots) return fail(FL_EINVAL, "window of %d slots > pool %d", n, h->p.pool_slots);
   if (n > 0 && (!occ || !size || !ctx)) return fail(FL_EINVAL, "null window array");

@@ -66,10 +66,13 @@ def bucket(n: int) -> int:
     the padding rows are ORPHAN rows over one stale position (discarded)."""
     if n <= 0:
         return 0
-    for limit, step in ((64, 8), (128, 16), (256, 32)):
+    # padding rows cost GEMM time roughly in proportion (the weight stream
+    # is shared, but MMA and epilogue work grow with the window): 16-row
+    # steps up to 256 rows, 32 beyond
+    for limit, step in ((64, 8), (256, 16)):
         if n <= limit:
             return -(-n // step) * step
-    return -(-n // 64) * 64
+    return -(-n // 32) * 32
 
 
 class CudaExecutor:
