@@ -139,6 +139,35 @@ FL_DEV void mma_pair_elect(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint
       "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
 }
+// One ring stage of a single token sub-tile with two 64-wide K chunks
+// (kpb = 2, mt = 1, the common case): 8 MMAs in ONE asm block, descriptors
+// stepped in PTX from three bases, so ptxas moves three values to uniform
+// registers per stage instead of five per MMA.  The 16-deep K step is +32 B
+// (+2 in the descriptor's 16-byte units), the second chunk of A is +16 KB.
+FL_DEV void mma_stage2_elect(uint32_t tmem_d, uint64_t ad0, uint64_t bd0, uint64_t bd1, uint32_t idesc,
+                             uint32_t acc_first) {
+  asm volatile(
+      "{\n\t.reg .pred e, p0, p1;\n\t.reg .b64 a, b;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p0, %5, 0;\n\t"
+      "setp.eq.b32 p1, %5, %5;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %4, p0;\n\t"
+      "add.s64 a, %1, 2;\n\tadd.s64 b, %2, 2;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %4, p1;\n\t"
+      "add.s64 a, %1, 4;\n\tadd.s64 b, %2, 4;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %4, p1;\n\t"
+      "add.s64 a, %1, 6;\n\tadd.s64 b, %2, 6;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %4, p1;\n\t"
+      "add.s64 a, %1, 1024;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, %3, %4, p1;\n\t"
+      "add.s64 a, %1, 1026;\n\tadd.s64 b, %3, 2;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %4, p1;\n\t"
+      "add.s64 a, %1, 1028;\n\tadd.s64 b, %3, 4;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %4, p1;\n\t"
+      "add.s64 a, %1, 1030;\n\tadd.s64 b, %3, 6;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %4, p1;\n\t}" ::"r"(tmem_d),
+      "l"(ad0), "l"(bd0), "l"(bd1), "r"(idesc), "r"(acc_first));
+}
 FL_DEV void commit_pair_elect(uint64_t* bar, uint16_t mask) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"
@@ -428,7 +457,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         // row of the contiguous 128 x 64 chunk (tile n0/128, K chunk k/64)
         const int wcol = P.w_tiled ? 0 : k;
         const int wrow = P.w_tiled ? ((n0 >> 7) * P.kch64 + (k >> 6)) * SK_BM : n0;
-        if (P.dbg_skip_x && role >= 0) {        // diagnostic: weights only (results garbage)
+        if ((P.dbg_skip_x && role >= 0) || (P.dbg_skip_x == 2 && role < 0)) {   // diagnostic (garbage results)
           if (leader) mbar_expect_tx(&full_bar[st], 0);
           return;
         }
@@ -548,6 +577,14 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
           }
           tc_fence_after();
           const uint8_t* st = smem + s * STAGE;
+          if (KPB == 2 && P.mt == 1 && !P.dbg_skip_mma) {
+            static_assert(SK_A_BYTES == 16384, "mma_stage2_elect steps A by 16 KB");
+            mma_stage2_elect(acc, desc_sw128(st), desc_sw128(st + AB), desc_sw128(st + AB + XB), idesc,
+                             c > klo ? 1u : 0u);
+            commit_pair_elect(&empty_bar[s], pmask);
+            if (++s == stages) { s = 0; ph ^= 1; }
+            continue;
+          }
           for (int kc = 0; kc < KPB && !P.dbg_skip_mma; ++kc) {
             const uint64_t ad = desc_sw128(st + kc * SK_A_BYTES);
             if (P.mt == 2) {
@@ -1231,7 +1268,7 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   P.slot_elems = SK_MAX_SPAN * SK_BM;
   P.flags = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + (size_t)SK_MAX_PAIRS * 2 * SK_MAX_SPAN * SK_BM * 4);
   P.dbg = g_sk_dbg;
-  P.dbg_skip_x = g_tune[6] == 1 ? 1 : 0;
+  P.dbg_skip_x = g_tune[6] == 1 || g_tune[6] == 2 ? g_tune[6] : 0;   // 2: no weight loads either
   P.dbg_skip_mma = g_tune[7] == 1 ? 1 : 0;
   P.l2_ahead = g_l2_ahead >= 0 ? g_l2_ahead : 0;
   P.dbg_skip_epi = g_l2_ahead == -2 ? 1 : 0;   // measured: 4..32 units slow every M (0.67 -> 0.57 at 144 rows)
