@@ -49,6 +49,7 @@ constexpr int SK_BK = 64;                  // K per stage (one 128-byte swizzle 
 constexpr int SK_THREADS = 320;
 constexpr int SK_A_BYTES = SK_BM * SK_BK * 2;
 constexpr int SK_MAXST = 16;
+constexpr int SK_MAXBUF = 4;               // TMEM accumulator buffers
 constexpr int SK_RING_BUDGET = 200 * 1024;
 constexpr int SK_STG_LD = 36;              // transpose row stride (floats): conflict-free
 
@@ -262,6 +263,7 @@ struct SkParams {
   int dbg_skip_x;            // diagnostics (fl_gemm_tune 6): no activation loads
   int dbg_skip_mma;          // diagnostics (fl_gemm_tune 7): no MMAs (pipeline + epilogue only)
   int dbg_skip_epi;          // diagnostics (fl_gemm_tune 8 = -2): no epilogue (TMEM drained unread)
+  int dbg_epi;               // diagnostics (key 8 = -10 - bits): 1 no GELU, 2 no output stores
   int l2_ahead;              // units of weights prefetched into L2 behind the ring fill
 };
 
@@ -329,15 +331,15 @@ FL_DEV void final_block(const SkParams& P, const uint32_t* r, float bv, float* w
 #pragma unroll
   for (int i = 0; i < 8; ++i) w[i] = *reinterpret_cast<const float4*>(ws_ + (i * 4 + jb) * SK_STG_LD + c4);
   const size_t o0 = static_cast<size_t>(m0 + cb) * P.ldo + ocol(P, nn);
-  const bool act = EPI == EPI_GELU && act_on(P, nn);
+  const bool act = EPI == EPI_GELU && act_on(P, nn) && !(P.dbg_epi & 1);
   if (EPI == EPI_STORE || EPI == EPI_GELU) {
     bf16* dst = static_cast<bf16*>(P.out) + o0;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int j = i * 4 + jb;
-      if (j >= ncol) continue;
+      if (j >= ncol || (P.dbg_epi & 2)) continue;
       float4 x = w[i];
-      if (act) { x.x = gelu_tanh(x.x); x.y = gelu_tanh(x.y); x.z = gelu_tanh(x.z); x.w = gelu_tanh(x.w); }
+      if (act) { x.x = gelu_fast(x.x); x.y = gelu_fast(x.y); x.z = gelu_fast(x.z); x.w = gelu_fast(x.w); }
       __nv_bfloat162 lo = __floats2bfloat162_rn(x.x, x.y), hi = __floats2bfloat162_rn(x.z, x.w);
       *reinterpret_cast<uint2*>(dst + static_cast<size_t>(j) * P.ldo) =
           make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
@@ -371,8 +373,8 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[SK_MAXST];
   __shared__ __align__(8) uint64_t empty_bar[SK_MAXST];
-  __shared__ __align__(8) uint64_t tfull_bar[2];
-  __shared__ __align__(8) uint64_t tempty_bar[2];
+  __shared__ __align__(8) uint64_t tfull_bar[SK_MAXBUF];
+  __shared__ __align__(8) uint64_t tempty_bar[SK_MAXBUF];
   __shared__ uint32_t tmem_base;
   __shared__ unsigned long long issue_clk[SK_MAXST];   // diagnostics: W issue time per stage
   __shared__ __align__(16) float stg[4 * 32 * SK_STG_LD];   // epilogue transpose, 32x36 per warp
@@ -411,7 +413,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       mbar_init(&full_bar[s], 1 + P.mt);   // weight producer + one per token sub-tile
       mbar_init(&empty_bar[s], 1);           // the pair's MMAs consumed the stage
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < SK_MAXBUF; ++b) {
       mbar_init(&tfull_bar[b], 1);
       mbar_init(&tempty_bar[b], 8);   // 4 epilogue warps x 2 CTAs
     }
@@ -521,7 +523,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       }
     }
     __syncwarp();
-    if (warp >= 6 && P.helpers && P.csplit == 1 && !P.dbg_skip_epi) {
+    if (warp >= 6 && P.helpers && P.csplit == 1 && !P.dbg_skip_epi) {   // (2: last segment skipped too)
       // ---- helpers: the odd 32-token blocks of the pair's last segment when
       // it is a whole tile (the ring is idle once its accumulator is full, so
       // the transpose buffers live there)
@@ -535,8 +537,8 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         const int quarter = warp & 3;
         const int n = nbase + quarter * 32 + lane;
         const float bv = (P.bias && n < P.N) ? __bfloat162float(P.bias[n]) : 0.f;
-        const int b = P.nbuf == 2 ? (seg & 1) : 0;
-        const uint32_t use = P.nbuf == 2 ? (seg >> 1) : seg;
+        const int b = seg % P.nbuf;
+        const uint32_t use = static_cast<uint32_t>(seg / P.nbuf);
         if (warp == 6 && lane == 0) mbar_wait_sleep(&tfull_bar[b], use & 1);
         asm volatile("bar.sync 2, 128;" ::: "memory");
         tc_fence_after();
@@ -559,8 +561,8 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       for (int u = R.lo[r]; u < R.hi[r];) {
         const Seg g = seg_at(u, R.hi[r], kch);
         const int klo = g.klo, khi = g.khi;
-        const int b = P.nbuf == 2 ? (seg & 1) : 0;
-        const uint32_t use = P.nbuf == 2 ? (seg >> 1) : seg;
+        const int b = seg % P.nbuf;
+        const uint32_t use = static_cast<uint32_t>(seg / P.nbuf);
         unsigned long long tw = P.dbg ? clock64() : 0;
         mbar_wait(&tempty_bar[b], (use & 1) ^ 1);   // epilogue drained this buffer
         if (P.dbg) twait += clock64() - tw;
@@ -724,7 +726,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
               *reinterpret_cast<float4*>(static_cast<float*>(P.out) + o) = acc;
             } else {
               if (act) {
-                acc.x = gelu_tanh(acc.x); acc.y = gelu_tanh(acc.y); acc.z = gelu_tanh(acc.z); acc.w = gelu_tanh(acc.w);
+                acc.x = gelu_fast(acc.x); acc.y = gelu_fast(acc.y); acc.z = gelu_fast(acc.z); acc.w = gelu_fast(acc.w);
               }
               __nv_bfloat162 l2 = __floats2bfloat162_rn(acc.x, acc.y), h2 = __floats2bfloat162_rn(acc.z, acc.w);
               *reinterpret_cast<uint2*>(static_cast<bf16*>(P.out) + o) =
@@ -735,7 +737,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
             for (int qq = 0; qq < 4 && nn + qq < P.N; ++qq) {
               if (EPI == EPI_ACC_F32) static_cast<float*>(P.out)[o + qq] += a4[qq];
               else if (EPI == EPI_STORE_F32) static_cast<float*>(P.out)[o + qq] = a4[qq];
-              else static_cast<bf16*>(P.out)[o + qq] = __float2bfloat16_rn(act ? gelu_tanh(a4[qq]) : a4[qq]);
+              else static_cast<bf16*>(P.out)[o + qq] = __float2bfloat16_rn(act ? gelu_fast(a4[qq]) : a4[qq]);
             }
           }
         }
@@ -756,8 +758,8 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
     for (int u = R.lo[r]; u < R.hi[r];) {
       const Seg g = seg_at(u, R.hi[r], kch);
       const int t = g.t, klo = g.klo, khi = g.khi;
-      const int b = P.nbuf == 2 ? (seg & 1) : 0;
-      const uint32_t use = P.nbuf == 2 ? (seg >> 1) : seg;
+      const int b = seg % P.nbuf;
+      const uint32_t use = static_cast<uint32_t>(seg / P.nbuf);
       const int tn = t / P.ntm, tm = t - tn * P.ntm;
       const int m0 = tm * P.span;
       const int mcount = min(P.slice, P.M - m0);
@@ -772,7 +774,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       epi_bar();
       if (P.dbg) e_wait += clock64() - tw0;
       tc_fence_after();
-      if (P.dbg_skip_epi) {                     // diagnostic: no epilogue work at all
+      if (P.dbg_skip_epi == 1 || (P.dbg_skip_epi == 2 && seg == nseg - 1)) {   // diagnostic: skip epilogue work
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(&tempty_bar[b], prank);
@@ -883,7 +885,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
               if (j >= ncol) continue;
               const size_t o = o0 + static_cast<size_t>(j) * P.ldo;
               if (EPI == EPI_STORE || EPI == EPI_GELU)
-                static_cast<bf16*>(P.out)[o] = __float2bfloat16_rn(act ? gelu_tanh(v[j]) : v[j]);
+                static_cast<bf16*>(P.out)[o] = __float2bfloat16_rn(act ? gelu_fast(v[j]) : v[j]);
               else if (EPI == EPI_ACC_F32)
                 static_cast<float*>(P.out)[o] += v[j];
               else
@@ -940,13 +942,13 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
           }
           if (EPI == EPI_STORE || EPI == EPI_GELU) {
             bf16* dst = static_cast<bf16*>(P.out) + static_cast<size_t>(m0 + cb) * P.ldo + ocol(P, nn);
-            const bool act = EPI == EPI_GELU && act_on(P, nn);
+            const bool act = EPI == EPI_GELU && act_on(P, nn) && !(P.dbg_epi & 1);
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
               const int j = i * 4 + jb;
-              if (j >= ncol) continue;
+              if (j >= ncol || (P.dbg_epi & 2)) continue;
               float4 x = w[i];
-              if (act) { x.x = gelu_tanh(x.x); x.y = gelu_tanh(x.y); x.z = gelu_tanh(x.z); x.w = gelu_tanh(x.w); }
+              if (act) { x.x = gelu_fast(x.x); x.y = gelu_fast(x.y); x.z = gelu_fast(x.z); x.w = gelu_fast(x.w); }
               __nv_bfloat162 lo = __floats2bfloat162_rn(x.x, x.y), hi = __floats2bfloat162_rn(x.z, x.w);
               *reinterpret_cast<uint2*>(dst + static_cast<size_t>(j) * P.ldo) =
                   make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
@@ -1162,7 +1164,14 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   P.stages = SK_RING_BUDGET / stage;
   if (P.stages > SK_MAXST) P.stages = SK_MAXST;
   if (g_tune[2] > 1 && g_tune[2] < P.stages) P.stages = g_tune[2];
-  P.nbuf = P.slice <= 256 ? 2 : 1;
+  // TMEM accumulator buffers: as many (<= SK_MAXBUF) as fit 512 columns, so
+  // the epilogue of a segment may lag the MMAs of the next ones
+  {
+    const int slice_cols = P.slice <= 32 ? 32 : P.slice <= 64 ? 64 : P.slice <= 128 ? 128 : P.slice;
+    int nb = 512 / slice_cols;
+    if (g_tune[7] >= 10) nb = g_tune[7] - 10;              // diagnostic: fixed buffer count
+    P.nbuf = nb < 1 ? 1 : nb > SK_MAXBUF ? SK_MAXBUF : nb;
+  }
   const int cols = P.nbuf * P.slice;
   P.ncols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
   P.units = ntm * P.ntn * P.kch;
@@ -1269,9 +1278,10 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   P.flags = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + (size_t)SK_MAX_PAIRS * 2 * SK_MAX_SPAN * SK_BM * 4);
   P.dbg = g_sk_dbg;
   P.dbg_skip_x = g_tune[6] == 1 || g_tune[6] == 2 ? g_tune[6] : 0;   // 2: no weight loads either
-  P.dbg_skip_mma = g_tune[7] == 1 ? 1 : 0;
+  P.dbg_skip_mma = g_tune[7] == 1 ? 1 : 0;   // (key 7 >= 10: TMEM buffer count - 10)
   P.l2_ahead = g_l2_ahead >= 0 ? g_l2_ahead : 0;
-  P.dbg_skip_epi = g_l2_ahead == -2 ? 1 : 0;   // measured: 4..32 units slow every M (0.67 -> 0.57 at 144 rows)
+  P.dbg_skip_epi = g_l2_ahead == -2 ? 1 : g_l2_ahead == -3 ? 2 : 0;   // -3: only the last segment
+  P.dbg_epi = g_l2_ahead <= -10 && g_l2_ahead > -20 ? -10 - g_l2_ahead : 0;   // measured: 4..32 units slow every M (0.67 -> 0.57 at 144 rows)
   P.nsplit = a.nsplit;
   P.ogap = a.ogap;
   P.vec = (a.ldo % 4 == 0 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0) ? 1 : 0;
