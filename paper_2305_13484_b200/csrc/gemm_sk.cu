@@ -46,7 +46,7 @@ namespace {
 
 constexpr int SK_BM = 128;                 // weight rows per CTA (256 per pair)
 constexpr int SK_BK = 64;                  // K per stage (one 128-byte swizzle row)
-constexpr int SK_THREADS = 320;
+constexpr int SK_THREADS = 384;             // 12 warps: producers 0,6,7; MMA 1; epilogue 2-5, 8-11
 constexpr int SK_A_BYTES = SK_BM * SK_BK * 2;
 constexpr int SK_MAXST = 16;
 constexpr int SK_MAXBUF = 4;               // TMEM accumulator buffers
@@ -218,6 +218,14 @@ FL_DEV void tmem_ld32(uint32_t taddr, uint32_t* r) {
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+FL_DEV void tmem_ld16(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
 FL_DEV unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -229,7 +237,7 @@ FL_DEV void st_release(unsigned* p, unsigned v) {
 FL_DEV void red_release_add(unsigned* p, unsigned v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-FL_DEV void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }   // the 4 epilogue warps
+FL_DEV void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }   // the 8 epilogue warps
 
 struct SkParams {
   int M, N, ldo, epi;
@@ -257,7 +265,6 @@ struct SkParams {
   int ntm;          // token tiles
   int w_tiled;      // weights in the fl_tile_weight layout [N/128][K/64][128][64]
   int kch64;        // K / 64
-  int helpers;      // warps 6-9 help drain the last whole tile
   int nsplit, ogap; // dual GEMM (GemmArgs::nsplit): rows >= nsplit read x2, GELU, column + ogap
   unsigned long long* dbg;   // diagnostics: per CTA [prod wait, prod total, mma wait, mma total]
   int dbg_skip_x;            // diagnostics (fl_gemm_tune 6): no activation loads
@@ -317,25 +324,78 @@ FL_DEV Seg seg_at(int u, int hi, int kch) {
   return g;
 }
 
-// Final epilogue of one 32-token block of a whole tile through the per-warp
-// smem transpose (lane -> 4 weight rows of one token, 16-byte accesses).
-template <int EPI>
-FL_DEV void final_block(const SkParams& P, const uint32_t* r, float bv, float* ws_, int lane, int quarter,
-                        int nbase, int m0, int cb, int ncol) {
+enum { BLK_FINAL = 0, BLK_PUB = 2, BLK_RED = 3 };
+
+// One 16-token block of one warp (lane = TMEM lane = weight row, r[j] = token
+// cb + j) through the per-warp smem transpose: afterwards lane holds 4
+// adjacent weight rows (c4) of tokens jb, jb + 4, jb + 8, jb + 12, so every
+// access is 16 bytes.  PUB: fp32 partial to the pair's slot; RED: red.add
+// into the fp32 residual.
+template <int EPI, int MODE>
+FL_DEV void block16(const SkParams& P, const uint32_t* r, float bv, float* ws_, int lane, int quarter, int nbase,
+                    int m0, int cb, int ncol, float* pub) {
 #pragma unroll
-  for (int j = 0; j < 32; ++j) ws_[j * SK_STG_LD + lane] = __uint_as_float(r[j]) + bv;
+  for (int j = 0; j < 16; ++j) ws_[j * SK_STG_LD + lane] = __uint_as_float(r[j]) + bv;
   __syncwarp();
   const int c4 = (lane & 7) * 4, jb = lane >> 3;
   const int nn = nbase + quarter * 32 + c4;
-  float4 w[8];
+  if (MODE == BLK_PUB) {
+    float* dst = pub + static_cast<size_t>(cb) * SK_BM + quarter * 32 + c4;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) w[i] = *reinterpret_cast<const float4*>(ws_ + (i * 4 + jb) * SK_STG_LD + c4);
+    for (int i = 0; i < 4; ++i) {
+      const int j = i * 4 + jb;
+      if (j < ncol)
+        *reinterpret_cast<float4*>(dst + j * SK_BM) = *reinterpret_cast<const float4*>(ws_ + j * SK_STG_LD + c4);
+    }
+  } else {
+    float* dst = static_cast<float*>(P.out) + static_cast<size_t>(m0 + cb) * P.ldo + nn;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int j = i * 4 + jb;
+      if (j < ncol) {
+        const float4 v = *reinterpret_cast<const float4*>(ws_ + j * SK_STG_LD + c4);
+        asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + static_cast<size_t>(j) * P.ldo),
+                     "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                     : "memory");
+      }
+    }
+  }
+  __syncwarp();
+}
+
+// Final epilogue of one 16-token block (whole tile, or the k = 0 owner of a
+// split tile adding the later pieces' partials of pairs pair+1 .. plast).
+template <int EPI>
+FL_DEV void final16(const SkParams& P, const uint32_t* r, float bv, float* ws_, int lane, int quarter, int nbase,
+                    int m0, int cb, int ncol, int pair, int plast, int xi) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j) ws_[j * SK_STG_LD + lane] = __uint_as_float(r[j]) + bv;
+  __syncwarp();
+  const int c4 = (lane & 7) * 4, jb = lane >> 3;
+  const int nn = nbase + quarter * 32 + c4;
+  float4 w[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) w[i] = *reinterpret_cast<const float4*>(ws_ + (i * 4 + jb) * SK_STG_LD + c4);
+  for (int p = pair + 1; p <= plast; ++p) {
+    const float* slot = P.part + static_cast<size_t>(p * 2 + xi) * P.slot_elems + static_cast<size_t>(cb) * SK_BM +
+                        quarter * 32 + c4;
+    float4 q[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int j = i * 4 + jb;
+      q[i] = j < ncol ? *reinterpret_cast<const float4*>(slot + j * SK_BM) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      w[i].x += q[i].x; w[i].y += q[i].y; w[i].z += q[i].z; w[i].w += q[i].w;
+    }
+  }
   const size_t o0 = static_cast<size_t>(m0 + cb) * P.ldo + ocol(P, nn);
-  const bool act = EPI == EPI_GELU && act_on(P, nn) && !(P.dbg_epi & 1);
   if (EPI == EPI_STORE || EPI == EPI_GELU) {
+    const bool act = EPI == EPI_GELU && act_on(P, nn) && !(P.dbg_epi & 1);
     bf16* dst = static_cast<bf16*>(P.out) + o0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < 4; ++i) {
       const int j = i * 4 + jb;
       if (j >= ncol || (P.dbg_epi & 2)) continue;
       float4 x = w[i];
@@ -346,16 +406,16 @@ FL_DEV void final_block(const SkParams& P, const uint32_t* r, float bv, float* w
     }
   } else {
     float* dst = static_cast<float*>(P.out) + o0;
-    float4 y[8];
+    float4 y[4];
     if (EPI == EPI_ACC_F32) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < 4; ++i) {
         const int j = i * 4 + jb;
         y[i] = j < ncol ? *reinterpret_cast<const float4*>(dst + static_cast<size_t>(j) * P.ldo) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
     }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < 4; ++i) {
       const int j = i * 4 + jb;
       if (j >= ncol) continue;
       float4 x = w[i];
@@ -364,6 +424,61 @@ FL_DEV void final_block(const SkParams& P, const uint32_t* r, float bv, float* w
     }
   }
   __syncwarp();
+}
+
+// Lane-per-weight-row final epilogue of one 16-token block (greedy argmax,
+// outputs not 16-byte aligned); the owner of a split tile adds the later
+// pieces' partials.
+template <int EPI>
+FL_DEV void rowwise16(const SkParams& P, const uint32_t* r, float bv, float* ws_, int lane, int quarter, int n,
+                      bool nok, int nbase, int m0, int cb, int ncol, int pair, int plast, int xi, int row) {
+  float v[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]) + bv;
+  for (int p = pair + 1; p <= plast; ++p) {
+    const float* slot = P.part + static_cast<size_t>(p * 2 + xi) * P.slot_elems + cb * SK_BM + row;
+    float q[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) q[j] = j < ncol ? slot[j * SK_BM] : 0.f;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] += q[j];
+  }
+  if (EPI == EPI_ARGMAX) {
+    // transpose through smem (stride 33: conflict-free both ways) so lane t
+    // (< 16) scans token t's 32 weight rows
+    float* tb = ws_;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) tb[j * 33 + lane] = v[j];
+    __syncwarp();
+    // lane t scans rows 16*(t / 16) .. +15 of token t % 16; the halves combine
+    const int nb = nbase + quarter * 32 + 16 * (lane >> 4), tok = lane & 15;
+    unsigned long long key = 0ull;
+#pragma unroll 8
+    for (int cc = 0; cc < 16; ++cc) {
+      if (nb + cc < P.N) {
+        const unsigned long long k2 = argmax_key(tb[tok * 33 + 16 * (lane >> 4) + cc], P.index_base + nb + cc);
+        key = k2 > key ? k2 : key;
+      }
+    }
+    const unsigned long long ko = __shfl_xor_sync(0xffffffffu, key, 16);
+    key = ko > key ? ko : key;
+    __syncwarp();
+    if (lane < ncol && key) atomicMax(&P.keys[m0 + cb + lane], key);
+  } else if (nok) {
+    const size_t o0 = static_cast<size_t>(m0 + cb) * P.ldo + ocol(P, n);
+    const bool act = EPI == EPI_GELU && act_on(P, n);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      if (j >= ncol) continue;
+      const size_t o = o0 + static_cast<size_t>(j) * P.ldo;
+      if (EPI == EPI_STORE || EPI == EPI_GELU)
+        static_cast<bf16*>(P.out)[o] = __float2bfloat16_rn(act ? gelu_fast(v[j]) : v[j]);
+      else if (EPI == EPI_ACC_F32)
+        static_cast<float*>(P.out)[o] += v[j];
+      else
+        static_cast<float*>(P.out)[o] = v[j];
+    }
+  }
 }
 
 template <int EPI>
@@ -377,7 +492,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
   __shared__ __align__(8) uint64_t tempty_bar[SK_MAXBUF];
   __shared__ uint32_t tmem_base;
   __shared__ unsigned long long issue_clk[SK_MAXST];   // diagnostics: W issue time per stage
-  __shared__ __align__(16) float stg[4 * 32 * SK_STG_LD];   // epilogue transpose, 32x36 per warp
+  __shared__ __align__(16) float stg[8 * 16 * SK_STG_LD];   // epilogue transpose, 16x36 per warp
 
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -395,7 +510,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
   const int stages = P.stages, kch = P.kch;
   const Ranges R = pair_ranges(P, pair);
   const int n0u = R.hi[0] - R.lo[0], nunits = n0u + R.hi[1] - R.lo[1];
-  // segments of this pair's work, and the last one (helpers drain it)
+  // segments of this pair's work
   int nseg = 0;
   Seg last{0, 0, 0};
   for (int r = 0; r < 2; ++r)
@@ -415,7 +530,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
     }
     for (int b = 0; b < SK_MAXBUF; ++b) {
       mbar_init(&tfull_bar[b], 1);
-      mbar_init(&tempty_bar[b], 8);   // 4 epilogue warps x 2 CTAs
+      mbar_init(&tempty_bar[b], 16);  // 8 epilogue warps x 2 CTAs
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -431,12 +546,11 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
   const uint32_t tmem = tmem_base;
   const int acc_cols = P.mt * P.bn;
 
-  if (warp == 0 || warp >= 6) {
-    // (warp 8: second weight producer when the weight tile is split in two)
+  if (warp == 0 || warp == 6 || warp == 7) {
     // producers: warp 0 streams the weight tiles, warp 6 + j the token
     // sub-tile j -- one TMA request per thread per K chunk (a request costs
     // its issuing thread ~250 cycles, tools/probes/tma_rate.cu)
-    const int role = warp == 0 ? -1 : warp == 8 ? -2 : warp - 6;   // -1/-2: weight parts, j >= 0: token sub-tile j
+    const int role = warp == 0 ? -1 : warp - 6;   // -1: weights, j >= 0: token sub-tile j
     if (lane == 0 && role < P.mt && role >= -1) {
       const uint32_t my_tx = 2u * (role < 0 ? AB : KPB * XB);   // both CTAs' bytes
       // units are issued strictly in order: walk the coordinates incrementally
@@ -523,34 +637,6 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       }
     }
     __syncwarp();
-    if (warp >= 6 && P.helpers && P.csplit == 1 && !P.dbg_skip_epi) {   // (2: last segment skipped too)
-      // ---- helpers: the odd 32-token blocks of the pair's last segment when
-      // it is a whole tile (the ring is idle once its accumulator is full, so
-      // the transpose buffers live there)
-      const int seg = nseg - 1, t = last.t, klo = last.klo, khi = last.khi;
-      const int tn = t / P.ntm, tm = t - tn * P.ntm;
-      const int m0 = tm * P.span;
-      const int mcount = min(P.slice, P.M - m0);
-      const int nbase = tn * 2 * SK_BM + xi * SK_BM;
-      const bool vec = P.vec && nbase + SK_BM <= P.N;
-      if (vec && klo == 0 && khi == kch && nseg > 0) {
-        const int quarter = warp & 3;
-        const int n = nbase + quarter * 32 + lane;
-        const float bv = (P.bias && n < P.N) ? __bfloat162float(P.bias[n]) : 0.f;
-        const int b = seg % P.nbuf;
-        const uint32_t use = static_cast<uint32_t>(seg / P.nbuf);
-        if (warp == 6 && lane == 0) mbar_wait_sleep(&tfull_bar[b], use & 1);
-        asm volatile("bar.sync 2, 128;" ::: "memory");
-        tc_fence_after();
-        const uint32_t tacc = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + b * acc_cols;
-        float* ws_ = reinterpret_cast<float*>(smem) + (warp - 6) * (32 * SK_STG_LD);
-        for (int cb = 32; cb < mcount; cb += 64) {
-          uint32_t r[32];
-          tmem_ld32(tacc + cb, r);
-          final_block<EPI>(P, r, bv, ws_, lane, quarter, nbase, m0, cb, min(32, mcount - cb));
-        }
-      }
-    }
   } else if (warp == 1) {
     if (leader) {                          // the whole warp; one elected lane issues
       const uint32_t idesc = idesc_bf16(2 * SK_BM, P.bn);
@@ -622,8 +708,12 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
     }
   } else {
     // ---------------------------------------------------------------- epilogue
+    // warps 2-5 and 8-11: a warp reads TMEM lane quarter warp % 4; the two
+    // warps of a quarter take alternate 16-token blocks (the epilogue, not
+    // the weight stream, bounds the wide windows: profiles/r02b_*)
     pdl_wait();   // EPI_ACC_F32 reads `out`, written by predecessors
-    const int quarter = warp & 3;
+    const int quarter = warp & 3, half = warp >= 8 ? 1 : 0;
+    float* ws_ = stg + (half * 4 + quarter) * (16 * SK_STG_LD);
     const int row = quarter * 32 + lane;
     int seg = 0;
     unsigned long long e_wait = 0, e_flag = 0, e_blk = 0, e_post = 0, e_ld = 0, e_sts = 0, e_t0 = clock64();
@@ -643,23 +733,10 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       epi_bar();
       tc_fence_after();
       float* pub = P.part + static_cast<size_t>(pair * 2 + xi) * P.slot_elems;
-      float* ws_ = stg + quarter * (32 * SK_STG_LD);
-      const int c4 = (lane & 7) * 4, jb = lane >> 3;
-      for (int cb = 0; cb < mcount; cb += 32) {
-        uint32_t r[32];
-        tmem_ld32(tacc + cb, r);
-        const int ncol = min(32, mcount - cb);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) ws_[j * SK_STG_LD + lane] = __uint_as_float(r[j]);
-        __syncwarp();
-        float* dst = pub + static_cast<size_t>(cb) * SK_BM + quarter * 32 + c4;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int j = i * 4 + jb;
-          if (j < ncol)
-            *reinterpret_cast<float4*>(dst + j * SK_BM) = *reinterpret_cast<const float4*>(ws_ + j * SK_STG_LD + c4);
-        }
-        __syncwarp();
+      for (int cb = 16 * half; cb < mcount; cb += 32) {
+        uint32_t r[16];
+        tmem_ld16(tacc + cb, r);
+        block16<EPI, BLK_PUB>(P, r, 0.f, ws_, lane, quarter, nbase, m0, cb, min(16, mcount - cb), pub);
       }
       // publish -> arrive: the CTA barrier orders every thread's partial
       // stores before one thread's gpu-scope release (CUTLASS's semaphore
@@ -678,11 +755,9 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       }
       epi_bar();
       if (P.dbg) e_flag += clock64() - tf0;
-      const unsigned long long tb0 = P.dbg ? clock64() : 0;
-      // reduce my token slice: warp (quarter) takes tokens, lane = 4 weight
-      // rows.  The partials come from L2 (other SMs wrote them): UN tokens'
-      // loads (x S pieces, + the residual for ACC) are issued before any is
-      // used, or the loop runs at one L2 round trip per token
+      // reduce my token slice: warp takes tokens, lane = 4 weight rows.  The
+      // partials come from L2 (other SMs wrote them): UN tokens' loads (x S
+      // pieces, + the residual for ACC) are issued before any is used
       const int lo = piece * mcount / S, hi = (piece + 1) * mcount / S;
       const int rrow = lane * 4;                      // row within this CTA's 128
       const int nn = nbase + rrow;
@@ -694,12 +769,13 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       const float* slot0 = P.part + static_cast<size_t>((t * S) * 2 + xi) * P.slot_elems + rrow;
       const size_t pstride = static_cast<size_t>(2) * P.slot_elems;   // next piece's slot
       constexpr int UN = 4;
-      for (int tok0 = lo + quarter; tok0 < hi; tok0 += 4 * UN) {
+      const int ew = half * 4 + quarter;
+      for (int tok0 = lo + ew; tok0 < hi; tok0 += 8 * UN) {
         float4 q[UN][4];
         float4 y[UN];
 #pragma unroll
         for (int u = 0; u < UN; ++u) {
-          const int tok = tok0 + 4 * u;
+          const int tok = tok0 + 8 * u;
 #pragma unroll
           for (int p = 0; p < 4; ++p)
             q[u][p] = (p < S && tok < hi) ? *reinterpret_cast<const float4*>(slot0 + p * pstride + static_cast<size_t>(tok) * SK_BM)
@@ -710,7 +786,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         }
 #pragma unroll
         for (int u = 0; u < UN; ++u) {
-          const int tok = tok0 + 4 * u;
+          const int tok = tok0 + 8 * u;
           if (tok >= hi) break;
           float4 acc = make_float4(b4[0], b4[1], b4[2], b4[3]);
 #pragma unroll
@@ -742,7 +818,6 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
           }
         }
       }
-      if (P.dbg) e_blk += clock64() - tb0;
       epi_bar();
       if (warp == 2 && lane == 0) {
         // the last reader re-arms both counters for the next launch
@@ -784,15 +859,15 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       }
 
       // segment mode: final epilogue (whole tile, or the k = 0 owner of a split
-      // tile after folding in the later pieces) or publish (a later piece of a
-      // split tile: the first segment of its pair's stream-K range)
-      enum { FINAL = 0, PUB = 2, RED = 3 };
-      int mode = FINAL, plast = pair;      // plast: last pair holding a piece
+      // tile after folding in the later pieces), publish (a later piece of a
+      // split tile: the first segment of its pair's stream-K range) or red
+      // (a piece of a split residual tile)
+      int mode = BLK_FINAL, plast = pair;      // plast: last pair holding a piece
       if (!whole && EPI == EPI_ACC_F32 && P.red) {
-        mode = RED;                        // residual: every piece red.adds its partial
+        mode = BLK_RED;
       } else if (!whole) {
         if (klo > 0) {
-          mode = PUB;
+          mode = BLK_PUB;
         } else {
           plast = owner_of((t + 1) * kch - 1, P);
           const unsigned long long tf0 = P.dbg ? clock64() : 0;
@@ -812,176 +887,55 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       }
       float* pub = P.part + static_cast<size_t>(pair * 2 + xi) * P.slot_elems;
       const unsigned long long tb0 = P.dbg ? clock64() : 0;
-      // Each mode has its own loops (mixing them lets the compiler predicate the
+      // Each mode has its own loop (mixing them lets the compiler predicate the
       // loads / atomics of other modes into the hot loop: 6x slower).  Stores
       // go through a per-warp smem transpose so every lane moves 16 bytes
-      // (4 weight rows of one token): a 32x32 block is 8 vector accesses per
-      // lane instead of 32 scalar ones (tools/probes/store_probe.cu: 2.8x).
+      // (4 weight rows of one token, tools/probes/store_probe.cu: 2.8x).
       const bool vec = P.vec && nbase + SK_BM <= P.N;
-      // last whole tile with helpers: warps 6-9 (done producing) drain the odd
-      // 32-token blocks, these warps the even ones
-      const bool helped = P.helpers && vec && whole && seg == nseg - 1;
-      if (helped) {
-        float* ws_ = stg + quarter * (32 * SK_STG_LD);
-        for (int cb = 0; cb < mcount; cb += 64) {
-          uint32_t r[32];
-          tmem_ld32(tacc + cb, r);
-          final_block<EPI>(P, r, bv, ws_, lane, quarter, nbase, m0, cb, min(32, mcount - cb));
+      if (mode == BLK_PUB) {
+        for (int cb = 16 * half; cb < mcount; cb += 32) {
+          uint32_t r[16];
+          tmem_ld16(tacc + cb, r);
+          block16<EPI, BLK_PUB>(P, r, bv, ws_, lane, quarter, nbase, m0, cb, min(16, mcount - cb), pub);
         }
-      }
-      for (int cb = 0; cb < mcount && !helped; cb += 32) {
-        uint32_t r[32];
-        const unsigned long long tl0 = P.dbg ? clock64() : 0;
-        tmem_ld32(tacc + cb, r);
-        const int ncol = min(32, mcount - cb);
-        if (P.dbg) e_ld += clock64() - tl0;
-        if (EPI == EPI_ACC_F32 && mode == RED && !vec) {
-          // unaligned residual rows: scalar float atomics, lane = weight row
+      } else if (EPI == EPI_ACC_F32 && mode == BLK_RED && vec) {
+        for (int cb = 16 * half; cb < mcount; cb += 32) {
+          uint32_t r[16];
+          tmem_ld16(tacc + cb, r);
+          block16<EPI, BLK_RED>(P, r, bv, ws_, lane, quarter, nbase, m0, cb, min(16, mcount - cb), pub);
+        }
+      } else if (EPI == EPI_ACC_F32 && mode == BLK_RED) {
+        // unaligned residual rows: scalar float atomics, lane = weight row
+        for (int cb = 16 * half; cb < mcount; cb += 32) {
+          uint32_t r[16];
+          tmem_ld16(tacc + cb, r);
+          const int ncol = min(16, mcount - cb);
           if (nok) {
             float* dst = static_cast<float*>(P.out) + static_cast<size_t>(m0 + cb) * P.ldo + n;
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
+            for (int j = 0; j < 16; ++j)
               if (j < ncol) atomicAdd(dst + static_cast<size_t>(j) * P.ldo, __uint_as_float(r[j]) + bv);
           }
-          continue;
         }
-        if ((EPI == EPI_ARGMAX || !vec) && mode == FINAL) {
-          // lane-per-weight-row epilogues (argmax reduce, unaligned outputs)
-          float v[32];
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) + bv;
-          for (int p = pair + 1; p <= plast; ++p) {
-            const float* slot = P.part + static_cast<size_t>(p * 2 + xi) * P.slot_elems + cb * SK_BM + row;
-            float q[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) q[j] = j < ncol ? slot[j * SK_BM] : 0.f;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] += q[j];
-          }
-          if (EPI == EPI_ARGMAX) {
-            // transpose through smem (stride 33: conflict-free both ways) so
-            // lane t scans token t's 32 weight rows: 64 shared accesses per
-            // block instead of 10 shuffles per token
-            float* tb = stg + quarter * (32 * SK_STG_LD);
-#pragma unroll
-            for (int j = 0; j < 32; ++j) tb[j * 33 + lane] = v[j];
-            __syncwarp();
-            const int nb = nbase + quarter * 32;
-            unsigned long long key = 0ull;
-#pragma unroll 8
-            for (int cc = 0; cc < 32; ++cc) {
-              if (nb + cc < P.N) {
-                const unsigned long long k2 = argmax_key(tb[lane * 33 + cc], P.index_base + nb + cc);
-                key = k2 > key ? k2 : key;
-              }
-            }
-            __syncwarp();
-            if (lane < ncol && key) atomicMax(&P.keys[m0 + cb + lane], key);
-          } else if (nok) {
-            const size_t o0 = static_cast<size_t>(m0 + cb) * P.ldo + ocol(P, n);
-            const bool act = EPI == EPI_GELU && act_on(P, n);
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              if (j >= ncol) continue;
-              const size_t o = o0 + static_cast<size_t>(j) * P.ldo;
-              if (EPI == EPI_STORE || EPI == EPI_GELU)
-                static_cast<bf16*>(P.out)[o] = __float2bfloat16_rn(act ? gelu_fast(v[j]) : v[j]);
-              else if (EPI == EPI_ACC_F32)
-                static_cast<float*>(P.out)[o] += v[j];
-              else
-                static_cast<float*>(P.out)[o] = v[j];
-            }
-          }
-          continue;
+      } else if (EPI == EPI_ARGMAX || !vec) {
+        for (int cb = 16 * half; cb < mcount; cb += 32) {
+          uint32_t r[16];
+          tmem_ld16(tacc + cb, r);
+          rowwise16<EPI>(P, r, bv, ws_, lane, quarter, n, nok, nbase, m0, cb, min(16, mcount - cb), pair, plast, xi,
+                         row);
         }
-        // ---- staged: lane -> token j = (i*32+lane)/8, weight rows c4..c4+3
-        float* ws_ = stg + quarter * (32 * SK_STG_LD);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) ws_[j * SK_STG_LD + lane] = __uint_as_float(r[j]) + bv;
-        __syncwarp();
-        const int c4 = (lane & 7) * 4;
-        const int jb = lane >> 3;
-        const int nn = nbase + quarter * 32 + c4;
-        if (EPI == EPI_ACC_F32 && mode == RED) {
-          float* dst = static_cast<float*>(P.out) + static_cast<size_t>(m0 + cb) * P.ldo + nn;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int j = i * 4 + jb;
-            if (j < ncol) {
-              const float4 v = *reinterpret_cast<const float4*>(ws_ + j * SK_STG_LD + c4);
-              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + static_cast<size_t>(j) * P.ldo),
-                           "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
-                           : "memory");
-            }
-          }
-        } else if (mode == PUB) {
-          float* dst = pub + static_cast<size_t>(cb) * SK_BM + quarter * 32 + c4;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int j = i * 4 + jb;
-            if (j < ncol)
-              *reinterpret_cast<float4*>(dst + j * SK_BM) = *reinterpret_cast<const float4*>(ws_ + j * SK_STG_LD + c4);
-          }
-        } else {
-          float4 w[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) w[i] = *reinterpret_cast<const float4*>(ws_ + (i * 4 + jb) * SK_STG_LD + c4);
-          for (int p = pair + 1; p <= plast; ++p) {
-            const float* slot = P.part + static_cast<size_t>(p * 2 + xi) * P.slot_elems +
-                                static_cast<size_t>(cb) * SK_BM + quarter * 32 + c4;
-            float4 q[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int j = i * 4 + jb;
-              q[i] = j < ncol ? *reinterpret_cast<const float4*>(slot + j * SK_BM) : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              w[i].x += q[i].x; w[i].y += q[i].y; w[i].z += q[i].z; w[i].w += q[i].w;
-            }
-          }
-          if (EPI == EPI_STORE || EPI == EPI_GELU) {
-            bf16* dst = static_cast<bf16*>(P.out) + static_cast<size_t>(m0 + cb) * P.ldo + ocol(P, nn);
-            const bool act = EPI == EPI_GELU && act_on(P, nn) && !(P.dbg_epi & 1);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int j = i * 4 + jb;
-              if (j >= ncol || (P.dbg_epi & 2)) continue;
-              float4 x = w[i];
-              if (act) { x.x = gelu_fast(x.x); x.y = gelu_fast(x.y); x.z = gelu_fast(x.z); x.w = gelu_fast(x.w); }
-              __nv_bfloat162 lo = __floats2bfloat162_rn(x.x, x.y), hi = __floats2bfloat162_rn(x.z, x.w);
-              *reinterpret_cast<uint2*>(dst + static_cast<size_t>(j) * P.ldo) =
-                  make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
-            }
-          } else if (EPI == EPI_ACC_F32) {
-            float* dst = static_cast<float*>(P.out) + static_cast<size_t>(m0 + cb) * P.ldo + nn;
-            float4 y[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int j = i * 4 + jb;
-              y[i] = j < ncol ? *reinterpret_cast<const float4*>(dst + static_cast<size_t>(j) * P.ldo) : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int j = i * 4 + jb;
-              if (j < ncol)
-                *reinterpret_cast<float4*>(dst + static_cast<size_t>(j) * P.ldo) =
-                    make_float4(y[i].x + w[i].x, y[i].y + w[i].y, y[i].z + w[i].z, y[i].w + w[i].w);
-            }
-          } else {
-            float* dst = static_cast<float*>(P.out) + static_cast<size_t>(m0 + cb) * P.ldo + nn;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int j = i * 4 + jb;
-              if (j < ncol) *reinterpret_cast<float4*>(dst + static_cast<size_t>(j) * P.ldo) = w[i];
-            }
-          }
+      } else {
+        for (int cb = 16 * half; cb < mcount; cb += 32) {
+          uint32_t r[16];
+          const unsigned long long tl0 = P.dbg ? clock64() : 0;
+          tmem_ld16(tacc + cb, r);
+          if (P.dbg) e_ld += clock64() - tl0;
+          final16<EPI>(P, r, bv, ws_, lane, quarter, nbase, m0, cb, min(16, mcount - cb), pair, plast, xi);
         }
-        __syncwarp();
       }
       const unsigned long long tb1 = P.dbg ? clock64() : 0;
       if (P.dbg) e_blk += tb1 - tb0;
-      if (mode == PUB) {
+      if (mode == BLK_PUB) {
         epi_bar();      // every thread's partial stores before the release
         if (warp == 2 && lane == 0) st_release(&P.flags[pair * 2 + xi], 1u);
       } else if (plast > pair) {
@@ -989,7 +943,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         if (warp == 2 && lane == 0)
           for (int q = pair + 1; q <= plast; ++q) P.flags[q * 2 + xi] = 0u;   // re-arm
       }
-      // this buffer may be overwritten by the next-but-one segment
+      // this buffer may be overwritten by the next-but-(nbuf-1) segment
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(&tempty_bar[b], prank);
@@ -1176,7 +1130,6 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   P.ncols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
   P.units = ntm * P.ntn * P.kch;
   P.ntm = ntm;
-  P.helpers = (a.epi == EPI_STORE || a.epi == EPI_GELU || a.epi == EPI_ACC_F32 || a.epi == EPI_STORE_F32) ? 1 : 0;
   void (*kern)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const SkParams) = nullptr;
   switch (a.epi) {
     case EPI_STORE: kern = k_gemm_sk<EPI_STORE>; break;
