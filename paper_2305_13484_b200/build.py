@@ -22,6 +22,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-v", "-I", os.path.join(ROOT, "include")]
+# FL_NVCC_DEFS="-DX=1 ...": extra defines for A/B builds in tools/ (not the product build)
+FLAGS += os.environ.get("FL_NVCC_DEFS", "").split()
 SOURCES = ["flover_abi.cu", "step_kernels.cu", "attention.cu", "shuffle.cu", "gemm_simt.cu",
            "gemm_sk.cu", "planner.cu"]
 

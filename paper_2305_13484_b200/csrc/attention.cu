@@ -19,6 +19,9 @@ namespace fl {
 
 constexpr int ATT_CHUNK = 256;
 constexpr int ATT_THREADS = 128;
+#ifndef ATT_TILE_BYTES
+#define ATT_TILE_BYTES 0   // 0: per head_dim (AttnCfg::TKB); A/B builds override
+#endif
 
 int attn_max_splits(int S) { return (S + ATT_CHUNK - 1) / ATT_CHUNK; }
 
@@ -63,8 +66,14 @@ struct AttnCfg {
   static constexpr int CW = 4;                            // consumer warps
   static constexpr int THREADS = (CW + 1) * 32;
   static constexpr int ROW = HD * sizeof(T);              // bytes per key row
-  static constexpr int TK = (16384 / ROW) / (CW * KPW) * (CW * KPW);   // keys per tile
-  static constexpr int STAGES = 3;
+  // K bytes per tile: 16 KB at head_dim 256; 8 KB below, where a key is cheap
+  // to stream but costly to score (finer tiles keep more of the 48 KB ring in
+  // flight: hd 96 5.07 -> 5.50 TB/s, hd 256 16 KB 6.2 vs 8 KB 6.0 TB/s,
+  // tools/attn_bench.py)
+  static constexpr int TKB = ATT_TILE_BYTES ? ATT_TILE_BYTES : (HD >= 256 ? 16384 : 8192);
+  static constexpr int TK = (TKB / ROW) / (CW * KPW) * (CW * KPW) > 0 ? (TKB / ROW) / (CW * KPW) * (CW * KPW)
+                                                                      : CW * KPW;   // keys per tile
+  static constexpr int STAGES = (3 * 16384) / (TK * ROW) < 2 ? 2 : (3 * 16384) / (TK * ROW);
   static constexpr int STAGE_BYTES = 2 * TK * ROW;        // K tile + V tile
   static constexpr int SMEM = STAGES * STAGE_BYTES;
 };
