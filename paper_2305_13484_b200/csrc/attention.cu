@@ -237,7 +237,8 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
         // four independent partial sums: the dot product is otherwise one
         // dependent FMA chain of PER*VEC links per key (latency-bound at the
         // ~2 consumer warps per scheduler the smem ring leaves room for)
-        float d4[4] = {0.f, 0.f, 0.f, 0.f};
+        // (sm_100 packed FFMA2: two fp32 FMAs per instruction)
+        float2 d2a = make_float2(0.f, 0.f), d2b = make_float2(0.f, 0.f);
         if (valid) {
 #pragma unroll
           for (int p = 0; p < PER; ++p) {
@@ -246,11 +247,15 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
               float kf[VEC];
               widen16<T>(*reinterpret_cast<const uint4*>(Ks + k * Cfg::ROW + vi * 16), kf);
 #pragma unroll
-              for (int j = 0; j < VEC; ++j) d4[j & 3] = fmaf(qv[p][j], kf[j], d4[j & 3]);
+              for (int j = 0; j < VEC; j += 2) {
+                const float2 q2 = make_float2(qv[p][j], qv[p][j + 1]), k2 = make_float2(kf[j], kf[j + 1]);
+                if ((j >> 1) & 1) d2b = __ffma2_rn(q2, k2, d2b);
+                else d2a = __ffma2_rn(q2, k2, d2a);
+              }
             }
           }
         }
-        float dot = (d4[0] + d4[1]) + (d4[2] + d4[3]);
+        float dot = (d2a.x + d2a.y) + (d2b.x + d2b.y);
 #pragma unroll
         for (int o = G / 2; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
         if (valid) {
@@ -265,8 +270,14 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
             if (vi < NV) {
               float vf[VEC];
               widen16<T>(*reinterpret_cast<const uint4*>(Vs + k * Cfg::ROW + vi * 16), vf);
+              const float2 pk2 = make_float2(pk, pk), c2 = make_float2(c, c);
 #pragma unroll
-              for (int j = 0; j < VEC; ++j) acc[p][j] = fmaf(pk, vf[j], acc[p][j] * c);
+              for (int j = 0; j < VEC; j += 2) {
+                const float2 a2 = __ffma2_rn(pk2, make_float2(vf[j], vf[j + 1]),
+                                             __fmul2_rn(make_float2(acc[p][j], acc[p][j + 1]), c2));
+                acc[p][j] = a2.x;
+                acc[p][j + 1] = a2.y;
+              }
             }
           }
         }
