@@ -47,7 +47,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 # steady_rows / steady_ctx: mean fused rows per iteration and mean attended
-# context of the GPU serve (BENCH_r01 / profiles/r01h_*), the shape of the
+# context of the GPU serve (profiles/r02i_bench_*), the shape of the
 # reference arm's steady-state CPU slice (ours re-measures them live)
 CONFIGS = {
     "c1": dict(workload="C1: tiny GPT (4L, d=256, 4 heads) fp32, 32 Poisson requests (mean gap 20 ms), "
@@ -56,15 +56,15 @@ CONFIGS = {
     "c2": dict(workload="C2: GPT-2 small (12L, d=768, 12 heads) bf16, 128 Poisson requests (mean gap "
                         "20 ms), U(32,512) outputs, input_len 32, 1 B200", spec="gpt2-small", n=128,
                mean=20.0, lo=32, hi=512, max_out=512, input_len=32, dtype="bf16", pool=160,
-               steady_rows=25, steady_ctx=85),
+               steady_rows=12, steady_ctx=120),
     "c3": dict(workload="C3: GPT-J 6B shape (28L, d=4096, 16 heads) bf16, 512 Poisson requests (mean gap "
                         "20 ms), U(128,1024) outputs, input_len 32, tensor-parallel", spec="gptj-6b",
                n=512, mean=20.0, lo=128, hi=1024, max_out=1024, input_len=32, dtype="bf16", pool=0,
-               steady_rows=158, steady_ctx=295),
+               steady_rows=123, steady_ctx=338),
     "c4": dict(workload="C4: GPT-NeoX 20B shape (44L, d=6144, 64 heads) bf16, 64 Poisson requests, "
                         "U(128,1024) outputs (long, shuffle-heavy), input_len 32", spec="neox-20b",
                n=64, mean=20.0, lo=128, hi=1024, max_out=1024, input_len=32, dtype="bf16", pool=0,
-               steady_rows=66, steady_ctx=198),
+               steady_rows=39, steady_ctx=328),
 }
 
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
