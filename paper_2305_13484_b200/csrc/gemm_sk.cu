@@ -58,7 +58,7 @@ thread_local std::string g_sk_err;
 // 2 ring stages, 3 K sub-chunks per unit, 4 min units per stream-K range,
 // 5 tokens per token tile (span cap, <= 512)
 int g_tune[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
-int g_l2_ahead = -1;                      // fl_gemm_tune key 8
+int g_l2_ahead = -1;                      // fl_gemm_tune key 8 (L2 prefetch depth / diagnostics)
 unsigned long long* g_sk_dbg = nullptr;
 
 FL_DEV uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -1232,9 +1232,12 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   P.dbg = g_sk_dbg;
   P.dbg_skip_x = g_tune[6] == 1 || g_tune[6] == 2 ? g_tune[6] : 0;   // 2: no weight loads either
   P.dbg_skip_mma = g_tune[7] == 1 ? 1 : 0;   // (key 7 >= 10: TMEM buffer count - 10)
+  // key 8 >= 0: L2 prefetch depth (measured: 4..32 units slow every M, so 0);
+  // diagnostics: -2 no epilogue, -3 no epilogue for the last segment,
+  // -10 - bits: 1 no GELU, 2 no output stores
   P.l2_ahead = g_l2_ahead >= 0 ? g_l2_ahead : 0;
-  P.dbg_skip_epi = g_l2_ahead == -2 ? 1 : g_l2_ahead == -3 ? 2 : 0;   // -3: only the last segment
-  P.dbg_epi = g_l2_ahead <= -10 && g_l2_ahead > -20 ? -10 - g_l2_ahead : 0;   // measured: 4..32 units slow every M (0.67 -> 0.57 at 144 rows)
+  P.dbg_skip_epi = g_l2_ahead == -2 ? 1 : g_l2_ahead == -3 ? 2 : 0;
+  P.dbg_epi = g_l2_ahead <= -10 && g_l2_ahead > -20 ? -10 - g_l2_ahead : 0;
   P.nsplit = a.nsplit;
   P.ogap = a.ogap;
   P.vec = (a.ldo % 4 == 0 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0) ? 1 : 0;
