@@ -19,6 +19,9 @@ namespace fl {
 
 constexpr int ATT_CHUNK = 256;
 constexpr int ATT_THREADS = 128;
+#ifndef ATT_CW
+#define ATT_CW 4   // consumer warps per CTA (A/B builds: 8 = one CTA per SM)
+#endif
 #ifndef ATT_TILE_BYTES
 #define ATT_TILE_BYTES 0   // 0: per head_dim (AttnCfg::TKB); A/B builds override
 #endif
@@ -63,7 +66,7 @@ struct AttnCfg {
   static constexpr int G = (NV % G0 == 0 || NV % 4 != 0) ? G0 : 4;   // lanes per key
   static constexpr int PER = (NV + G - 1) / G;            // vectors per lane
   static constexpr int KPW = 32 / G;                      // keys per warp-step
-  static constexpr int CW = 4;                            // consumer warps
+  static constexpr int CW = ATT_CW;                       // consumer warps
   static constexpr int THREADS = (CW + 1) * 32;
   static constexpr int ROW = HD * sizeof(T);              // bytes per key row
   // K bytes per tile: 16 KB at head_dim 256; 8 KB below, where a key is cheap
@@ -73,7 +76,9 @@ struct AttnCfg {
   static constexpr int TKB = ATT_TILE_BYTES ? ATT_TILE_BYTES : (HD >= 256 ? 16384 : 8192);
   static constexpr int TK = (TKB / ROW) / (CW * KPW) * (CW * KPW) > 0 ? (TKB / ROW) / (CW * KPW) * (CW * KPW)
                                                                       : CW * KPW;   // keys per tile
-  static constexpr int STAGES = (3 * 16384) / (TK * ROW) < 2 ? 2 : (3 * 16384) / (TK * ROW);
+  // ring budget per CTA: 96 KB at 4 consumer warps (2 CTAs per SM), 192 KB at 8 (1 CTA per SM)
+  static constexpr int RING = ATT_CW >= 8 ? 6 * 32768 : 3 * 32768;
+  static constexpr int STAGES = (RING / 2) / (TK * ROW) < 2 ? 2 : (RING / 2) / (TK * ROW);
   static constexpr int STAGE_BYTES = 2 * TK * ROW;        // K tile + V tile
   static constexpr int SMEM = STAGES * STAGE_BYTES;
 };
@@ -382,7 +387,8 @@ static int attn_launch(const void* q, const fl_row* rows, const int32_t* row_ctx
   const int ms = attn_max_splits(S);           // workspace stride (CHUNK-sized splits)
   const int splits = (S + kps - 1) / kps;
   const int items = M * Hl * splits;
-  const int grid = items < 2 * num_sms ? items : 2 * num_sms;
+  const int per_sm = ATT_CW >= 8 ? 1 : 2;
+  const int grid = items < per_sm * num_sms ? items : per_sm * num_sms;
   launch_k(k_attn_tma<T, HD>, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM, s, 1, (const T*)q, rows,
            row_ctx, M, Hl, (const T*)kv_layer, S, (T*)out, ws_o, ws_ml, ms, kps, splits, order, ldo);
   if (splits > 1) {
