@@ -1,5 +1,10 @@
 #!/bin/bash
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_kernels.py -x -q -k "argmax or lm_head" > gpurun_out/e8b_tests.log 2>&1
-for o in out lm; do ONLY=$o timeout 200 python tools/step_gemm_bench.py 8 64 144 256 >> gpurun_out/e8b.log 2>&1; done
-for o in out lm; do ONLY=$o FL_LIB=tools/_ab/lib_pre8.so timeout 200 python tools/step_gemm_bench.py 8 64 144 256 >> gpurun_out/e8b.log 2>&1; done
+for lib in base cw8; do
+for rep in 1 2; do
+FL_LIB=tools/_ab/lib_$lib.so timeout 120 python tools/attn_bench.py 144 256 16 700 >> gpurun_out/ab4_att_$lib.log 2>&1
+FL_LIB=tools/_ab/lib_$lib.so timeout 120 python tools/attn_bench.py 64 96 64 1055 >> gpurun_out/ab4_att_$lib.log 2>&1
+FL_LIB=tools/_ab/lib_$lib.so timeout 120 python tools/attn_bench.py 144 256 16 300 >> gpurun_out/ab4_att_$lib.log 2>&1
+done
+FL_LIB=tools/_ab/lib_$lib.so timeout 300 python tools/prof_step.py --config c3 --rows 128 --pre 300 --iters 20 >> gpurun_out/ab4_step_$lib.log 2>&1
+done
