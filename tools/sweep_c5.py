@@ -33,6 +33,9 @@ def main():
     ap.add_argument("--window", type=float, default=50.0)
     ap.add_argument("--spec", default="gptj-6b")
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--instances-max-rate", type=float, default=0.0,
+                    help="also run concurrent instances (device clock, one batch-1 decoder per live request on "
+                         "its own stream) at rates up to this many req/s")
     a = ap.parse_args()
     spec = get_spec(a.spec)
     params = fl.CostParams(preprocess_ms=0.0)
@@ -49,7 +52,10 @@ def main():
         ex.prompts = prompts
         tokens = sum(r.actual_output_length for r in reqs)
         out = {"lambda_req_s": lam, "requests": a.n, "tokens": tokens, "model": a.spec}
-        for name in ("fusion", "dynamic_batching"):
+        names = ["fusion", "dynamic_batching"]
+        if lam <= a.instances_max_rate:
+            names.append("concurrent_instances")
+        for name in names:
             ex.reset()
             t0 = time.perf_counter()
             if name == "fusion":
@@ -59,11 +65,15 @@ def main():
                 tr = fl.Trace("fusion", st.events)
                 tr.sort()
                 busy = sum(st.device_ms)
-            else:
-                before = len(ex.shuffle_log)
+            elif name == "dynamic_batching":
                 tr = fl.run_dynamic_batching(reqs, fl.BatchWindowConfig(a.window), params,
                                              executor=ex, clock="device")
                 busy = sum(e.value for e in tr.of_kind(fl.EventKind.ITERATION_COMPLETED))
+            else:
+                tr = fl.run_concurrent_instances(reqs, params, executor=ex, clock="device",
+                                                 max_instances=64)
+                m0 = fl.compute_metrics(tr, a.n)
+                busy = m0.makespan_ms              # instances overlap: device time = their span
             wall = time.perf_counter() - t0
             m = fl.compute_metrics(tr, a.n)
             out[name] = {"tokens_per_s_busy": tokens / (busy / 1e3), "busy_ms": busy,
