@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
     const T* __restrict__ q, const fl_row* __restrict__ rows, const int32_t* __restrict__ row_ctx,
     int M, int Hl, const T* __restrict__ kv_layer, int S, T* __restrict__ out,
     float* __restrict__ ws_o, float* __restrict__ ws_ml, int max_splits, int keys_per_split,
-    int splits, const int32_t* __restrict__ order, int ldo) {
+    int splits, const int32_t* __restrict__ order, int ldo, unsigned* __restrict__ ctr) {
   using Cfg = AttnCfg<T, HD>;
   constexpr int VEC = Cfg::VEC, NV = Cfg::NV, G = Cfg::G, PER = Cfg::PER, KPW = Cfg::KPW;
   constexpr int CW = Cfg::CW, TK = Cfg::TK, STAGES = Cfg::STAGES, NP = CW;
@@ -139,12 +139,23 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
   __shared__ __align__(8) uint64_t empty[STAGES];
   __shared__ float s_m[NP], s_l[NP];
   __shared__ __align__(16) float s_acc[NP][HD];
+  // items are handed out dynamically (one atomic per item, in descending-cost
+  // order): the producer claims the next item and passes it to the consumers
+  // through a small smem queue -- a CTA that runs fast takes more items
+  constexpr int QD = 4;
+  __shared__ int q_item[QD];
+  __shared__ __align__(8) uint64_t q_full[QD];
+  __shared__ __align__(8) uint64_t q_empty[QD];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
       mbar_init_(&full[i], 1);
       mbar_init_(&empty[i], CW);
+    }
+    for (int i = 0; i < QD; ++i) {
+      mbar_init_(&q_full[i], 1);
+      mbar_init_(&q_empty[i], CW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -154,30 +165,31 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
 
   const int n_items = M * Hl * splits;
   const int D = Hl * HD;
-  // items (rank of the row by descending context, head, split) are dealt out
-  // boustrophedon-style: CTA b takes item b in even rounds and G-1-b in odd
-  // rounds, so with costs sorted longest-first every CTA gets a near-equal
-  // share (static round-robin over mixed contexts left a ~1.4x tail)
-  auto snake_item = [&](int round) {
-    const int G = static_cast<int>(gridDim.x);
-    return round * G + ((round & 1) ? (G - 1 - static_cast<int>(blockIdx.x)) : static_cast<int>(blockIdx.x));
-  };
   const size_t head_stride = static_cast<size_t>(S) * HD;
 
   if (warp == CW) {
     // ---------------- producer: one lane streams K/V tiles into the ring
     if (lane == 0) {
-      int st = 0;
-      uint32_t ph = 0;
-      for (int round = 0; round * static_cast<int>(gridDim.x) < n_items; ++round) {
-        const int item = snake_item(round);
-        if (item >= n_items) continue;
-        const int sp = item % splits;
-        const int rh = item / splits;
-        const int h = rh % Hl, r = order ? order[rh / Hl] : rh / Hl;
-        const int ctx = row_ctx[r];
-        const int k0 = sp * keys_per_split;
-        if (k0 >= ctx) continue;
+      int st = 0, qs = 0;
+      uint32_t ph = 0, qph = 0;
+      for (;;) {
+        int item = static_cast<int>(atomicAdd(ctr, 1u));
+        if (item >= n_items) item = -1;
+        int sp = 0, h = 0, r = 0, ctx = 0, k0 = 0;
+        if (item >= 0) {
+          sp = item % splits;
+          const int rh = item / splits;
+          h = rh % Hl;
+          r = order ? order[rh / Hl] : rh / Hl;
+          ctx = row_ctx[r];
+          k0 = sp * keys_per_split;
+          if (k0 >= ctx) continue;            // a split past this row's context: no work
+        }
+        mbar_wait_(&q_empty[qs], qph ^ 1);
+        q_item[qs] = item;
+        mbar_arrive_(&q_full[qs]);
+        if (++qs == QD) { qs = 0; qph ^= 1; }
+        if (item < 0) break;
         const int k1 = min(ctx, k0 + keys_per_split);
         const size_t slot = rows[r].slot;
         const T* Kb = kv_layer + ((slot * 2 + 0) * Hl + h) * head_stride;
@@ -201,11 +213,15 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
   const int kw = lane / G;          // key group within the warp
 
   const float scale = rsqrtf(static_cast<float>(HD));
-  int st = 0;
-  uint32_t ph = 0;
-  for (int round = 0; round * static_cast<int>(gridDim.x) < n_items; ++round) {
-    const int item = snake_item(round);
-    if (item >= n_items) continue;
+  int st = 0, qs = 0;
+  uint32_t ph = 0, qph = 0;
+  for (;;) {
+    mbar_wait_(&q_full[qs], qph);
+    const int item = q_item[qs];
+    __syncwarp();
+    if (lane == 0) mbar_arrive_(&q_empty[qs]);
+    if (++qs == QD) { qs = 0; qph ^= 1; }
+    if (item < 0) break;
     const int sp = item % splits;
     const int rh = item / splits;
     const int h = rh % Hl, r = order ? order[rh / Hl] : rh / Hl;
@@ -349,6 +365,12 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
     }
     asm volatile("bar.sync 1, %0;" ::"n"(CW * 32) : "memory");   // merge buffers reused
   }
+  // this CTA's producer claimed its last item before it sent the sentinel:
+  // the last CTA to finish re-arms the item counter for the next launch
+  if (threadIdx.x == 0 && atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {
+    ctr[0] = 0u;
+    ctr[1] = 0u;
+  }
 }
 
 template <typename T, int HD>
@@ -375,7 +397,7 @@ __global__ void k_attn_combine(const int32_t* __restrict__ row_ctx, int Hl,
 template <typename T, int HD>
 static int attn_launch(const void* q, const fl_row* rows, const int32_t* row_ctx, int M, int Hl,
                        const void* kv_layer, int S, int kps, void* out, float* ws_o, float* ws_ml,
-                       const int32_t* order, int ldo, cudaStream_t s) {
+                       const int32_t* order, int ldo, cudaStream_t s, unsigned* ctr) {
   using Cfg = AttnCfg<T, HD>;
   static int num_sms = 0;
   if (!num_sms) {
@@ -390,7 +412,7 @@ static int attn_launch(const void* q, const fl_row* rows, const int32_t* row_ctx
   const int per_sm = ATT_CW >= 8 ? 1 : 2;
   const int grid = items < per_sm * num_sms ? items : per_sm * num_sms;
   launch_k(k_attn_tma<T, HD>, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM, s, 1, (const T*)q, rows,
-           row_ctx, M, Hl, (const T*)kv_layer, S, (T*)out, ws_o, ws_ml, ms, kps, splits, order, ldo);
+           row_ctx, M, Hl, (const T*)kv_layer, S, (T*)out, ws_o, ws_ml, ms, kps, splits, order, ldo, ctr);
   if (splits > 1) {
     launch_k(k_attn_combine<T, HD>, dim3(Hl, M), dim3(HD < 128 ? HD : 128), 0, s, 1, row_ctx, Hl,
              ws_o, ws_ml, ms, kps, (T*)out, ldo);
@@ -434,16 +456,16 @@ void launch_row_order(const int32_t* row_ctx, int M, int32_t* order, cudaStream_
 
 int launch_attention(const void* q, const fl_row* rows, const int32_t* row_ctx, int M, int Hl,
                      int hd, const void* kv_layer, int C, int S, int kps, void* out, float* ws_o,
-                     float* ws_ml, int dtype, cudaStream_t s, const int32_t* order, int ldo) {
+                     float* ws_ml, int dtype, cudaStream_t s, const int32_t* order, int ldo, unsigned* ctr) {
   if (ldo <= 0) ldo = Hl * hd;
   if (M <= 0) return 0;
 #define FL_ATT(HDV)                                                                          \
   case HDV:                                                                                  \
     return dtype == FL_DTYPE_BF16                                                            \
                ? attn_launch<bf16, HDV>(q, rows, row_ctx, M, Hl, kv_layer, S, kps, out, ws_o, \
-                                        ws_ml, order, ldo, s)                                \
+                                        ws_ml, order, ldo, s, ctr)                           \
                : attn_launch<float, HDV>(q, rows, row_ctx, M, Hl, kv_layer, S, kps, out,      \
-                                         ws_o, ws_ml, order, ldo, s);
+                                         ws_o, ws_ml, order, ldo, s, ctr);
   switch (hd) {
     FL_ATT(64)
     FL_ATT(96)

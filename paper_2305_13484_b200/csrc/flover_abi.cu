@@ -102,6 +102,7 @@ struct fl_handle {
   char* plan_ws;
   std::vector<char> plan_stage;           // host staging of the window arrays
   float *x, *y, *logits, *att_o, *att_ml;
+  unsigned* att_ctr;                      // attention's dynamic item counters (self re-arming)
   void *h, *h2, *qkv, *q, *a, *f;
   unsigned long long* keys;
   fl::TcWorkspace tcws;
@@ -203,7 +204,7 @@ struct Carve {
 };
 
 struct Layout {
-  size_t rows, row_tok, row_pos, row_ctx, row_order, moves, plan, x, y, logits, att_o, att_ml, h, h2, qkv, q, a, f,
+  size_t rows, row_tok, row_pos, row_ctx, row_order, moves, plan, x, y, logits, att_o, att_ml, att_ctr, h, h2, qkv, q, a, f,
       keys, tc, total;
 };
 
@@ -249,6 +250,7 @@ Layout plan(const fl_model_desc* m, const fl_pool_desc* p) {
   L.logits = c.take(Md * Vl * 4);
   L.att_o = c.take(Mr * Hl * ms * m->head_dim * 4);
   L.att_ml = c.take(Mr * Hl * ms * 2 * 4);
+  L.att_ctr = c.take(256);
   L.h = c.take(Mr * d * es);
   L.h2 = c.take(m->family == FL_FAMILY_NEOX ? Mr * d * es : 0);
   // q|k|v, the attention output a and the FFN activation f share rows:
@@ -316,6 +318,11 @@ int fl_create(const fl_model_desc* m, const fl_pool_desc* p, fl_handle** out) {
   h->logits = (float*)(w + L.logits);
   h->att_o = (float*)(w + L.att_o);
   h->att_ml = (float*)(w + L.att_ml);
+  h->att_ctr = (unsigned*)(w + L.att_ctr);
+  if (cudaMemset(h->att_ctr, 0, 256) != cudaSuccess) {
+    delete h;
+    return fail(FL_ECUDA, "attention counters: %s", cudaGetErrorString(cudaGetLastError()));
+  }
   h->h = w + L.h;
   h->h2 = w + L.h2;
   h->qkv = w + L.qkv;
@@ -544,7 +551,8 @@ int enqueue_step(fl_handle* h, int n_rows, int n_dec, bool want_logits, cudaStre
       ProfScope ps(h, FL_PROF_ATTENTION, s);
       fl::g_launches += fl::launch_attention(h->q, h->rows, h->row_ctx, n_rows, Hl, hd, kvl,
                                              p.pool_slots, p.max_seq, att_keys, h->a, h->att_o,
-                                             h->att_ml, dt, s, ordered ? h->row_order : nullptr, h->ldaf);
+                                             h->att_ml, dt, s, ordered ? h->row_order : nullptr, h->ldaf,
+                                             h->att_ctr);
     }
     fl::g_launches += 1;
     // K5 attn-out (+ all-reduce); merged into K7 for parallel-residual models
@@ -805,7 +813,7 @@ extern "C" int fl_gemm(const void* x, int ldx, const void* w, const void* bias, 
 
 extern "C" size_t fl_attention_workspace_bytes(int M, int Hl, int hd, int S) {
   const size_t ms = fl::attn_max_splits(S);
-  return align256((size_t)M * Hl * ms * hd * 4) + align256((size_t)M * Hl * ms * 2 * 4);
+  return align256((size_t)M * Hl * ms * hd * 4) + align256((size_t)M * Hl * ms * 2 * 4) + 256;
 }
 
 extern "C" int fl_attention(const void* q, const fl_row* rows, const int32_t* row_ctx, int M, int Hl,
@@ -818,9 +826,15 @@ extern "C" int fl_attention(const void* q, const fl_row* rows, const int32_t* ro
   float* ws_o = static_cast<float*>(workspace);
   float* ws_ml = reinterpret_cast<float*>(static_cast<char*>(workspace) +
                                           align256((size_t)M * Hl * ms * hd * 4));
+  // the item counters follow the partials; the caller's scratch is not
+  // zeroed, so arm them on the stream (diagnostic entry)
+  unsigned* ctr = reinterpret_cast<unsigned*>(static_cast<char*>(workspace) +
+                                              align256((size_t)M * Hl * ms * hd * 4) +
+                                              align256((size_t)M * Hl * ms * 2 * 4));
+  FL_CUDA(cudaMemsetAsync(ctr, 0, 8, static_cast<cudaStream_t>(stream)));
   fl::launch_attention(q, rows, row_ctx, M, Hl, hd, kv_layer, C, S,
                        fl::attn_keys_per_split(M * Hl, S), out, ws_o, ws_ml, dtype,
-                       static_cast<cudaStream_t>(stream));
+                       static_cast<cudaStream_t>(stream), nullptr, 0, ctr);
   FL_CUDA(cudaGetLastError());
   return FL_OK;
 }

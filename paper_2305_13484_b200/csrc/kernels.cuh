@@ -68,10 +68,12 @@ int attn_max_splits(int S);
 // keys per split: one split per (row, head) when rows*heads fill the GPU.
 int attn_keys_per_split(int row_heads, int S);
 // returns the number of kernels launched (1 or 2)
+// ctr: two zero-initialised device counters (item claims, finished CTAs);
+// the kernel re-arms them, so one pair per stream of launches suffices
 int launch_attention(const void* q, const fl_row* rows, const int32_t* row_ctx, int M, int Hl,
                      int hd, const void* kv_layer, int C, int S, int keys_per_split, void* out,
-                     float* ws_o, float* ws_ml, int dtype, cudaStream_t s,
-                     const int32_t* order = nullptr, int ldo = 0);
+                     float* ws_o, float* ws_ml, int dtype, cudaStream_t s, const int32_t* order,
+                     int ldo, unsigned* ctr);
 // order[i] = row of rank i by descending context (attention's snake schedule)
 void launch_row_order(const int32_t* row_ctx, int M, int32_t* order, cudaStream_t s);
 
