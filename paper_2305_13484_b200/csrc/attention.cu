@@ -147,6 +147,7 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
   __shared__ __align__(8) uint64_t q_full[QD];
   __shared__ __align__(8) uint64_t q_empty[QD];
 
+  pdl_trigger();    // the successor launches now; its griddepcontrol.wait waits for this grid
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
@@ -160,7 +161,6 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  pdl_trigger();
   pdl_wait();       // q, row_ctx and this step's K/V rows come from predecessors
 
   const int n_items = M * Hl * splits;

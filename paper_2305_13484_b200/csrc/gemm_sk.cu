@@ -82,6 +82,11 @@ FL_DEV bool mbar_try(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 // one waiting thread with back-off (keeps the MIO queue free for the others)
+FL_DEV unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 FL_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
   while (!mbar_try(bar, parity)) __nanosleep(40);
 }
@@ -498,6 +503,10 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned long long g_start = 0;
   if (P.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
+  // let the next kernel's CTAs launch (and run their prologue) now: it only
+  // launches once every CTA of this grid has started, and its
+  // griddepcontrol.wait still waits for this grid's completion
+  pdl_trigger();
   const int xi = blockIdx.x & 1;                 // position in the pair (cluster rank)
   const int pair = blockIdx.x >> 1;              // pair id = work range
   const bool leader = xi == 0;
@@ -510,15 +519,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
   const int stages = P.stages, kch = P.kch;
   const Ranges R = pair_ranges(P, pair);
   const int n0u = R.hi[0] - R.lo[0], nunits = n0u + R.hi[1] - R.lo[1];
-  // segments of this pair's work
-  int nseg = 0;
-  Seg last{0, 0, 0};
-  for (int r = 0; r < 2; ++r)
-    for (int u = R.lo[r]; u < R.hi[r];) {
-      last = seg_at(u, R.hi[r], kch);
-      u += last.khi - last.klo;
-      ++nseg;
-    }
+  if (P.dbg && threadIdx.x == 0) P.dbg[4 * 9216 + blockIdx.x * 4 + 0] = gtimer();
 
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_w)) : "memory");
@@ -538,11 +539,13 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
                  "r"(P.ncols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    if (P.dbg && lane == 0) P.dbg[4 * 9216 + blockIdx.x * 4 + 1] = gtimer();
   }
+  if (P.dbg && threadIdx.x == 0) P.dbg[4 * 9216 + blockIdx.x * 4 + 2] = gtimer();
   tc_fence_before();
   cluster_sync_all();
   tc_fence_after();
-  pdl_trigger();
+  if (P.dbg && threadIdx.x == 0) P.dbg[4 * 9216 + blockIdx.x * 4 + 3] = gtimer();
   const uint32_t tmem = tmem_base;
   const int acc_cols = P.mt * P.bn;
 
@@ -579,6 +582,8 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         }
         if (leader) mbar_expect_tx(&full_bar[st], my_tx);
         if (P.dbg && role < 0) issue_clk[st] = clock64();
+        if (P.dbg && role == 0 && u < 32 + R.lo[0] && u >= R.lo[0]) P.dbg[4 * 12288 + blockIdx.x * 32 + (u - R.lo[0])] = gtimer();
+        if (P.dbg && role < 0 && u < 32 + R.lo[0] && u >= R.lo[0]) P.dbg[4 * 14336 + blockIdx.x * 32 + (u - R.lo[0])] = gtimer();
         if (role < 0 && KPB > 1 && P.w_tiled)
           tma_load_pair(&tma_w, &full_bar[st], smem + st * STAGE, 0, wrow);   // 2 chunks, 32 KB contiguous
         else if (role < 0 && KPB > 1)
@@ -618,6 +623,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       };
       const int pre = min(nunits, stages);
       if (role >= 0) pdl_wait();            // activations are the predecessor's output
+      if (P.dbg && role == 0) P.dbg[4 * (8192 + blockIdx.x) + 0] = gtimer();
       for (int i = 0; i < pre; ++i) issue(unit(i), i);   // weights stream ahead of the wait
       if (role == -1 && P.l2_ahead > 0)
         for (int i = pre; i < min(nunits, pre + P.l2_ahead); ++i) prefetch(unit(i));
@@ -657,6 +663,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         for (int c = klo; c < khi; ++c) {
           tw = P.dbg ? clock64() : 0;
           mbar_wait(&full_bar[s], ph);
+          if (P.dbg && nlat < 32) P.dbg[4 * 10240 + blockIdx.x * 32 + nlat] = gtimer();
           if (P.dbg) {
             const unsigned long long now = clock64();
             waited += now - tw;
@@ -700,6 +707,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         ++seg;
       }
       if (P.dbg && lane == 0) {
+        P.dbg[4 * (8192 + blockIdx.x) + 1] = gtimer();
         P.dbg[4 * blockIdx.x + 2] = waited;
         P.dbg[4 * blockIdx.x + 3] = clock64() - t_start;
         P.dbg[4 * (2048 + blockIdx.x) + 0] = twait;
@@ -848,8 +856,9 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
       if (warp == 2 && lane == 0) mbar_wait_sleep(&tfull_bar[b], use & 1);
       epi_bar();
       if (P.dbg) e_wait += clock64() - tw0;
+      if (P.dbg && warp == 2 && lane == 0 && seg == 0) P.dbg[4 * (8192 + blockIdx.x) + 2] = gtimer();
       tc_fence_after();
-      if (P.dbg_skip_epi == 1 || (P.dbg_skip_epi == 2 && seg == nseg - 1)) {   // diagnostic: skip epilogue work
+      if (P.dbg_skip_epi == 1) {   // diagnostic: skip epilogue work
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(&tempty_bar[b], prank);
@@ -973,6 +982,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(P.ncols));
+    if (P.dbg && threadIdx.x == 32) P.dbg[4 * (8192 + blockIdx.x) + 3] = gtimer();
   }
 }
 

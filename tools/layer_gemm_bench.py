@@ -1,6 +1,6 @@
 """GEMM-only replay of one fused GPT-J decode step with cold weights.
 
-    python tools/layer_gemm_bench.py [M ...]
+    python tools/layer_gemm_bench.py [M ...]      (MODEL=gpt2: the C2 shapes)
 
 28 layers x (QKV store, attn-out residual-add, FFN-up GELU, FFN-down
 residual-add) + the LM head with the fused greedy argmax, each layer with its
@@ -16,8 +16,13 @@ from paper_2305_13484_b200 import _lib
 
 lib = _lib.load()
 lib.fl_gemm_set_rearm(0)   # one workspace for every call: the flags self-reset
+for kv in filter(None, (os.environ.get("TUNE") or "").split(",")):   # diagnostics: fl_gemm_tune key=value
+    k, v = kv.split("=")
+    lib.fl_gemm_tune(int(k), int(v))
 ws = torch.empty(lib.fl_gemm_workspace_bytes(), dtype=torch.uint8, device="cuda")
 L, d, F, V = 28, 4096, 16384, 50400
+if os.environ.get("MODEL") == "gpt2":     # C2 shapes (GPT-2 small)
+    L, d, F, V = 12, 768, 3072, 50257
 g = torch.Generator(device="cuda").manual_seed(0)
 W = [[(torch.randn(n, k, device="cuda", generator=g) * 0.02).bfloat16() for n, k in
       ((3 * d, d), (d, d), (F, d), (d, F))] for _ in range(L)]
@@ -91,7 +96,7 @@ for M in Ms:
         res.append(f"{name} {1e3 * ms / L:7.1f} us/layer ({tf:5.0f} TF/s, {gb:5.0f} GB/s weights)")
     print(f"{ONLY or 'all'} M={M:4d}  " + "   ".join(res), flush=True)
     if os.environ.get("GEMM_DBG"):
-        dbg = torch.zeros(4 * 8192, dtype=torch.int64, device="cuda")
+        dbg = torch.zeros(4 * 16384, dtype=torch.int64, device="cuda")
         lib.fl_gemm_debug(C.c_void_p(dbg.data_ptr())); ours(); torch.cuda.synchronize(); lib.fl_gemm_debug(None)
         dd = dbg.view(-1, 4).cpu().double()
         p = dd[:2048][dd[:2048, 1] > 0]
@@ -106,3 +111,25 @@ for M in Ms:
               f" mma full-waits {100*m[:,2].sum()/max(m[:,3].sum(),1):.0f}% of {m[:,3].mean():.0f} clk; issue->full {lat.mean():.0f} clk;"
               f" CTA start spread {(e[:,0].max()-t0)/1e3:.1f} us, end {(e[:,1].min()-t0)/1e3:.1f}..{(e[:,1].max()-t0)/1e3:.1f} us;"
               f" tfull-wait {e[:,2].mean():.0f} clk, epi total {e[:,3].mean():.0f} clk", flush=True)
+        t = dd[8192:8192 + 2048]
+        ok2 = (t[:, 3] > 0) & (dd[4096:6144, 0] > 0)
+        g0 = dd[4096:6144, 0][ok2]
+        T0 = g0.min()
+        tl = t[ok2]
+        def rng(v):
+            v = v[v > 0] - T0
+            return f"{v.min()/1e3:.2f}..{v.max()/1e3:.2f}" if len(v) else "-"
+        print(f"   timeline us (from first CTA start): start {rng(g0)} | X after pdl_wait {rng(tl[:,0])} |"
+              f" last MMA {rng(tl[:,1])} | epi got acc {rng(tl[:,2])} | epi end {rng(dd[4096:6144,1][ok2])} |"
+              f" dealloc {rng(tl[:,3])}", flush=True)
+        raw = dbg.view(-1).cpu().double()
+        for b in range(0, 4, 2):
+            fulls = raw[4 * 10240 + b * 32: 4 * 10240 + b * 32 + 32]
+            xs = raw[4 * 12288 + b * 32: 4 * 12288 + b * 32 + 32]
+            ws_ = raw[4 * 14336 + b * 32: 4 * 14336 + b * 32 + 32]
+            f = lambda v: " ".join(f"{(x - T0) / 1e3:.2f}" for x in v.tolist() if x > 0)
+            print(f"   CTA {b}: W issue [{f(ws_)}]\n          X issue [{f(xs)}]\n          full    [{f(fulls)}]", flush=True)
+        e6 = dd[6144:8192][ok2]
+        print(f"   epi clk means: wait {e[:, 2].mean():.0f} flag {e6[:, 0].mean():.0f} blk {e6[:, 1].mean():.0f} post {e6[:, 2].mean():.0f} ld {e6[:, 3].mean():.0f}", flush=True)
+        pro = raw[4 * 9216: 4 * 9216 + 4 * 148].view(-1, 4)[ok2[:148]]
+        print(f"   prologue: ranges {rng(pro[:,0])} | alloc {rng(pro[:,1])} | init {rng(pro[:,2])} | cluster sync {rng(pro[:,3])}", flush=True)

@@ -10,7 +10,7 @@ __device__ __forceinline__ uint64_t desc_sw128(const void* tile) {
   uint64_t a = smem_u32(tile);
   return ((a >> 4) & 0x3FFF) | (1ull << 16) | ((1024ull >> 4) << 32) | (1ull << 46) | (2ull << 61);
 }
-__global__ void probe(int n_mma, int N, unsigned long long* out, const uint8_t* g, int tma_on) {
+__global__ void probe(int n_mma, int N, unsigned long long* out, const uint8_t* g, int tma_on, int nacc) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ uint32_t tmem_base;
@@ -53,8 +53,8 @@ __global__ void probe(int n_mma, int N, unsigned long long* out, const uint8_t* 
       const int st = (i >> 2) % nst;
       uint64_t ad = desc_sw128(smem + st * stage_b), bd = desc_sw128(smem + st * stage_b + 16384);
       asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                   "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_base),
-                   "l"(ad + 2 * k), "l"(bd + 2 * k), "r"(idesc), "r"(i));
+                   "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_base + (i % nacc) * N),
+                   "l"(ad + 2 * k), "l"(bd + 2 * k), "r"(idesc), "r"((int)(i >= nacc)));
     }
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)));
     asm volatile("{\n\t.reg .pred d;\nW:\n\tmbarrier.try_wait.parity.shared::cta.b64 d, [%0], 0;\n\t@!d bra W;\n\t}" ::"r"(smem_u32(&bar)));
@@ -70,16 +70,19 @@ int main() {
   cudaMalloc(&d, 8 * 148);
   uint8_t* g; cudaMalloc(&g, (size_t)4096 * 16384);
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
-  for (int N : {16, 32, 64, 128, 256}) {
-    for (int grid : {1, 148}) {
+  for (int N : {16, 32, 64, 128}) {
+    for (int grid : {1}) {
      for (int tma_on : {0, 2}) {
-      probe<<<grid, 128, 210 * 1024>>>(4096, N, d, g, tma_on);
+      for (int nacc : {1, 2, 4}) {
+      if (nacc * N > 256) continue;
+      probe<<<grid, 128, 210 * 1024>>>(4096, N, d, g, tma_on, nacc);
       cudaDeviceSynchronize();
       unsigned long long h[148];
       cudaMemcpy(h, d, 8 * grid, cudaMemcpyDeviceToHost);
       double avg = 0; for (int i = 0; i < grid; ++i) avg += h[i]; avg /= grid;
-      printf("N=%3d grid=%3d tma=%d: %.1f cycles per MMA (floor %d)  err=%s\n", N, grid, tma_on, avg / 4096, 128 * N / 256,
+      printf("N=%3d grid=%3d tma=%d nacc=%d: %.1f cycles per MMA (floor %d)  err=%s\n", N, grid, tma_on, nacc, avg / 4096, 128 * N / 256,
              cudaGetErrorString(cudaGetLastError()));
+      }
      }
     }
   }

@@ -113,7 +113,7 @@ for M in Ms:
     if os.environ.get("GEMM_DBG"):
         # in-kernel clocks of the LAST GEMM of ours(): per CTA producer wait /
         # total, MMA full-barrier wait / total, mean weight issue -> full
-        dbg = torch.zeros(4 * 8192, dtype=torch.int64, device="cuda")
+        dbg = torch.zeros(4 * 16384, dtype=torch.int64, device="cuda")
         lib.fl_gemm_debug(C.c_void_p(dbg.data_ptr()))
         ours()
         torch.cuda.synchronize()
@@ -133,3 +133,18 @@ for M in Ms:
               f" CTA start spread {(e[:, 0].max() - t0) / 1e3:.1f} us, end {(e[:, 1].min() - t0) / 1e3:.1f}.."
               f"{(e[:, 1].max() - t0) / 1e3:.1f} us; epi tfull-wait {e[:, 2].mean():.0f} clk, epi total {e[:, 3].mean():.0f}",
               flush=True)
+        ok2 = (dd[8192:8192 + 2048, 3] > 0) & (dd[4096:6144, 0] > 0)
+        g0 = dd[4096:6144, 0][ok2]
+        T0 = g0.min()
+        tl = dd[8192:8192 + 2048][ok2]
+
+        def rng(v):
+            v = v[v > 0] - T0
+            return f"{v.min() / 1e3:.2f}..{v.max() / 1e3:.2f}" if len(v) else "-"
+        raw = dbg.view(-1).cpu().double()
+        pro = raw[4 * 9216: 4 * 9216 + 4 * 148].view(-1, 4)[ok2[:148]]
+        print(f"   timeline us: start {rng(g0)} | prologue done {rng(pro[:, 3])} | X after pdl_wait {rng(tl[:, 0])} |"
+              f" last MMA {rng(tl[:, 1])} | epi got acc {rng(tl[:, 2])} | epi end {rng(dd[4096:6144, 1][ok2])} |"
+              f" dealloc {rng(tl[:, 3])}", flush=True)
+        ends = (dd[4096:6144, 1][ok2] - T0) / 1e3
+        print("   epi end quantiles us: " + " ".join(f"{q:.2f}" for q in torch.quantile(ends, torch.tensor([0.0, 0.1, 0.5, 0.9, 1.0], dtype=ends.dtype)).tolist()), flush=True)
