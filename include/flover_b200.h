@@ -206,6 +206,10 @@ size_t fl_gemm_workspace_bytes(void);
 /* Diagnostics: when non-NULL, every tensor-core GEMM CTA b writes 4 clocks to
  * dev_counters[4b..4b+3]: producer wait, producer total, MMA wait, MMA total. */
 void fl_gemm_debug(unsigned long long* dev_counters);
+/* Diagnostics: when non-NULL, every attention CTA b writes %globaltimer stamps to
+ * dev_stamps[64b..64b+63]: [0] start, [1] after the grid dependency wait, then
+ * per item i < 31: [2+2i] the consumers got the item, [3+2i] its output written. */
+void fl_attention_debug(unsigned long long* dev_stamps);
 /* Diagnostic entry: K4 alone.  q [M, Hl*hd]; rows (device) give the slot of each
  * row, row_ctx (device) its context length; kv_layer is one layer of the pool
  * [C][2][Hl][S][hd]; out [M, Hl*hd].  workspace >= fl_attention_workspace_bytes. */

@@ -24,7 +24,7 @@ EXPORTS = ("fl_abi_version", "fl_last_error", "fl_workspace_bytes", "fl_create",
            "fl_comm_unique_id", "fl_comm_init", "fl_step", "fl_shuffle", "fl_kernel_launches",
            "fl_gemm_workspace_bytes", "fl_gemm", "fl_profile", "fl_profile_read", "fl_configure",
            "fl_last_duration_ms", "fl_attention_workspace_bytes", "fl_attention",
-           "fl_gemm_debug", "fl_plan_shuffle", "fl_tiled_weight_bytes", "fl_tile_weight",
+           "fl_gemm_debug", "fl_attention_debug", "fl_plan_shuffle", "fl_tiled_weight_bytes", "fl_tile_weight",
            "fl_set_merged_out", "fl_set_merged_in", "fl_gemm2", "fl_gemm_set_rearm", "fl_gemm_tune",
            "fl_set_side_stream", "fl_step_import", "fl_shuffle_planned")
 PROF_ATTENTION, PROF_GEMM, PROF_SHUFFLE, PROF_STEP = 0, 1, 2, 3
@@ -100,6 +100,8 @@ def load() -> C.CDLL:
                                     C.POINTER(C.c_double)]
     lib.fl_gemm_debug.argtypes = [C.c_void_p]
     lib.fl_gemm_debug.restype = None
+    lib.fl_attention_debug.argtypes = [C.c_void_p]
+    lib.fl_attention_debug.restype = None
     lib.fl_attention_workspace_bytes.restype = C.c_size_t
     lib.fl_attention_workspace_bytes.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int]
     lib.fl_attention.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int,

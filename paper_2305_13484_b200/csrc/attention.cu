@@ -26,6 +26,14 @@ constexpr int ATT_THREADS = 128;
 #define ATT_TILE_BYTES 0   // 0: per head_dim (AttnCfg::TKB); A/B builds override
 #endif
 
+__device__ unsigned long long* g_att_dbg = nullptr;   // fl_attention_debug
+void attn_set_debug(unsigned long long* p) { cudaMemcpyToSymbol(g_att_dbg, &p, sizeof(p)); }
+FL_DEV unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 int attn_max_splits(int S) { return (S + ATT_CHUNK - 1) / ATT_CHUNK; }
 
 template <int X> struct NextPow2 {
@@ -143,11 +151,14 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
   // order): the producer claims the next item and passes it to the consumers
   // through a small smem queue -- a CTA that runs fast takes more items
   constexpr int QD = 4;
-  __shared__ int q_item[QD];
+  __shared__ int q_item[QD][4];                       // item, row, head, context
+  __shared__ __align__(16) T q_s[QD][HD];             // the item's query (bulk copy)
   __shared__ __align__(8) uint64_t q_full[QD];
   __shared__ __align__(8) uint64_t q_empty[QD];
 
   pdl_trigger();    // the successor launches now; its griddepcontrol.wait waits for this grid
+  unsigned long long* const dbg = g_att_dbg ? g_att_dbg + 64 * blockIdx.x : nullptr;
+  if (dbg && threadIdx.x == 0) dbg[0] = gtime();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
@@ -185,9 +196,19 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
           k0 = sp * keys_per_split;
           if (k0 >= ctx) continue;            // a split past this row's context: no work
         }
+        // the consumers get the item's indices and its query through the
+        // queue slot: no dependent global loads on their side per item
         mbar_wait_(&q_empty[qs], qph ^ 1);
-        q_item[qs] = item;
-        mbar_arrive_(&q_full[qs]);
+        q_item[qs][0] = item;
+        q_item[qs][1] = r;
+        q_item[qs][2] = h;
+        q_item[qs][3] = ctx;
+        if (item >= 0) {
+          mbar_expect_tx_(&q_full[qs], HD * sizeof(T));
+          bulk_g2s(q_s[qs], q + static_cast<size_t>(r) * D + h * HD, HD * sizeof(T), &q_full[qs]);
+        } else {
+          mbar_arrive_(&q_full[qs]);
+        }
         if (++qs == QD) { qs = 0; qph ^= 1; }
         if (item < 0) break;
         const int k1 = min(ctx, k0 + keys_per_split);
@@ -213,37 +234,40 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
   const int kw = lane / G;          // key group within the warp
 
   const float scale = rsqrtf(static_cast<float>(HD));
+  int n_done = 0;   // items finished (diagnostic stamps)
   int st = 0, qs = 0;
   uint32_t ph = 0, qph = 0;
   for (;;) {
     mbar_wait_(&q_full[qs], qph);
-    const int item = q_item[qs];
+    if (dbg && threadIdx.x == 0) {
+      if (n_done == 0) dbg[1] = gtime();
+      if (n_done < 31) dbg[2 + 2 * n_done] = gtime();
+    }
+    const int item = q_item[qs][0];
+    const int r = q_item[qs][1], h = q_item[qs][2], ctx = q_item[qs][3];
+    float qv[PER][VEC], acc[PER][VEC];
+    if (item >= 0) {
+#pragma unroll
+      for (int p = 0; p < PER; ++p) {
+        const int vi = g + p * G;
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) acc[p][j] = 0.f;
+        if (vi < NV) {
+          widen16<T>(*reinterpret_cast<const uint4*>(&q_s[qs][vi * VEC]), qv[p]);
+#pragma unroll
+          for (int j = 0; j < VEC; ++j) qv[p][j] *= scale;
+        }
+      }
+    }
     __syncwarp();
     if (lane == 0) mbar_arrive_(&q_empty[qs]);
     if (++qs == QD) { qs = 0; qph ^= 1; }
     if (item < 0) break;
     const int sp = item % splits;
-    const int rh = item / splits;
-    const int h = rh % Hl, r = order ? order[rh / Hl] : rh / Hl;
-    const int ctx = row_ctx[r];
     const int k0 = sp * keys_per_split;
-    if (k0 >= ctx) continue;
     const int k1 = min(ctx, k0 + keys_per_split);
     const int nsplit = (ctx + keys_per_split - 1) / keys_per_split;
 
-    float qv[PER][VEC], acc[PER][VEC];
-    const T* qr = q + static_cast<size_t>(r) * D + h * HD;
-#pragma unroll
-    for (int p = 0; p < PER; ++p) {
-      const int vi = g + p * G;
-#pragma unroll
-      for (int j = 0; j < VEC; ++j) acc[p][j] = 0.f;
-      if (vi < NV) {
-        load16(qr + vi * VEC, qv[p]);
-#pragma unroll
-        for (int j = 0; j < VEC; ++j) qv[p][j] *= scale;
-      }
-    }
     float m = -INFINITY, l = 0.f;
 
     for (int t0 = k0; t0 < k1; t0 += TK) {
@@ -364,6 +388,8 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
       }
     }
     asm volatile("bar.sync 1, %0;" ::"n"(CW * 32) : "memory");   // merge buffers reused
+    if (dbg && threadIdx.x == 0 && n_done < 31) dbg[3 + 2 * n_done] = gtime();
+    ++n_done;
   }
   // this CTA's producer claimed its last item before it sent the sentinel:
   // the last CTA to finish re-arms the item counter for the next launch

@@ -768,6 +768,8 @@ extern "C" void fl_gemm_tune(int key, int value) {
 
 extern "C" size_t fl_gemm_workspace_bytes(void) { return fl::tc_workspace_bytes(0, 0); }
 extern "C" void fl_gemm_debug(unsigned long long* dev_counters) { fl::tc_set_debug(dev_counters); }
+namespace fl { void attn_set_debug(unsigned long long* p); }
+extern "C" void fl_attention_debug(unsigned long long* dev_stamps) { fl::attn_set_debug(dev_stamps); }
 
 extern "C" int fl_gemm2(const void* x, const void* x2, int ldx, const void* w, const void* bias, void* out,
                         int ldo, int M, int N, int K, int epi, int dtype, int use_tc, int nsplit, int ogap,

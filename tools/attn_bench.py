@@ -17,6 +17,8 @@ g = torch.Generator(device="cuda").manual_seed(0)
 kv = torch.randn((M, 2, H, S, hd), device="cuda", generator=g).bfloat16()
 q = torch.randn((M, H * hd), device="cuda", generator=g).bfloat16()
 ctx = torch.randint(32, S + 1, (M,), device="cuda", generator=g, dtype=torch.int32)
+if os.environ.get("ORDER"):      # rows by descending context, as the step's row_order ranks them
+    ctx = ctx.sort(descending=True).values.contiguous()
 rows = torch.zeros((M, 6), dtype=torch.int32, device="cuda")
 rows[:, 0] = torch.arange(M, dtype=torch.int32)
 out = torch.empty_like(q)
@@ -44,3 +46,30 @@ e1.record(); torch.cuda.synchronize()
 us = e0.elapsed_time(e1) * 1e3 / R
 byt = int(ctx.sum()) * 2 * H * hd * 2 + M * 2 * H * hd * 2
 print(f"attention M={M} hd={hd} H={H}: {us:.1f} us, {byt/1e6:.1f} MB, {byt/us/1e3:.0f} GB/s, max err {ref_err:.3e}")
+if os.environ.get("ATT_DBG"):
+    # per-CTA %globaltimer stamps of one launch (fl_attention_debug)
+    nb = 2 * 148
+    dbg = torch.zeros(64 * nb, dtype=torch.int64, device="cuda")
+    lib.fl_attention_debug(C.c_void_p(dbg.data_ptr()))
+    run()
+    torch.cuda.synchronize()
+    lib.fl_attention_debug(None)
+    d = dbg.view(nb, 64).cpu().double()
+    d = d[d[:, 0] > 0]
+    T0 = d[:, 0].min()
+    starts, pdl = (d[:, 0] - T0) / 1e3, (d[:, 1] - T0) / 1e3
+    items, gaps, firsts, ends, counts = [], [], [], [], []
+    for row in d:
+        st = [(row[2 + 2 * i] - T0) / 1e3 for i in range(31) if row[3 + 2 * i] > 0]
+        en = [(row[3 + 2 * i] - T0) / 1e3 for i in range(31) if row[3 + 2 * i] > 0]
+        counts.append(len(st))
+        if st:
+            firsts.append(st[0])
+            ends.append(en[-1])
+        items += [e - s for s, e in zip(st, en)]
+        gaps += [st[i + 1] - en[i] for i in range(len(st) - 1)]
+    q = lambda v: "min %.2f med %.2f max %.2f" % (min(v), sorted(v)[len(v) // 2], max(v)) if v else "-"
+    print(f"   CTAs {len(d)}: start {q(starts.tolist())} | dep wait done {q(pdl.tolist())} | first item {q(firsts)} |"
+          f" end {q(ends)}")
+    print(f"   items/CTA {q(counts)} | item us {q(items)} (mean {sum(items) / max(len(items), 1):.2f}) |"
+          f" gap between items {q(gaps)} (mean {sum(gaps) / max(len(gaps), 1):.2f})", flush=True)

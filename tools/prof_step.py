@@ -28,6 +28,10 @@ reqs = [fl.Request(i, 1, cfg["input_len"], cfg["max_out"], cfg["max_out"], 0.0) 
 prompts = fl.synthetic_prompts(reqs, spec.vocab, 1)
 ex = CudaExecutor(spec, prompts, dtype=cfg["dtype"], pool_slots=max(a.rows, 8), input_len=cfg["input_len"],
                   max_new_tokens=cfg["max_out"], state_slots=1024, max_rows=max(a.rows, 8) + 256)
+# TUNE="7=1,...": fl_gemm_tune diagnostics for every graph this run captures (results garbage, timing valid)
+for kv in filter(None, (os.environ.get("TUNE") or "").split(",")):
+    k, v = kv.split("=")
+    ex.lib.fl_gemm_tune(int(k), int(v))
 st = fl.FusionStream(reqs, fl.CostParams(preprocess_ms=0.0), fl.TPConfig(), executor=ex, record_tokens=False)
 torch.cuda.set_stream(ex.cs)
 st.try_fuse_pending()
