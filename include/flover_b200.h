@@ -235,7 +235,10 @@ void fl_gemm_set_rearm(int on);
 /* Tuning studies only (tools/): key 0 = programmatic dependent launch (1 on,
  * 0 off) for every kernel launched afterwards; keys 1-4 override the GEMM's
  * work decomposition (max pairs, ring stages, K sub-chunks per unit, minimum
- * units per stream-K range); -1 restores the built-in choice. */
+ * units per stream-K range); 5 span cap; 6-8 diagnostic switches (no loads /
+ * no MMAs / no epilogue: garbage results); 9 = 1: fl_gemm_debug launches
+ * alternate between two 64 K-entry halves of the buffer; -1 restores the
+ * built-in choice. */
 void fl_gemm_tune(int key, int value);
 
 /* Parallel-residual families (gptj, neox): run the attention output projection

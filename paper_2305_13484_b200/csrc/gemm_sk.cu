@@ -57,7 +57,7 @@ thread_local std::string g_sk_err;
 // diagnostic overrides (fl_gemm_tune; -1 = the built-in choice): 1 max pairs,
 // 2 ring stages, 3 K sub-chunks per unit, 4 min units per stream-K range,
 // 5 tokens per token tile (span cap, <= 512)
-int g_tune[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
+int g_tune[10] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
 int g_l2_ahead = -1;                      // fl_gemm_tune key 8 (L2 prefetch depth / diagnostics)
 unsigned long long* g_sk_dbg = nullptr;
 
@@ -1049,7 +1049,7 @@ size_t sk_workspace_bytes() {
 
 const char* sk_last_error() { return g_sk_err.c_str(); }
 void sk_tune(int key, int value) {
-  if (key >= 1 && key < 8) g_tune[key] = value;
+  if (key >= 1 && key < 10) g_tune[key] = value;
   if (key == 8) g_l2_ahead = value;
 }
 void sk_set_debug(unsigned long long* p) { g_sk_dbg = p; }
@@ -1239,7 +1239,10 @@ int gemm_sk(void* ws, int num_sms, const GemmArgs& a, cudaStream_t s) {
   P.part = static_cast<float*>(ws);
   P.slot_elems = SK_MAX_SPAN * SK_BM;
   P.flags = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + (size_t)SK_MAX_PAIRS * 2 * SK_MAX_SPAN * SK_BM * 4);
-  P.dbg = g_sk_dbg;
+  // diagnostics (key 9 = 1): consecutive launches alternate between two
+  // 64 K-entry halves of the buffer, so a tool sees a launch and its predecessor
+  static unsigned dbg_flip = 0;
+  P.dbg = g_sk_dbg && g_tune[9] == 1 ? g_sk_dbg + (dbg_flip++ & 1u) * (4 * 16384) : g_sk_dbg;
   P.dbg_skip_x = g_tune[6] == 1 || g_tune[6] == 2 ? g_tune[6] : 0;   // 2: no weight loads either
   P.dbg_skip_mma = g_tune[7] == 1 ? 1 : 0;   // (key 7 >= 10: TMEM buffer count - 10)
   // key 8 >= 0: L2 prefetch depth (measured: 4..32 units slow every M, so 0);

@@ -46,11 +46,41 @@ __global__ void k_chain(int flags, int clustered_unused, float* sink) {
   if (flags & 4) asm volatile("griddepcontrol.launch_dependents;");
 }
 
+// a distinct kernel with the same body (alternation = a different function each launch)
+template <int CL>
+__global__ void k_chain_b(int flags, int clustered_unused, float* sink) {
+  constexpr bool clustered = CL != 0;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint32_t tmem_base;
+  if (!(flags & 4)) asm volatile("griddepcontrol.launch_dependents;");
+  const int warp = threadIdx.x >> 5;
+  if ((flags & 1) && warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(sa(&tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  if ((flags & 2) && clustered)
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  else
+    __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (threadIdx.x == 0 && blockIdx.x == 0) sink[1] += 1.f;
+  if ((flags & 2) && clustered)
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  else
+    __syncthreads();
+  if ((flags & 1) && warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 64;" ::"r"(tmem_base));
+}
+
+static int g_alt = 0, g_smem_b = 0;   // alternate with k_chain_b (its dynamic smem)
+
 static float run(int grid, int threads, int smem, int clustered, int flags, int pdl, float* sink) {
   cudaStream_t s;
   cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
   cudaFuncSetAttribute(k_chain<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_chain<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_chain_b<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  int li = 0;
   const int n = 200;
   auto launch = [&]() {
     cudaLaunchConfig_t cfg = {};
@@ -74,7 +104,10 @@ static float run(int grid, int threads, int smem, int clustered, int flags, int 
     }
     cfg.attrs = at;
     cfg.numAttrs = na;
-    if (clustered) cudaLaunchKernelEx(&cfg, k_chain<1>, flags, clustered, sink);
+    const bool b = g_alt && (li++ & 1);
+    if (b) cfg.dynamicSmemBytes = g_smem_b;
+    if (b) cudaLaunchKernelEx(&cfg, k_chain_b<1>, flags, clustered, sink);
+    else if (clustered) cudaLaunchKernelEx(&cfg, k_chain<1>, flags, clustered, sink);
     else cudaLaunchKernelEx(&cfg, k_chain<0>, flags, clustered, sink);
   };
   cudaGraph_t g;
@@ -123,11 +156,17 @@ int main() {
       {"18x384, 200 KB, PDL, cluster 2 + barriers + TMEM 2-CTA", 18, 384, 200 * 1024, 1, 3, 1},
       {"288x256, no smem, PDL (LayerNorm-like)", 288, 256, 0, 0, 0, 1},
   };
+  for (int alt = 0; alt < 3; ++alt) {
+  g_alt = alt > 0;
+  g_smem_b = alt == 1 ? 200 * 1024 : 150 * 1024;
+  printf("---- %s\n", alt == 0 ? "same kernel" : alt == 1 ? "alternating kernels, same smem" : "alternating kernels, 200 / 150 KB smem");
   for (auto& v : vs) {
+    if (alt && !v.clustered) continue;
     printf("%-60s ", v.name);
     fflush(stdout);
     printf("%6.2f us per kernel\n", run(v.grid, v.threads, v.smem, v.clustered, v.flags, v.pdl, sink));
     fflush(stdout);
+  }
   }
   return 0;
 }

@@ -113,7 +113,9 @@ for M in Ms:
     if os.environ.get("GEMM_DBG"):
         # in-kernel clocks of the LAST GEMM of ours(): per CTA producer wait /
         # total, MMA full-barrier wait / total, mean weight issue -> full
-        dbg = torch.zeros(4 * 16384, dtype=torch.int64, device="cuda")
+        dbg2 = torch.zeros(2 * 4 * 16384, dtype=torch.int64, device="cuda")
+        dbg = dbg2[:4 * 16384]
+        lib.fl_gemm_tune(9, 1)    # alternate halves: the last two launches
         lib.fl_gemm_debug(C.c_void_p(dbg.data_ptr()))
         ours()
         torch.cuda.synchronize()
@@ -148,3 +150,19 @@ for M in Ms:
               f" dealloc {rng(tl[:, 3])}", flush=True)
         ends = (dd[4096:6144, 1][ok2] - T0) / 1e3
         print("   epi end quantiles us: " + " ".join(f"{q:.2f}" for q in torch.quantile(ends, torch.tensor([0.0, 0.1, 0.5, 0.9, 1.0], dtype=ends.dtype)).tolist()), flush=True)
+        # the last two launches (alternating halves): predecessor end -> successor start
+        halves = [dbg2[i * 4 * 16384:(i + 1) * 4 * 16384].view(-1, 4).cpu().double() for i in range(2)]
+        info = []
+        for hv in halves:
+            ok = (hv[4096:6144, 0] > 0) & (hv[8192:8192 + 2048, 3] > 0)
+            if ok.any():
+                info.append((hv[4096:6144, 0][ok].min(), hv[4096:6144, 0][ok].max(), hv[8192:8192 + 2048, 0][ok].max(),
+                             hv[4096:6144, 1][ok].max(), hv[8192:8192 + 2048, 3][ok].max(), int(ok.sum())))
+        if len(info) == 2:
+            info.sort()
+            a_, b_ = info
+            Z = a_[0]
+            f = lambda t: f"{(t - Z) / 1e3:.2f}"
+            print(f"   pair of launches (us from the first's first CTA): first [{a_[5]} CTAs] start {f(a_[0])}..{f(a_[1])},"
+                  f" X ready {f(a_[2])}, epi end {f(a_[3])}, last dealloc {f(a_[4])} | second [{b_[5]} CTAs] start"
+                  f" {f(b_[0])}..{f(b_[1])}, X ready {f(b_[2])}, epi end {f(b_[3])}, last dealloc {f(b_[4])}", flush=True)
