@@ -78,6 +78,36 @@ __global__ void __launch_bounds__(256) k_layernorm(const float* __restrict__ x,
                                                    const T* __restrict__ b, T* __restrict__ out,
                                                    int d, float eps) {
   pdl_trigger();
+  // gamma / beta are weights (never written by a predecessor): load them
+  // before the grid dependency wait, off the critical path
+  float gv[PER * 4], bv[PER * 4];
+#pragma unroll
+  for (int c = 0; c < PER; ++c) {
+    const int i = (c * blockDim.x + threadIdx.x) * 4;
+    if constexpr (sizeof(T) == 2) {   // 8-byte loads: 4 bf16
+      uint2 gr = make_uint2(0u, 0u), br = make_uint2(0u, 0u);
+      if (i < d) {
+        gr = *reinterpret_cast<const uint2*>(g + i);
+        br = *reinterpret_cast<const uint2*>(b + i);
+      }
+      const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gr);
+      const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&br);
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const float2 gf = __bfloat1622float2(g2[h2]), bf = __bfloat1622float2(b2[h2]);
+        gv[4 * c + 2 * h2] = gf.x;
+        gv[4 * c + 2 * h2 + 1] = gf.y;
+        bv[4 * c + 2 * h2] = bf.x;
+        bv[4 * c + 2 * h2 + 1] = bf.y;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        gv[4 * c + j] = i < d ? to_f(g[i + j]) : 0.f;
+        bv[4 * c + j] = i < d ? to_f(b[i + j]) : 0.f;
+      }
+    }
+  }
   pdl_wait();
   __shared__ float red[32];
   const int r = blockIdx.x;
@@ -111,22 +141,18 @@ __global__ void __launch_bounds__(256) k_layernorm(const float* __restrict__ x,
     const int i = (c * blockDim.x + threadIdx.x) * 4;
     if (i < d) {
       if constexpr (sizeof(T) == 2) {
-        // 8-byte gamma / beta loads and output stores (4 bf16 per thread)
-        const uint2 gr = *reinterpret_cast<const uint2*>(g + i), br = *reinterpret_cast<const uint2*>(b + i);
-        const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gr);
-        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&br);
+        // 8-byte output stores (4 bf16 per thread)
         __nv_bfloat162 y[2];
 #pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {
-          const float2 gf = __bfloat1622float2(g2[h2]), bf = __bfloat1622float2(b2[h2]);
-          y[h2] = __floats2bfloat162_rn((v[4 * c + 2 * h2] - mean) * rstd * gf.x + bf.x,
-                                        (v[4 * c + 2 * h2 + 1] - mean) * rstd * gf.y + bf.y);
-        }
+        for (int h2 = 0; h2 < 2; ++h2)
+          y[h2] = __floats2bfloat162_rn((v[4 * c + 2 * h2] - mean) * rstd * gv[4 * c + 2 * h2] + bv[4 * c + 2 * h2],
+                                        (v[4 * c + 2 * h2 + 1] - mean) * rstd * gv[4 * c + 2 * h2 + 1] +
+                                            bv[4 * c + 2 * h2 + 1]);
         *reinterpret_cast<uint2*>(o + i) = *reinterpret_cast<const uint2*>(y);
       } else {
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          o[i + j] = from_f<T>((v[4 * c + j] - mean) * rstd * to_f(g[i + j]) + to_f(b[i + j]));
+          o[i + j] = from_f<T>((v[4 * c + j] - mean) * rstd * gv[4 * c + j] + bv[4 * c + j]);
       }
     }
   }
