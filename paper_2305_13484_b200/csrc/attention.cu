@@ -40,10 +40,17 @@ template <int X> struct NextPow2 {
   static constexpr int v = X <= 1 ? 1 : X <= 2 ? 2 : X <= 4 ? 4 : X <= 8 ? 8 : X <= 16 ? 16 : 32;
 };
 
+// split rows' contexts (flash-decoding + combine) only below one item per
+// SM: between 148 and 296 (row, head) items the combine pass costs more than
+// the idle half of the second CTA slots (C3 at 16 rows 2836 -> 2772 us per
+// iteration; 64 loses at C2 8 rows: tools/prof_step.py)
+#ifndef ATT_SPLIT_BELOW
+#define ATT_SPLIT_BELOW 148
+#endif
 int attn_keys_per_split(int row_heads, int S) {
   const int full = attn_max_splits(S);
   int splits = 1;
-  if (row_heads < 2 * 148) splits = (2 * 148 + row_heads - 1) / row_heads;
+  if (row_heads < ATT_SPLIT_BELOW) splits = (2 * 148 + row_heads - 1) / row_heads;
   if (splits > full) splits = full;
   const int keys = (S + splits - 1) / splits;
   return (keys + ATT_CHUNK - 1) / ATT_CHUNK * ATT_CHUNK;
