@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
     const T* __restrict__ q, const fl_row* __restrict__ rows, const int32_t* __restrict__ row_ctx,
     int M, int Hl, const T* __restrict__ kv_layer, int S, T* __restrict__ out,
     float* __restrict__ ws_o, float* __restrict__ ws_ml, int max_splits, int keys_per_split,
-    int splits, const int32_t* __restrict__ order, int ldo, unsigned* __restrict__ ctr) {
+    int splits, const int4* __restrict__ meta, int ldo, unsigned* __restrict__ ctr) {
   using Cfg = AttnCfg<T, HD>;
   constexpr int VEC = Cfg::VEC, NV = Cfg::NV, G = Cfg::G, PER = Cfg::PER, KPW = Cfg::KPW;
   constexpr int CW = Cfg::CW, TK = Cfg::TK, STAGES = Cfg::STAGES, NP = CW;
@@ -190,16 +190,29 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
     if (lane == 0) {
       int st = 0, qs = 0;
       uint32_t ph = 0, qph = 0;
+      bool first = true;
       for (;;) {
-        int item = static_cast<int>(atomicAdd(ctr, 1u));
+        // CTA b starts with item b (the first round needs no atomic); later
+        // items come from the counter, offset by the grid
+        int item = first ? static_cast<int>(blockIdx.x) : static_cast<int>(gridDim.x + atomicAdd(ctr, 1u));
+        first = false;
         if (item >= n_items) item = -1;
         int sp = 0, h = 0, r = 0, ctx = 0, k0 = 0;
+        size_t slot = 0;
         if (item >= 0) {
           sp = item % splits;
           const int rh = item / splits;
           h = rh % Hl;
-          r = order ? order[rh / Hl] : rh / Hl;
-          ctx = row_ctx[r];
+          if (meta) {                          // rank -> (row, context, slot): one 16-byte load
+            const int4 m = meta[rh / Hl];
+            r = m.x;
+            ctx = m.y;
+            slot = static_cast<size_t>(m.z);
+          } else {
+            r = rh / Hl;
+            ctx = row_ctx[r];
+            slot = rows[r].slot;
+          }
           k0 = sp * keys_per_split;
           if (k0 >= ctx) continue;            // a split past this row's context: no work
         }
@@ -219,7 +232,6 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
         if (++qs == QD) { qs = 0; qph ^= 1; }
         if (item < 0) break;
         const int k1 = min(ctx, k0 + keys_per_split);
-        const size_t slot = rows[r].slot;
         const T* Kb = kv_layer + ((slot * 2 + 0) * Hl + h) * head_stride;
         const T* Vb = kv_layer + ((slot * 2 + 1) * Hl + h) * head_stride;
         for (int t0 = k0; t0 < k1; t0 += TK) {
@@ -430,7 +442,7 @@ __global__ void k_attn_combine(const int32_t* __restrict__ row_ctx, int Hl,
 template <typename T, int HD>
 static int attn_launch(const void* q, const fl_row* rows, const int32_t* row_ctx, int M, int Hl,
                        const void* kv_layer, int S, int kps, void* out, float* ws_o, float* ws_ml,
-                       const int32_t* order, int ldo, cudaStream_t s, unsigned* ctr) {
+                       const int4* meta, int ldo, cudaStream_t s, unsigned* ctr) {
   using Cfg = AttnCfg<T, HD>;
   static int num_sms = 0;
   if (!num_sms) {
@@ -445,7 +457,7 @@ static int attn_launch(const void* q, const fl_row* rows, const int32_t* row_ctx
   const int per_sm = ATT_CW >= 8 ? 1 : 2;
   const int grid = items < per_sm * num_sms ? items : per_sm * num_sms;
   launch_k(k_attn_tma<T, HD>, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM, s, 1, (const T*)q, rows,
-           row_ctx, M, Hl, (const T*)kv_layer, S, (T*)out, ws_o, ws_ml, ms, kps, splits, order, ldo, ctr);
+           row_ctx, M, Hl, (const T*)kv_layer, S, (T*)out, ws_o, ws_ml, ms, kps, splits, meta, ldo, ctr);
   if (splits > 1) {
     launch_k(k_attn_combine<T, HD>, dim3(Hl, M), dim3(HD < 128 ? HD : 128), 0, s, 1, row_ctx, Hl,
              ws_o, ws_ml, ms, kps, (T*)out, ldo);
@@ -456,8 +468,9 @@ static int attn_launch(const void* q, const fl_row* rows, const int32_t* row_ctx
 
 // Row ranks by descending context (ties: lower row first) for the snake
 // schedule: one CTA bitonic-sorts packed (~ctx, row) keys, M <= 1024.
-__global__ void __launch_bounds__(1024) k_row_order(const int32_t* __restrict__ row_ctx, int M,
-                                                   int32_t* __restrict__ order) {
+__global__ void __launch_bounds__(1024) k_row_order(const int32_t* __restrict__ row_ctx,
+                                                   const fl_row* __restrict__ rows, int M,
+                                                   int4* __restrict__ meta) {
   __shared__ unsigned long long key[1024];
   pdl_trigger();
   pdl_wait();
@@ -479,26 +492,29 @@ __global__ void __launch_bounds__(1024) k_row_order(const int32_t* __restrict__ 
       }
       __syncthreads();
     }
-  for (int i = threadIdx.x; i < M; i += blockDim.x) order[i] = static_cast<int32_t>(key[i] & 0xffffffffu);
+  for (int i = threadIdx.x; i < M; i += blockDim.x) {
+    const int r = static_cast<int>(key[i] & 0xffffffffu);
+    meta[i] = make_int4(r, row_ctx[r], rows[r].slot, 0);
+  }
 }
 
-void launch_row_order(const int32_t* row_ctx, int M, int32_t* order, cudaStream_t s) {
+void launch_row_order(const int32_t* row_ctx, const fl_row* rows, int M, int4* meta, cudaStream_t s) {
   if (M <= 0 || M > 1024) return;
-  launch_k(k_row_order, dim3(1), dim3(M > 512 ? 1024 : 512), 0, s, 1, row_ctx, M, order);
+  launch_k(k_row_order, dim3(1), dim3(M > 512 ? 1024 : 512), 0, s, 1, row_ctx, rows, M, meta);
 }
 
 int launch_attention(const void* q, const fl_row* rows, const int32_t* row_ctx, int M, int Hl,
                      int hd, const void* kv_layer, int C, int S, int kps, void* out, float* ws_o,
-                     float* ws_ml, int dtype, cudaStream_t s, const int32_t* order, int ldo, unsigned* ctr) {
+                     float* ws_ml, int dtype, cudaStream_t s, const int4* meta, int ldo, unsigned* ctr) {
   if (ldo <= 0) ldo = Hl * hd;
   if (M <= 0) return 0;
 #define FL_ATT(HDV)                                                                          \
   case HDV:                                                                                  \
     return dtype == FL_DTYPE_BF16                                                            \
                ? attn_launch<bf16, HDV>(q, rows, row_ctx, M, Hl, kv_layer, S, kps, out, ws_o, \
-                                        ws_ml, order, ldo, s, ctr)                           \
+                                        ws_ml, meta, ldo, s, ctr)                            \
                : attn_launch<float, HDV>(q, rows, row_ctx, M, Hl, kv_layer, S, kps, out,      \
-                                         ws_o, ws_ml, order, ldo, s, ctr);
+                                         ws_o, ws_ml, meta, ldo, s, ctr);
   switch (hd) {
     FL_ATT(64)
     FL_ATT(96)

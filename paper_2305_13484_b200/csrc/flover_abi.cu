@@ -98,7 +98,8 @@ struct fl_handle {
   int Hl, Dl, Fl, Vl, Vloc, es, ms;
   // workspace carve
   fl_row* rows;
-  int32_t *row_tok, *row_pos, *row_ctx, *row_order, *moves;
+  int32_t *row_tok, *row_pos, *row_ctx, *moves;
+  int4* row_order;   // per rank: (row, context, slot) by descending context
   char* plan_ws;
   std::vector<char> plan_stage;           // host staging of the window arrays
   float *x, *y, *logits, *att_o, *att_ml;
@@ -241,7 +242,7 @@ Layout plan(const fl_model_desc* m, const fl_pool_desc* p) {
   L.row_tok = c.take(Mr * 4);
   L.row_pos = c.take(Mr * 4);
   L.row_ctx = c.take(Mr * 4);
-  L.row_order = c.take(Mr * 4);
+  L.row_order = c.take(Mr * 16);
   L.moves = c.take(size_t(p->pool_slots) * 3 * 4 + 16);
   // device-planned shuffle: window occ/ctx (int32) + sizes (int64) in, plan out
   L.plan = c.take(size_t(p->pool_slots) * 16 + (3 + 2 * size_t(p->pool_slots)) * 4 + 64);
@@ -310,7 +311,7 @@ int fl_create(const fl_model_desc* m, const fl_pool_desc* p, fl_handle** out) {
   h->row_tok = (int32_t*)(w + L.row_tok);
   h->row_pos = (int32_t*)(w + L.row_pos);
   h->row_ctx = (int32_t*)(w + L.row_ctx);
-  h->row_order = (int32_t*)(w + L.row_order);
+  h->row_order = (int4*)(w + L.row_order);
   h->moves = (int32_t*)(w + L.moves);
   h->plan_ws = w + L.plan;
   h->x = (float*)(w + L.x);
@@ -518,7 +519,7 @@ int enqueue_step(fl_handle* h, int n_rows, int n_dec, bool want_logits, cudaStre
   // rows ranked by descending context once per step (attention's schedule)
   const bool ordered = n_rows <= 1024;
   if (ordered) {
-    fl::launch_row_order(h->row_ctx, n_rows, h->row_order, s);
+    fl::launch_row_order(h->row_ctx, h->rows, n_rows, h->row_order, s);
     fl::g_launches += 1;
   }
   for (int l = 0; l < L; ++l) {

@@ -72,10 +72,11 @@ int attn_keys_per_split(int row_heads, int S);
 // the kernel re-arms them, so one pair per stream of launches suffices
 int launch_attention(const void* q, const fl_row* rows, const int32_t* row_ctx, int M, int Hl,
                      int hd, const void* kv_layer, int C, int S, int keys_per_split, void* out,
-                     float* ws_o, float* ws_ml, int dtype, cudaStream_t s, const int32_t* order,
+                     float* ws_o, float* ws_ml, int dtype, cudaStream_t s, const int4* meta,
                      int ldo, unsigned* ctr);
-// order[i] = row of rank i by descending context (attention's snake schedule)
-void launch_row_order(const int32_t* row_ctx, int M, int32_t* order, cudaStream_t s);
+// meta[i] = (row, context, KV slot, 0) of rank i by descending context
+// (attention's item order; M <= 1024)
+void launch_row_order(const int32_t* row_ctx, const fl_row* rows, int M, int4* meta, cudaStream_t s);
 
 // per-row (max logit, lowest index) as a packed 64-bit key
 void launch_argmax(const float* logits, int M, int V, int ldl, int index_base,
