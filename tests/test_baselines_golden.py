@@ -58,5 +58,6 @@ def test_concurrent_scenario_dispatch():
         fl.Scenario("x", fl.Discipline.FUSION, 12, fl.PoissonArrival(30.0),
                     fl.UniformLength(10, 40), 40), 3), 12)
     assert conc.makespan_ms > 0 and fu.makespan_ms > 0
-    with pytest.raises(fl.ConfigError):
+    # the device clock needs an executor (device-clock instances: tests/test_gpu_parity.py)
+    with pytest.raises(fl.InvalidParam):
         fl.run_scenario(sc, 3, clock="device")
