@@ -21,6 +21,9 @@ The outputs are small JSON(.gz) fixtures next to this script:
                       cases (engine.py:128-207)
   dynbatch.json.gz    run_dynamic_batching traces (baselines.py:51-127)
   concurrent.json.gz  run_concurrent_instances traces (baselines.py:130-229)
+  suite.csv           the results CSV of a scenario grid (suite.py:23-54,
+                      137-172): every discipline, constant / Poisson
+                      arrivals, fixed / uniform lengths, TP 1 / 2, 1-3 seeds
 """
 
 from __future__ import annotations
@@ -366,10 +369,22 @@ def gen_concurrent():
     _dump("concurrent.json.gz", {"cases": cases}, gz=True)
 
 
+def gen_suite():
+    """suite.py: run_cells -> result_rows -> write_csv on a small grid."""
+    from fusionsim import suite as rsuite
+    from fusionsim.scenario import ConstantArrival
+    sys.path.insert(0, HERE)
+    from suite_grid import suite_grid
+    grid = suite_grid(Scenario, Discipline, ConstantArrival, PoissonArrival, FixedLength, UniformLength, TPConfig,
+                      Placement)
+    rsuite.write_csv(rsuite.result_rows(rsuite.run_cells(grid)), os.path.join(HERE, "suite.csv"))
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         globals()["gen_" + sys.argv[1]]()
         sys.exit(0)
+    gen_suite()
     gen_concurrent()
     gen_dynbatch()
     gen_rng()

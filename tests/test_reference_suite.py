@@ -3,9 +3,8 @@
 ``/root/reference/pkg/tests`` imports ``fusionsim.*``.  A pytest plugin
 written to a temp dir maps ``fusionsim`` and every module this package
 implements (engine, buffer, core, cost, trace, scenario, baselines, metrics,
-arrivals, rng, errors) onto ``paper_2305_13484_b200``; the out-of-scope
-modules (suite, config, calibrate, cli, the reference's test
-oracle) are served from the reference sources, and they in turn import the
+arrivals, rng, errors, suite) onto ``paper_2305_13484_b200``; the out-of-scope
+modules (config, calibrate, cli, the reference's test oracle) are served from the reference sources, and they in turn import the
 in-scope API from THIS package.  Every reference test must pass.
 
 Skipped where the reference is absent (the GPU box has no /root/reference).
@@ -63,4 +62,4 @@ def test_reference_suite_passes_against_this_package(tmp_path):
     # the engine, buffer, core, cost ... under test are ours, not the reference's
     served = set(re.findall(r"reference module: fusionsim\.(\w+)", p.stderr))
     assert not served & {"engine", "buffer", "core", "cost", "trace", "scenario", "baselines",
-                         "metrics", "arrivals", "rng", "errors"}, served
+                         "metrics", "arrivals", "rng", "errors", "suite"}, served
