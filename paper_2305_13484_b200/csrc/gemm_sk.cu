@@ -952,10 +952,15 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
         if (warp == 2 && lane == 0)
           for (int q = pair + 1; q <= plast; ++q) P.flags[q * 2 + xi] = 0u;   // re-arm
       }
-      // this buffer may be overwritten by the next-but-(nbuf-1) segment
+      // this buffer may be overwritten by the next-but-(nbuf-1) segment --
+      // unless this was the pair's last segment (no MMA waits on it; the
+      // release-ordered remote arrive would wait for this warp's stores:
+      // out-projection at 16 / 144 rows 761 -> 752 / 882 -> 873 us per 28
+      // layers, C2 step 491 -> 483 us)
+      const bool last_seg = u + (khi - klo) >= R.hi[r] && (r == 1 || R.hi[1] <= R.lo[1]);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(&tempty_bar[b], prank);
+      if (lane == 0 && !last_seg) mbar_arrive_cluster(&tempty_bar[b], prank);
       if (P.dbg) e_post += clock64() - tb1;
       u += khi - klo;
       ++seg;
