@@ -103,7 +103,11 @@ FL_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
 FL_DEV void mbar_arrive_cluster(uint64_t* bar, uint32_t rank) {
   uint32_t remote;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+  // default semantics (release, CTA scope), as CUTLASS's ClusterBarrier::arrive:
+  // the consumer's TMEM reads are ordered by tcgen05.wait::ld +
+  // fence::before_thread_sync, and a cluster-scope release would also wait
+  // for this thread's global stores
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
 // 2-SM load: lands in this CTA's smem, completes tx on the leader's barrier
 FL_DEV void tma_load_pair(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1) {
@@ -983,7 +987,11 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
   __syncwarp();
   tc_fence_before();
   __syncwarp();
-  cluster_sync_all();            // the pair's TMEM is freed jointly
+  // the pair's TMEM is freed jointly.  Only TMEM is handed over here and its
+  // accesses are ordered by the tcgen05 fences around this execution
+  // barrier, so the arrive is relaxed: a release would first drain every
+  // thread's epilogue stores (C2 step 484 -> 472 us)
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(P.ncols));
