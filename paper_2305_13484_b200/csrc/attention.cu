@@ -145,7 +145,8 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
     const T* __restrict__ q, const fl_row* __restrict__ rows, const int32_t* __restrict__ row_ctx,
     int M, int Hl, const T* __restrict__ kv_layer, int S, T* __restrict__ out,
     float* __restrict__ ws_o, float* __restrict__ ws_ml, int max_splits, int keys_per_split,
-    int splits, const int4* __restrict__ meta, int ldo, unsigned* __restrict__ ctr) {
+    int splits, const int4* __restrict__ meta, int ldo, unsigned* __restrict__ ctr,
+    unsigned* __restrict__ next_ctr) {
   using Cfg = AttnCfg<T, HD>;
   constexpr int VEC = Cfg::VEC, NV = Cfg::NV, G = Cfg::G, PER = Cfg::PER, KPW = Cfg::KPW;
   constexpr int CW = Cfg::CW, TK = Cfg::TK, STAGES = Cfg::STAGES, NP = CW;
@@ -410,6 +411,14 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
     if (dbg && threadIdx.x == 0 && n_done < 31) dbg[3 + 2 * n_done] = gtime();
     ++n_done;
   }
+  if (next_ctr) {
+    // a chain of launches with one counter each: this launch arms the next
+    // one's (that launch claims only after its grid dependency wait, i.e.
+    // after this grid completed; the launch before this one, which used it,
+    // completed before this grid's own wait returned) -- no exit atomic
+    if (blockIdx.x == 0 && threadIdx.x == 0) *next_ctr = 0u;
+    return;
+  }
   // this CTA's producer claimed its last item before it sent the sentinel:
   // the last CTA to finish re-arms the item counter for the next launch
   if (threadIdx.x == 0 && atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {
@@ -442,7 +451,7 @@ __global__ void k_attn_combine(const int32_t* __restrict__ row_ctx, int Hl,
 template <typename T, int HD>
 static int attn_launch(const void* q, const fl_row* rows, const int32_t* row_ctx, int M, int Hl,
                        const void* kv_layer, int S, int kps, void* out, float* ws_o, float* ws_ml,
-                       const int4* meta, int ldo, cudaStream_t s, unsigned* ctr) {
+                       const int4* meta, int ldo, cudaStream_t s, unsigned* ctr, unsigned* next_ctr) {
   using Cfg = AttnCfg<T, HD>;
   static int num_sms = 0;
   if (!num_sms) {
@@ -457,7 +466,8 @@ static int attn_launch(const void* q, const fl_row* rows, const int32_t* row_ctx
   const int per_sm = ATT_CW >= 8 ? 1 : 2;
   const int grid = items < per_sm * num_sms ? items : per_sm * num_sms;
   launch_k(k_attn_tma<T, HD>, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM, s, 1, (const T*)q, rows,
-           row_ctx, M, Hl, (const T*)kv_layer, S, (T*)out, ws_o, ws_ml, ms, kps, splits, meta, ldo, ctr);
+           row_ctx, M, Hl, (const T*)kv_layer, S, (T*)out, ws_o, ws_ml, ms, kps, splits, meta, ldo, ctr,
+           next_ctr);
   if (splits > 1) {
     launch_k(k_attn_combine<T, HD>, dim3(Hl, M), dim3(HD < 128 ? HD : 128), 0, s, 1, row_ctx, Hl,
              ws_o, ws_ml, ms, kps, (T*)out, ldo);
@@ -495,16 +505,17 @@ void launch_row_order(const int32_t* row_ctx, const fl_row* rows, int M, int4* m
 
 int launch_attention(const void* q, const fl_row* rows, const int32_t* row_ctx, int M, int Hl,
                      int hd, const void* kv_layer, int C, int S, int kps, void* out, float* ws_o,
-                     float* ws_ml, int dtype, cudaStream_t s, const int4* meta, int ldo, unsigned* ctr) {
+                     float* ws_ml, int dtype, cudaStream_t s, const int4* meta, int ldo, unsigned* ctr,
+                     unsigned* next_ctr) {
   if (ldo <= 0) ldo = Hl * hd;
   if (M <= 0) return 0;
 #define FL_ATT(HDV)                                                                          \
   case HDV:                                                                                  \
     return dtype == FL_DTYPE_BF16                                                            \
                ? attn_launch<bf16, HDV>(q, rows, row_ctx, M, Hl, kv_layer, S, kps, out, ws_o, \
-                                        ws_ml, meta, ldo, s, ctr)                            \
+                                        ws_ml, meta, ldo, s, ctr, next_ctr)                  \
                : attn_launch<float, HDV>(q, rows, row_ctx, M, Hl, kv_layer, S, kps, out,      \
-                                         ws_o, ws_ml, meta, ldo, s, ctr);
+                                         ws_o, ws_ml, meta, ldo, s, ctr, next_ctr);
   switch (hd) {
     FL_ATT(64)
     FL_ATT(96)

@@ -212,6 +212,7 @@ struct Layout {
 int check_desc(const fl_model_desc* m, const fl_pool_desc* p) {
   if (!m || !p) return fail(FL_EINVAL, "null descriptor");
   if (m->family < 0 || m->family > 2) return fail(FL_EINVAL, "bad family %d", m->family);
+  if (m->n_layer < 1 || m->n_layer > 256) return fail(FL_EINVAL, "n_layer %d outside [1, 256]", m->n_layer);
   if (m->dtype != FL_DTYPE_F32 && m->dtype != FL_DTYPE_BF16) return fail(FL_EINVAL, "bad dtype");
   if (m->tp_size < 1 || m->tp_rank < 0 || m->tp_rank >= m->tp_size)
     return fail(FL_EINVAL, "bad tp rank/size");
@@ -251,7 +252,7 @@ Layout plan(const fl_model_desc* m, const fl_pool_desc* p) {
   L.logits = c.take(Md * Vl * 4);
   L.att_o = c.take(Mr * Hl * ms * m->head_dim * 4);
   L.att_ml = c.take(Mr * Hl * ms * 2 * 4);
-  L.att_ctr = c.take(256);
+  L.att_ctr = c.take(1024);
   L.h = c.take(Mr * d * es);
   L.h2 = c.take(m->family == FL_FAMILY_NEOX ? Mr * d * es : 0);
   // q|k|v, the attention output a and the FFN activation f share rows:
@@ -320,7 +321,7 @@ int fl_create(const fl_model_desc* m, const fl_pool_desc* p, fl_handle** out) {
   h->att_o = (float*)(w + L.att_o);
   h->att_ml = (float*)(w + L.att_ml);
   h->att_ctr = (unsigned*)(w + L.att_ctr);
-  if (cudaMemset(h->att_ctr, 0, 256) != cudaSuccess) {
+  if (cudaMemset(h->att_ctr, 0, 1024) != cudaSuccess) {
     delete h;
     return fail(FL_ECUDA, "attention counters: %s", cudaGetErrorString(cudaGetLastError()));
   }
@@ -553,7 +554,10 @@ int enqueue_step(fl_handle* h, int n_rows, int n_dec, bool want_logits, cudaStre
       fl::g_launches += fl::launch_attention(h->q, h->rows, h->row_ctx, n_rows, Hl, hd, kvl,
                                              p.pool_slots, p.max_seq, att_keys, h->a, h->att_o,
                                              h->att_ml, dt, s, ordered ? h->row_order : nullptr, h->ldaf,
-                                             h->att_ctr);
+                                             // one claim counter per layer, each launch arms the next
+                                             // layer's (the last the next step's layer 0)
+                                             L >= 2 ? h->att_ctr + l : h->att_ctr,
+                                             L >= 2 ? h->att_ctr + (l + 1) % L : nullptr);
     }
     fl::g_launches += 1;
     // K5 attn-out (+ all-reduce); merged into K7 for parallel-residual models

@@ -69,11 +69,14 @@ int attn_max_splits(int S);
 int attn_keys_per_split(int row_heads, int S);
 // returns the number of kernels launched (1 or 2)
 // ctr: two zero-initialised device counters (item claims, finished CTAs);
-// the kernel re-arms them, so one pair per stream of launches suffices
+// the kernel re-arms them, so one pair per stream of launches suffices.
+// next_ctr (a chain of launches, one counter each, >= 2 in the cycle): the
+// launch zeroes the next launch's claim counter instead of re-arming its own
+// at exit
 int launch_attention(const void* q, const fl_row* rows, const int32_t* row_ctx, int M, int Hl,
                      int hd, const void* kv_layer, int C, int S, int keys_per_split, void* out,
                      float* ws_o, float* ws_ml, int dtype, cudaStream_t s, const int4* meta,
-                     int ldo, unsigned* ctr);
+                     int ldo, unsigned* ctr, unsigned* next_ctr = nullptr);
 // meta[i] = (row, context, KV slot, 0) of rank i by descending context
 // (attention's item order; M <= 1024)
 void launch_row_order(const int32_t* row_ctx, const fl_row* rows, int M, int4* meta, cudaStream_t s);
