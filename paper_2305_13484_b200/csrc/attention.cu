@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
     int M, int Hl, const T* __restrict__ kv_layer, int S, T* __restrict__ out,
     float* __restrict__ ws_o, float* __restrict__ ws_ml, int max_splits, int keys_per_split,
     int splits, const int4* __restrict__ meta, int ldo, unsigned* __restrict__ ctr,
-    unsigned* __restrict__ next_ctr) {
+    unsigned* __restrict__ next_ctr, unsigned* __restrict__ pre, int pre_mode) {
   using Cfg = AttnCfg<T, HD>;
   constexpr int VEC = Cfg::VEC, NV = Cfg::NV, G = Cfg::G, PER = Cfg::PER, KPW = Cfg::KPW;
   constexpr int CW = Cfg::CW, TK = Cfg::TK, STAGES = Cfg::STAGES, NP = CW;
@@ -180,7 +180,6 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  pdl_wait();       // q, row_ctx and this step's K/V rows come from predecessors
 
   const int n_items = M * Hl * splits;
   const int D = Hl * HD;
@@ -191,6 +190,47 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
     if (lane == 0) {
       int st = 0, qs = 0;
       uint32_t ph = 0, qph = 0;
+      // Before the grid dependency resolves (pre_mode 1: a step-graph launch
+      // that is not the step's last attention), stream up to a ring of this
+      // CTA's first item from keys written by EARLIER graph launches: with
+      // every kernel triggering its dependents at entry, only data from a
+      // previous launch is safe here.  The item's (row, context, slot, old
+      // keys) come from this step's k_row_order, which publishes
+      // pre[1] = pre[0] + 1 after writing them (pre[0] is advanced by the
+      // step's last attention launch, after its own dependency wait, so it is
+      // stable for the whole step).  meta.w = keys [0, w) of the row that no
+      // kernel of this step writes (decode: ctx - 1; prefill / orphan: 0).
+      int n_pre = 0;
+      if (pre_mode == 1 && meta && static_cast<int>(blockIdx.x) < n_items) {
+        const unsigned want = __ldcg(pre) + 1u;
+        for (;;) {
+          unsigned f;
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(pre + 1) : "memory");
+          if (f == want) break;
+          __nanosleep(32);
+        }
+        const int item = static_cast<int>(blockIdx.x);
+        const int rh = item / splits;
+        const int4 m = __ldcg(meta + rh / Hl);
+        const int h = rh % Hl, ctx = m.y, safe = m.w;
+        const size_t slot = static_cast<size_t>(m.z);
+        const int k0 = (item % splits) * keys_per_split;
+        const int k1 = min(ctx, k0 + keys_per_split);
+        const T* Kb = kv_layer + ((slot * 2 + 0) * Hl + h) * head_stride;
+        const T* Vb = kv_layer + ((slot * 2 + 1) * Hl + h) * head_stride;
+        for (int t0 = k0; t0 < k1 && n_pre < STAGES; t0 += TK) {
+          const int nk = min(TK, k1 - t0);
+          if (t0 + nk > safe) break;
+          uint8_t* buf = smem + st * Cfg::STAGE_BYTES;   // ring still empty: no slot wait
+          mbar_expect_tx_(&full[st], 2u * nk * Cfg::ROW);
+          bulk_g2s(buf, Kb + static_cast<size_t>(t0) * HD, nk * Cfg::ROW, &full[st]);
+          bulk_g2s(buf + TK * Cfg::ROW, Vb + static_cast<size_t>(t0) * HD, nk * Cfg::ROW, &full[st]);
+          if (++st == STAGES) { st = 0; ph ^= 1; }
+          ++n_pre;
+        }
+      }
+      pdl_wait();   // q, row_ctx, the counters and this step's K/V rows come from predecessors
+      if (pre_mode == 2 && blockIdx.x == 0) pre[0] += 1u;   // the step's last attention: next step's epoch
       bool first = true;
       for (;;) {
         // CTA b starts with item b (the first round needs no atomic); later
@@ -235,7 +275,7 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
         const int k1 = min(ctx, k0 + keys_per_split);
         const T* Kb = kv_layer + ((slot * 2 + 0) * Hl + h) * head_stride;
         const T* Vb = kv_layer + ((slot * 2 + 1) * Hl + h) * head_stride;
-        for (int t0 = k0; t0 < k1; t0 += TK) {
+        for (int t0 = k0 + n_pre * TK; t0 < k1; t0 += TK) {
           const int nk = min(TK, k1 - t0);
           mbar_wait_(&empty[st], ph ^ 1);
           uint8_t* buf = smem + st * Cfg::STAGE_BYTES;
@@ -244,11 +284,13 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
           bulk_g2s(buf + TK * Cfg::ROW, Vb + static_cast<size_t>(t0) * HD, nk * Cfg::ROW, &full[st]);
           if (++st == STAGES) { st = 0; ph ^= 1; }
         }
+        n_pre = 0;
       }
     }
     return;
   }
 
+  pdl_wait();
   // ---------------- consumers
   const int g = lane % G;           // lane within the key group
   const int kw = lane / G;          // key group within the warp
@@ -451,7 +493,8 @@ __global__ void k_attn_combine(const int32_t* __restrict__ row_ctx, int Hl,
 template <typename T, int HD>
 static int attn_launch(const void* q, const fl_row* rows, const int32_t* row_ctx, int M, int Hl,
                        const void* kv_layer, int S, int kps, void* out, float* ws_o, float* ws_ml,
-                       const int4* meta, int ldo, cudaStream_t s, unsigned* ctr, unsigned* next_ctr) {
+                       const int4* meta, int ldo, cudaStream_t s, unsigned* ctr, unsigned* next_ctr,
+                       unsigned* pre, int pre_mode) {
   using Cfg = AttnCfg<T, HD>;
   static int num_sms = 0;
   if (!num_sms) {
@@ -467,7 +510,7 @@ static int attn_launch(const void* q, const fl_row* rows, const int32_t* row_ctx
   const int grid = items < per_sm * num_sms ? items : per_sm * num_sms;
   launch_k(k_attn_tma<T, HD>, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM, s, 1, (const T*)q, rows,
            row_ctx, M, Hl, (const T*)kv_layer, S, (T*)out, ws_o, ws_ml, ms, kps, splits, meta, ldo, ctr,
-           next_ctr);
+           next_ctr, pre, pre ? pre_mode : 0);
   if (splits > 1) {
     launch_k(k_attn_combine<T, HD>, dim3(Hl, M), dim3(HD < 128 ? HD : 128), 0, s, 1, row_ctx, Hl,
              ws_o, ws_ml, ms, kps, (T*)out, ldo);
@@ -483,39 +526,62 @@ static int attn_launch(const void* q, const fl_row* rows, const int32_t* row_ctx
 // step's first kernels wait on it).  meta[rank] = (row, ctx, slot, 0).
 __global__ void __launch_bounds__(1024) k_row_order(const int32_t* __restrict__ row_ctx,
                                                    const fl_row* __restrict__ rows, int M,
-                                                   int4* __restrict__ meta) {
+                                                   int4* __restrict__ meta, unsigned* __restrict__ pre) {
   __shared__ unsigned long long key[1024];
+  __shared__ int pf_slot[1024];   // slots that prefill rows of this step write
+  __shared__ int n_pf;
   pdl_trigger();
   pdl_wait();
-  for (int i = threadIdx.x; i < M; i += blockDim.x)
+  if (threadIdx.x == 0) n_pf = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < M; i += blockDim.x) {
     key[i] = (static_cast<unsigned long long>(0x7fffffffu - static_cast<uint32_t>(row_ctx[i])) << 32) | i;
+    if (pre && rows[i].kind == FL_ROW_PREFILL) pf_slot[atomicAdd(&n_pf, 1)] = rows[i].slot;
+  }
   __syncthreads();
   for (int i = threadIdx.x; i < M; i += blockDim.x) {
     const unsigned long long k = key[i];
     int rank = 0;
     for (int j = 0; j < M; ++j) rank += key[j] < k;
-    meta[rank] = make_int4(i, row_ctx[i], rows[i].slot, 0);
+    const int ctx = row_ctx[i];
+    const fl_row ri = rows[i];
+    // keys no kernel of this step writes (attention may stream them before its
+    // grid dependency wait): a decode row appends key ctx - 1 this step, and
+    // a request admitted this step has its prompt written by prefill rows
+    int old = ri.kind == FL_ROW_DECODE ? ctx - 1 : 0;
+    for (int j = 0; j < n_pf && old > 0; ++j)
+      if (pf_slot[j] == ri.slot) old = 0;
+    meta[rank] = make_int4(i, ctx, ri.slot, old > 0 ? old : 0);
+  }
+  if (pre) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      const unsigned v = __ldcg(pre) + 1u;
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(pre + 1), "r"(v) : "memory");
+    }
   }
 }
 
-void launch_row_order(const int32_t* row_ctx, const fl_row* rows, int M, int4* meta, cudaStream_t s) {
+void launch_row_order(const int32_t* row_ctx, const fl_row* rows, int M, int4* meta, cudaStream_t s,
+                      unsigned* pre) {
   if (M <= 0 || M > 1024) return;
-  launch_k(k_row_order, dim3(1), dim3((M + 31) / 32 * 32), 0, s, 1, row_ctx, rows, M, meta);
+  launch_k(k_row_order, dim3(1), dim3((M + 31) / 32 * 32), 0, s, 1, row_ctx, rows, M, meta, pre);
 }
 
 int launch_attention(const void* q, const fl_row* rows, const int32_t* row_ctx, int M, int Hl,
                      int hd, const void* kv_layer, int C, int S, int kps, void* out, float* ws_o,
                      float* ws_ml, int dtype, cudaStream_t s, const int4* meta, int ldo, unsigned* ctr,
-                     unsigned* next_ctr) {
+                     unsigned* next_ctr, unsigned* pre, int pre_mode) {
   if (ldo <= 0) ldo = Hl * hd;
   if (M <= 0) return 0;
 #define FL_ATT(HDV)                                                                          \
   case HDV:                                                                                  \
     return dtype == FL_DTYPE_BF16                                                            \
                ? attn_launch<bf16, HDV>(q, rows, row_ctx, M, Hl, kv_layer, S, kps, out, ws_o, \
-                                        ws_ml, meta, ldo, s, ctr, next_ctr)                  \
+                                        ws_ml, meta, ldo, s, ctr, next_ctr, pre, pre_mode)                  \
                : attn_launch<float, HDV>(q, rows, row_ctx, M, Hl, kv_layer, S, kps, out,      \
-                                         ws_o, ws_ml, meta, ldo, s, ctr, next_ctr);
+                                         ws_o, ws_ml, meta, ldo, s, ctr, next_ctr, pre, pre_mode);
   switch (hd) {
     FL_ATT(64)
     FL_ATT(96)

@@ -252,7 +252,7 @@ Layout plan(const fl_model_desc* m, const fl_pool_desc* p) {
   L.logits = c.take(Md * Vl * 4);
   L.att_o = c.take(Mr * Hl * ms * m->head_dim * 4);
   L.att_ml = c.take(Mr * Hl * ms * 2 * 4);
-  L.att_ctr = c.take(1024);
+  L.att_ctr = c.take(1024 + 64);   // 256 per-layer claim counters + {epoch, published} at 256
   L.h = c.take(Mr * d * es);
   L.h2 = c.take(m->family == FL_FAMILY_NEOX ? Mr * d * es : 0);
   // q|k|v, the attention output a and the FFN activation f share rows:
@@ -321,7 +321,7 @@ int fl_create(const fl_model_desc* m, const fl_pool_desc* p, fl_handle** out) {
   h->att_o = (float*)(w + L.att_o);
   h->att_ml = (float*)(w + L.att_ml);
   h->att_ctr = (unsigned*)(w + L.att_ctr);
-  if (cudaMemset(h->att_ctr, 0, 1024) != cudaSuccess) {
+  if (cudaMemset(h->att_ctr, 0, 1024 + 64) != cudaSuccess) {
     delete h;
     return fail(FL_ECUDA, "attention counters: %s", cudaGetErrorString(cudaGetLastError()));
   }
@@ -519,8 +519,12 @@ int enqueue_step(fl_handle* h, int n_rows, int n_dec, bool want_logits, cudaStre
   const int att_keys = fl::attn_keys_per_split(n_rows * Hl, p.max_seq);
   // rows ranked by descending context once per step (attention's schedule)
   const bool ordered = n_rows <= 1024;
+  // attention's pre-dependency streaming: CUDA graphs only (a graph launch
+  // starts after the previous one completed, so earlier steps' K/V is final;
+  // eager launches of consecutive steps may overlap through the PDL chain)
+  unsigned* const pre = ordered && h->capturing && L >= 2 ? h->att_ctr + 256 : nullptr;
   if (ordered) {
-    fl::launch_row_order(h->row_ctx, h->rows, n_rows, h->row_order, s);
+    fl::launch_row_order(h->row_ctx, h->rows, n_rows, h->row_order, s, pre);
     fl::g_launches += 1;
   }
   for (int l = 0; l < L; ++l) {
@@ -557,7 +561,8 @@ int enqueue_step(fl_handle* h, int n_rows, int n_dec, bool want_logits, cudaStre
                                              // one claim counter per layer, each launch arms the next
                                              // layer's (the last the next step's layer 0)
                                              L >= 2 ? h->att_ctr + l : h->att_ctr,
-                                             L >= 2 ? h->att_ctr + (l + 1) % L : nullptr);
+                                             L >= 2 ? h->att_ctr + (l + 1) % L : nullptr,
+                                             pre, l == L - 1 ? 2 : 1);
     }
     fl::g_launches += 1;
     // K5 attn-out (+ all-reduce); merged into K7 for parallel-residual models

@@ -76,10 +76,16 @@ int attn_keys_per_split(int row_heads, int S);
 int launch_attention(const void* q, const fl_row* rows, const int32_t* row_ctx, int M, int Hl,
                      int hd, const void* kv_layer, int C, int S, int keys_per_split, void* out,
                      float* ws_o, float* ws_ml, int dtype, cudaStream_t s, const int4* meta,
-                     int ldo, unsigned* ctr, unsigned* next_ctr = nullptr);
-// meta[i] = (row, context, KV slot, 0) of rank i by descending context
-// (attention's item order; M <= 1024)
-void launch_row_order(const int32_t* row_ctx, const fl_row* rows, int M, int4* meta, cudaStream_t s);
+                     int ldo, unsigned* ctr, unsigned* next_ctr = nullptr, unsigned* pre = nullptr,
+                     int pre_mode = 0);
+// meta[i] = (row, context, KV slot, keys not written this step) of rank i by
+// descending context (attention's item order; M <= 1024).  pre (step graphs
+// only): two words {epoch, published}; the kernel sets published = epoch + 1
+// after meta, so attention launches (pre_mode 1) may stream their first
+// item's older keys before their grid dependency wait; the step's last
+// attention launch (pre_mode 2) advances the epoch after its wait.
+void launch_row_order(const int32_t* row_ctx, const fl_row* rows, int M, int4* meta, cudaStream_t s,
+                      unsigned* pre = nullptr);
 
 // per-row (max logit, lowest index) as a packed 64-bit key
 void launch_argmax(const float* logits, int M, int V, int ldl, int index_base,
