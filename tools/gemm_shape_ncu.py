@@ -31,7 +31,7 @@ for f in glob.glob(os.path.join(sys.argv[1], "gemm_shape_*_*.csv")):
         if name.startswith("dram__bytes"):
             v *= {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
         if name == "gpu__time_duration.sum":
-            v *= {"nsecond": 1e-3, "usecond": 1, "msecond": 1e3}.get(unit, 1)
+            v *= {"ns": 1e-3, "nsecond": 1e-3, "us": 1, "usecond": 1, "ms": 1e3, "msecond": 1e3}.get(unit, 1)
         met[r["ID"]][name] = v
     if not met:
         continue
