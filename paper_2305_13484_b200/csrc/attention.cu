@@ -22,6 +22,18 @@ constexpr int ATT_THREADS = 128;
 #ifndef ATT_CW
 #define ATT_CW 4   // consumer warps per CTA (A/B builds: 8 = one CTA per SM)
 #endif
+// K/V ring bytes per CTA.  The consumers are latency-bound (ncu at C4, hd 96:
+// 2.4 active / 0.56 eligible warps per scheduler, issue slots 44 % busy), so
+// smaller rings that let more CTAs share an SM win: 44 KB below head_dim 128
+// (4 CTAs per SM, register-limited; C4 48 rows 10.54 -> 10.03 ms per
+// iteration, C2 16 rows 463 -> 455 us), 64 KB from 128 (3 CTAs per SM with
+// 8 KB K tiles; C3 128 rows 5932 -> 5896 us, 224 rows ~ -1 %)
+#ifndef ATT_RING_SMALL
+#define ATT_RING_SMALL 45056
+#endif
+#ifndef ATT_RING_LARGE
+#define ATT_RING_LARGE 65536
+#endif
 #ifndef ATT_TILE_BYTES
 #define ATT_TILE_BYTES 0   // 0: per head_dim (AttnCfg::TKB); A/B builds override
 #endif
@@ -84,18 +96,24 @@ struct AttnCfg {
   static constexpr int CW = ATT_CW;                       // consumer warps
   static constexpr int THREADS = (CW + 1) * 32;
   static constexpr int ROW = HD * sizeof(T);              // bytes per key row
-  // K bytes per tile: 16 KB at head_dim 256; 8 KB below, where a key is cheap
-  // to stream but costly to score (finer tiles keep more of the 48 KB ring in
-  // flight: hd 96 5.07 -> 5.50 TB/s, hd 256 16 KB 6.2 vs 8 KB 6.0 TB/s,
-  // tools/attn_bench.py)
-  static constexpr int TKB = ATT_TILE_BYTES ? ATT_TILE_BYTES : (HD >= 256 ? 16384 : 8192);
+  // K bytes per tile: 8 KB (finer tiles keep more of the ring in flight:
+  // hd 96 5.07 -> 5.50 TB/s at 2 CTAs per SM, tools/attn_bench.py; at head_dim
+  // 256 16 KB tiles won at 2 CTAs per SM, 8 KB wins with 3 and a 64 KB ring)
+  static constexpr int TKB = ATT_TILE_BYTES ? ATT_TILE_BYTES : 8192;
   static constexpr int TK = (TKB / ROW) / (CW * KPW) * (CW * KPW) > 0 ? (TKB / ROW) / (CW * KPW) * (CW * KPW)
                                                                       : CW * KPW;   // keys per tile
-  // ring budget per CTA: 96 KB at 4 consumer warps (2 CTAs per SM), 192 KB at 8 (1 CTA per SM)
-  static constexpr int RING = ATT_CW >= 8 ? 6 * 32768 : 3 * 32768;
+  // ring budget per CTA (the launcher sizes the grid by the co-resident CTAs per SM)
+  static constexpr int RING = ATT_CW >= 8 ? 6 * 32768 : HD < 128 ? ATT_RING_SMALL : ATT_RING_LARGE;
   static constexpr int STAGES = (RING / 2) / (TK * ROW) < 2 ? 2 : (RING / 2) / (TK * ROW);
   static constexpr int STAGE_BYTES = 2 * TK * ROW;        // K tile + V tile
   static constexpr int SMEM = STAGES * STAGE_BYTES;
+  // co-resident CTAs per SM the ring sizes are chosen for (register cap)
+  static constexpr int MINB = ATT_CW >= 8 ? 1 : HD < 128 ? 4 : 3;
+  // two keys per lane group and warp-step (one softmax rescale for both):
+  // only where a tile holds >= 2 steps per warp without costing registers --
+  // head_dim 64 (C2 16 rows 453.5 -> 446.7 us per iteration); at 96 / 256 it
+  // needs 16 KB tiles and spills or loses a CTA per SM (C4 +5 %, C3 +1.3 %)
+  static constexpr bool PAIR = HD <= 64;
 };
 
 FL_DEV uint32_t smem_addr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -141,7 +159,7 @@ FL_DEV void widen16(const uint4& raw, float* out) {
 }
 
 template <typename T, int HD>
-__global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
+__global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS, AttnCfg<T, HD>::MINB) k_attn_tma(
     const T* __restrict__ q, const fl_row* __restrict__ rows, const int32_t* __restrict__ row_ctx,
     int M, int Hl, const T* __restrict__ kv_layer, int S, T* __restrict__ out,
     float* __restrict__ ws_o, float* __restrict__ ws_ml, int max_splits, int keys_per_split,
@@ -337,6 +355,68 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
       mbar_wait_(&full[st], ph);
       const uint8_t* Ks = smem + st * Cfg::STAGE_BYTES;
       const uint8_t* Vs = Ks + TK * Cfg::ROW;
+      if constexpr (Cfg::PAIR) {
+      // two keys per lane group and step, one online-softmax rescale for
+      // both: half the exp / acc-rescale chain per key
+      for (int kb = warp * KPW; kb < nk; kb += 2 * CW * KPW) {
+        const int ka = kb + kw, kc = ka + CW * KPW;
+        const bool va = ka < nk, vc = kc < nk;     // vc implies va
+        float2 a0 = make_float2(0.f, 0.f), a1 = a0, c0 = a0, c1 = a0;
+#pragma unroll
+        for (int p = 0; p < PER; ++p) {
+          const int vi = g + p * G;
+          if (vi < NV) {
+            float kf[VEC], kg[VEC];
+            if (va) widen16<T>(*reinterpret_cast<const uint4*>(Ks + ka * Cfg::ROW + vi * 16), kf);
+            if (vc) widen16<T>(*reinterpret_cast<const uint4*>(Ks + kc * Cfg::ROW + vi * 16), kg);
+#pragma unroll
+            for (int j = 0; j < VEC; j += 2) {
+              const float2 q2 = make_float2(qv[p][j], qv[p][j + 1]);
+              if (va) {
+                if ((j >> 1) & 1) a1 = __ffma2_rn(q2, make_float2(kf[j], kf[j + 1]), a1);
+                else a0 = __ffma2_rn(q2, make_float2(kf[j], kf[j + 1]), a0);
+              }
+              if (vc) {
+                if ((j >> 1) & 1) c1 = __ffma2_rn(q2, make_float2(kg[j], kg[j + 1]), c1);
+                else c0 = __ffma2_rn(q2, make_float2(kg[j], kg[j + 1]), c0);
+              }
+            }
+          }
+        }
+        float da = (a0.x + a0.y) + (a1.x + a1.y), dc = (c0.x + c0.y) + (c1.x + c1.y);
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) {
+          da += __shfl_xor_sync(0xffffffffu, da, o);
+          dc += __shfl_xor_sync(0xffffffffu, dc, o);
+        }
+        if (va) {
+          const float m_new = fmaxf(m, vc ? fmaxf(da, dc) : da);
+          const float c = __expf(m - m_new);
+          const float pa = __expf(da - m_new);
+          const float pc = vc ? __expf(dc - m_new) : 0.f;
+          l = l * c + (pa + pc);
+          m = m_new;
+          const float2 pa2 = make_float2(pa, pa), pc2 = make_float2(pc, pc), cc = make_float2(c, c);
+#pragma unroll
+          for (int p = 0; p < PER; ++p) {
+            const int vi = g + p * G;
+            if (vi < NV) {
+              float vf[VEC], vg[VEC];
+              widen16<T>(*reinterpret_cast<const uint4*>(Vs + ka * Cfg::ROW + vi * 16), vf);
+              if (vc) widen16<T>(*reinterpret_cast<const uint4*>(Vs + kc * Cfg::ROW + vi * 16), vg);
+#pragma unroll
+              for (int j = 0; j < VEC; j += 2) {
+                float2 a2 = __ffma2_rn(pa2, make_float2(vf[j], vf[j + 1]),
+                                       __fmul2_rn(make_float2(acc[p][j], acc[p][j + 1]), cc));
+                if (vc) a2 = __ffma2_rn(pc2, make_float2(vg[j], vg[j + 1]), a2);
+                acc[p][j] = a2.x;
+                acc[p][j + 1] = a2.y;
+              }
+            }
+          }
+        }
+      }
+      } else {
 #pragma unroll 2
       for (int kb = warp * KPW; kb < nk; kb += CW * KPW) {
         const int k = kb + kw;
@@ -388,6 +468,7 @@ __global__ void __launch_bounds__(AttnCfg<T, HD>::THREADS) k_attn_tma(
             }
           }
         }
+      }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive_(&empty[st]);
@@ -496,17 +577,19 @@ static int attn_launch(const void* q, const fl_row* rows, const int32_t* row_ctx
                        const int4* meta, int ldo, cudaStream_t s, unsigned* ctr, unsigned* next_ctr,
                        unsigned* pre, int pre_mode) {
   using Cfg = AttnCfg<T, HD>;
-  static int num_sms = 0;
+  static int num_sms = 0, per_sm = 0;
   if (!num_sms) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(k_attn_tma<T, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    // co-resident CTAs per SM (smem-limited: 2 with 96 KB rings)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_attn_tma<T, HD>, Cfg::THREADS, Cfg::SMEM);
+    if (per_sm < 1) per_sm = 1;
   }
   const int ms = attn_max_splits(S);           // workspace stride (CHUNK-sized splits)
   const int splits = (S + kps - 1) / kps;
   const int items = M * Hl * splits;
-  const int per_sm = ATT_CW >= 8 ? 1 : 2;
   const int grid = items < per_sm * num_sms ? items : per_sm * num_sms;
   launch_k(k_attn_tma<T, HD>, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM, s, 1, (const T*)q, rows,
            row_ctx, M, Hl, (const T*)kv_layer, S, (T*)out, ws_o, ws_ml, ms, kps, splits, meta, ldo, ctr,
