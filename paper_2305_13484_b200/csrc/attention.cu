@@ -59,10 +59,13 @@ template <int X> struct NextPow2 {
 #ifndef ATT_SPLIT_BELOW
 #define ATT_SPLIT_BELOW 148
 #endif
+#ifndef ATT_SPLIT_TARGET
+#define ATT_SPLIT_TARGET (2 * 148)
+#endif
 int attn_keys_per_split(int row_heads, int S) {
   const int full = attn_max_splits(S);
   int splits = 1;
-  if (row_heads < ATT_SPLIT_BELOW) splits = (2 * 148 + row_heads - 1) / row_heads;
+  if (row_heads < ATT_SPLIT_BELOW) splits = (ATT_SPLIT_TARGET + row_heads - 1) / row_heads;
   if (splits > full) splits = full;
   const int keys = (S + splits - 1) / splits;
   return (keys + ATT_CHUNK - 1) / ATT_CHUNK * ATT_CHUNK;
