@@ -531,13 +531,14 @@ int enqueue_step(fl_handle* h, int n_rows, int n_dec, bool want_logits, cudaStre
     const void* const* W = m.layers + (size_t)l * FL_W_LAYER_COUNT;
     void* kvl = kv + kv_layer_elems * es * l;
     // K2 + K3
-    fl::launch_layernorm(h->x, W[FL_W_LN1_G], W[FL_W_LN1_B], h->h, n_rows, d, m.ln_eps, dt, s);
     // MLP input: GPT-2 = LN2 of the updated residual; GPT-J = LN1 output;
-    // NeoX = LN2 of the residual *before* the attention update.
-    if (m.family == FL_FAMILY_NEOX) {
-      fl::launch_layernorm(h->x, W[FL_W_LN2_G], W[FL_W_LN2_B], h->h2, n_rows, d, m.ln_eps, dt, s);
-      fl::g_launches += 1;
-    }
+    // NeoX = LN2 of the residual *before* the attention update (both
+    // LayerNorms of x in one launch: one kernel less on the layer's chain)
+    if (m.family == FL_FAMILY_NEOX)
+      fl::launch_layernorm2(h->x, W[FL_W_LN1_G], W[FL_W_LN1_B], h->h, W[FL_W_LN2_G], W[FL_W_LN2_B], h->h2,
+                            n_rows, d, m.ln_eps, dt, s);
+    else
+      fl::launch_layernorm(h->x, W[FL_W_LN1_G], W[FL_W_LN1_B], h->h, n_rows, d, m.ln_eps, dt, s);
     const void* mlp_in = m.family == FL_FAMILY_NEOX ? h->h2 : h->h;
     const bool merged_in = h->merged_in && n_rows <= h->merged_in_max_rows;
     if (merged_in) {

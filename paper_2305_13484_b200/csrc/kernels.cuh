@@ -52,6 +52,9 @@ void launch_embed(const fl_row* rows, int n_rows, int n_dec, const int32_t* req_
 // out(T)[M, d] = LN(x[M, d]) * g + b
 void launch_layernorm(const float* x, const void* g, const void* b, void* out, int M, int d,
                       float eps, int dtype, cudaStream_t s);
+// two LayerNorms of the same rows in one launch (gridDim.y = 2)
+void launch_layernorm2(const float* x, const void* g, const void* b, void* out, const void* g2,
+                       const void* b2, void* out2, int M, int d, float eps, int dtype, cudaStream_t s);
 
 // x += y + b1 (+ b2)   (after a tensor-parallel all-reduce of y)
 void launch_add_partial(float* x, const float* y, const void* b1, const void* b2, int M, int d,

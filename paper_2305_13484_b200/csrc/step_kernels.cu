@@ -76,8 +76,16 @@ template <typename T, int PER>
 __global__ void __launch_bounds__(256) k_layernorm(const float* __restrict__ x,
                                                    const T* __restrict__ g,
                                                    const T* __restrict__ b, T* __restrict__ out,
-                                                   int d, float eps) {
+                                                   int d, float eps, const T* __restrict__ g2,
+                                                   const T* __restrict__ b2, T* __restrict__ out2) {
   pdl_trigger();
+  // gridDim.y == 2: a second (gamma, beta, out) of the same rows (NeoX's LN1
+  // and LN2 of one residual in one launch)
+  if (blockIdx.y) {
+    g = g2;
+    b = b2;
+    out = out2;
+  }
   // gamma / beta are weights (never written by a predecessor): load them
   // before the grid dependency wait, off the critical path
   float gv[PER * 4], bv[PER * 4];
@@ -160,19 +168,26 @@ __global__ void __launch_bounds__(256) k_layernorm(const float* __restrict__ x,
 
 template <typename T>
 static void ln_dispatch(const float* x, const void* g, const void* b, void* out, int M, int d,
-                        float eps, cudaStream_t s) {
+                        float eps, cudaStream_t s, const void* g2 = nullptr, const void* b2 = nullptr,
+                        void* out2 = nullptr) {
   const int per = (d + 1023) / 1024;  // float4 chunks per thread at 256 threads
   const T* G = (const T*)g;
   const T* B = (const T*)b;
   T* O = (T*)out;
+  const T* G2 = (const T*)g2;
+  const T* B2 = (const T*)b2;
+  T* O2 = (T*)out2;
+  const dim3 grid(M, out2 ? 2 : 1);
+#define FL_LN(P) launch_k(k_layernorm<T, P>, grid, dim3(256), 0, s, 1, x, G, B, O, d, eps, G2, B2, O2)
   switch (per) {
-    case 1: launch_k(k_layernorm<T, 1>, dim3(M), dim3(256), 0, s, 1, x, G, B, O, d, eps); break;
-    case 2: launch_k(k_layernorm<T, 2>, dim3(M), dim3(256), 0, s, 1, x, G, B, O, d, eps); break;
-    case 3: launch_k(k_layernorm<T, 3>, dim3(M), dim3(256), 0, s, 1, x, G, B, O, d, eps); break;
-    case 4: launch_k(k_layernorm<T, 4>, dim3(M), dim3(256), 0, s, 1, x, G, B, O, d, eps); break;
-    case 5: case 6: launch_k(k_layernorm<T, 6>, dim3(M), dim3(256), 0, s, 1, x, G, B, O, d, eps); break;
-    default: launch_k(k_layernorm<T, 8>, dim3(M), dim3(256), 0, s, 1, x, G, B, O, d, eps); break;
+    case 1: FL_LN(1); break;
+    case 2: FL_LN(2); break;
+    case 3: FL_LN(3); break;
+    case 4: FL_LN(4); break;
+    case 5: case 6: FL_LN(6); break;
+    default: FL_LN(8); break;
   }
+#undef FL_LN
 }
 
 void launch_layernorm(const float* x, const void* g, const void* b, void* out, int M, int d,
@@ -180,6 +195,13 @@ void launch_layernorm(const float* x, const void* g, const void* b, void* out, i
   if (M <= 0) return;
   if (dtype == FL_DTYPE_BF16) ln_dispatch<bf16>(x, g, b, out, M, d, eps, s);
   else ln_dispatch<float>(x, g, b, out, M, d, eps, s);
+}
+
+void launch_layernorm2(const float* x, const void* g, const void* b, void* out, const void* g2,
+                       const void* b2, void* out2, int M, int d, float eps, int dtype, cudaStream_t s) {
+  if (M <= 0) return;
+  if (dtype == FL_DTYPE_BF16) ln_dispatch<bf16>(x, g, b, out, M, d, eps, s, g2, b2, out2);
+  else ln_dispatch<float>(x, g, b, out, M, d, eps, s, g2, b2, out2);
 }
 
 // ---------------------------------------------------------------- residual add
